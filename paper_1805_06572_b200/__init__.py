@@ -1,1 +1,53 @@
-"""B200-native FCA / FastFCA EM (package init placeholder)."""
+"""B200-native FCA / FastFCA EM (arXiv 1805.06572), drop-in for the hot path
+of the reference package ``fastfca`` 0.1.0.
+
+Two-source multichannel separation with full-rank spatial covariances:
+``fastfca_run`` (joint-diagonalisation EM) and ``fca_run`` (frame-wise EM)
+run entirely on the GPU through hand-written sm_100a CUDA kernels in
+``lib/libfastfca_b200.so`` (C ABI: ``include/fastfca_b200.h``). Names,
+signatures, layouts, return types and exceptions follow the reference
+(``pkg/src/fastfca/__init__.py:10-77``) for everything on the EM path; the
+STFT front end, simulator, metrics and CLI are out of scope.
+"""
+
+from .conventional import e_step, fca_run, log_likelihood, m_step
+from .errors import (BackendUnavailableError, ConfigurationError, DefinitenessError,
+                     FastFcaError, NonHermitianError, SingularMatrixError,
+                     SingularMixtureError)
+from .fast import (fast_e_step, fast_m_step_S, fast_m_step_v, fastfca_run, propagate_pencil,
+                   transform_observations)
+from .initializers import init_random
+from .pencil import PencilDecomposition, gevd_hpd, hermitian_eig, solve_hermitian_system
+from .types import OpCounts, PosteriorMoments, SeparationResult, SpatialModel, SpectrogramTensor
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BackendUnavailableError",
+    "ConfigurationError",
+    "DefinitenessError",
+    "FastFcaError",
+    "NonHermitianError",
+    "OpCounts",
+    "PencilDecomposition",
+    "PosteriorMoments",
+    "SeparationResult",
+    "SingularMatrixError",
+    "SingularMixtureError",
+    "SpatialModel",
+    "SpectrogramTensor",
+    "e_step",
+    "fast_e_step",
+    "fast_m_step_S",
+    "fast_m_step_v",
+    "fastfca_run",
+    "fca_run",
+    "gevd_hpd",
+    "hermitian_eig",
+    "init_random",
+    "log_likelihood",
+    "m_step",
+    "propagate_pencil",
+    "solve_hermitian_system",
+    "transform_observations",
+]

@@ -1,0 +1,99 @@
+"""Build libfastfca_b200.so in-tree (sm_100a) with nvcc.
+
+    python -m paper_1805_06572_b200.build [--verbose-ptxas] [--jobs N]
+
+Each ``csrc/*.cu`` is compiled to an object in ``build/`` (parallel), then
+linked into ``paper_1805_06572_b200/lib/libfastfca_b200.so``. Objects are
+rebuilt only when a source or header is newer.
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+REPO = PKG.parent
+CSRC = PKG / "csrc"
+INCLUDE = REPO / "include"
+BUILD = REPO / "build" / "csrc"
+LIB = PKG / "lib" / "libfastfca_b200.so"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [
+    "-O3",
+    "-lineinfo",
+    "-std=c++17",
+    "-Xcompiler",
+    "-fPIC",
+    "-Xcompiler",
+    "-O2",
+    "--expt-relaxed-constexpr",
+    "-Wno-deprecated-gpu-targets",
+]
+
+
+def nvcc():
+    cand = os.environ.get("NVCC") or "/usr/local/cuda/bin/nvcc"
+    return cand if Path(cand).exists() else "nvcc"
+
+
+def _deps():
+    return [*CSRC.glob("*.cuh"), INCLUDE / "fastfca_b200.h"]
+
+
+def _needs(obj: Path, src: Path) -> bool:
+    if not obj.exists():
+        return True
+    t = obj.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in [src, *_deps()])
+
+
+def compile_one(src: Path, verbose_ptxas=False) -> Path:
+    obj = BUILD / (src.stem + ".o")
+    if not _needs(obj, src):
+        return obj
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, f"-I{INCLUDE}", "-c", str(src), "-o", str(obj)]
+    if verbose_ptxas:
+        cmd.insert(1, "-Xptxas=-v")
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src.name}:\n{res.stderr}")
+    if verbose_ptxas and res.stderr:
+        (BUILD / (src.stem + ".ptxas.txt")).write_text(res.stderr)
+    return obj
+
+
+def build(verbose_ptxas=False, jobs=None) -> Path:
+    BUILD.mkdir(parents=True, exist_ok=True)
+    LIB.parent.mkdir(parents=True, exist_ok=True)
+    sources = sorted(CSRC.glob("*.cu"))
+    jobs = jobs or min(len(sources), os.cpu_count() or 4)
+    with ThreadPoolExecutor(jobs) as ex:
+        objs = list(ex.map(lambda s: compile_one(s, verbose_ptxas), sources))
+    if LIB.exists() and all(LIB.stat().st_mtime >= o.stat().st_mtime for o in objs):
+        return LIB
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed:\n{res.stderr}")
+    os.replace(tmp, LIB)
+    return LIB
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--verbose-ptxas", action="store_true")
+    ap.add_argument("--jobs", type=int, default=None)
+    args = ap.parse_args(argv)
+    lib = build(args.verbose_ptxas, args.jobs)
+    print(lib)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,444 @@
+// extern "C" entry points: the device-resident EM drivers (the native runtime
+// of the hot path) and the per-bin batched routines.
+//
+// ffca_fastfca_run mirrors fastfca_run (reference fast.py:156-260) and
+// ffca_fca_run mirrors fca_run (conventional.py:104-164): same iteration
+// structure, same likelihood / history / image semantics, but every step is
+// a kernel on one stream and nothing returns to the host inside the loop.
+#include <cstring>
+
+#include "ffca_internal.cuh"
+
+namespace ffca {
+cudaError_t launch_gevd_batch(const double2* Phi, const double2* Psi, double* lam, double2* P,
+                              const double2* Pprev, int64_t B, int I, int check,
+                              ffca_status_dev* st, cudaStream_t s);
+cudaError_t launch_cholinv(const double2* S, double2* Sinv, int64_t B, int I, ffca_status_dev* st,
+                           cudaStream_t s);
+cudaError_t launch_regularize(const double2* S, double2* out, int64_t B, int I, cudaStream_t s);
+cudaError_t launch_reg_transformed(const double2* S, const double2* gram, double2* out,
+                                   int64_t B, int I, cudaStream_t s);
+cudaError_t launch_inverse_h(const double2* P, double2* W, double* logdet2, int64_t B, int I,
+                             ffca_status_dev* st, cudaStream_t s);
+cudaError_t launch_apply_w(const double2* mu_t, const double2* W, double2* out, int64_t Src,
+                           int64_t N, int64_t F, int I, cudaStream_t s);
+cudaError_t launch_conj_w(const double2* S, const double2* W, double2* out, int64_t Src,
+                          int64_t F, int I, cudaStream_t s);
+cudaError_t launch_init_powers(const void* y, void* v, double* floor, int64_t M, int64_t N,
+                               int64_t F, int I, int dtype, cudaStream_t s);
+}  // namespace ffca
+
+using namespace ffca;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Carve {
+  char* base;
+  size_t off = 0;
+  explicit Carve(void* b) : base((char*)b) {}
+  template <typename T>
+  T* take(size_t count) {
+    T* p = base ? (T*)(base + off) : nullptr;
+    off += align_up(count * sizeof(T));
+    return p;
+  }
+};
+
+struct FastWs {
+  ffca_status_dev* st;
+  double2 *P, *W;
+  double *lam, *logdet2, *Spart, *llbin, *llg;
+  int64_t chunk_frames;
+  int nchunk;
+  size_t bytes;
+};
+
+void chunking(int64_t G, int64_t N, int64_t cf_req, int64_t* cf, int* nc) {
+  if (cf_req > 0) {
+    *cf = cf_req < N ? cf_req : N;
+    *nc = (int)((N + *cf - 1) / *cf);
+  } else {
+    plan_chunks(G, N, cf, nc);
+  }
+}
+
+FastWs carve_fast(void* base, int64_t M, int64_t N, int64_t F, int I, int L, unsigned flags,
+                  int64_t cf_req) {
+  FastWs w{};
+  const int64_t G = M * F;
+  chunking(G, N, cf_req, &w.chunk_frames, &w.nchunk);
+  Carve c(base);
+  w.st = c.take<ffca_status_dev>(1);
+  w.P = c.take<double2>(G * I * I);
+  w.W = c.take<double2>(G * I * I);
+  w.lam = c.take<double>(G * I);
+  w.logdet2 = c.take<double>(G);
+  w.Spart = c.take<double>((size_t)w.nchunk * 2 * I * I * G);
+  const bool ll = flags & FFCA_FLAG_LIKELIHOOD;
+  w.llbin = ll ? c.take<double>((size_t)w.nchunk * G) : nullptr;
+  w.llg = ll ? c.take<double>((size_t)(L + 1) * G) : nullptr;
+  w.bytes = c.off;
+  return w;
+}
+
+struct FcaWs {
+  ffca_status_dev* st;
+  double *Sp, *Spart, *llbin, *llg;
+  int64_t chunk_frames;
+  int nchunk;
+  size_t bytes;
+};
+
+FcaWs carve_fca(void* base, int64_t M, int64_t N, int64_t F, int I, int L, unsigned flags,
+                int64_t cf_req) {
+  FcaWs w{};
+  const int64_t G = M * F;
+  chunking(G, N, cf_req, &w.chunk_frames, &w.nchunk);
+  Carve c(base);
+  w.st = c.take<ffca_status_dev>(1);
+  w.Sp = c.take<double>((size_t)4 * I * I * G);
+  w.Spart = c.take<double>((size_t)w.nchunk * 2 * I * I * G);
+  const bool ll = flags & FFCA_FLAG_LIKELIHOOD;
+  w.llbin = ll ? c.take<double>((size_t)w.nchunk * G) : nullptr;
+  w.llg = ll ? c.take<double>((size_t)(L + 1) * G) : nullptr;
+  w.bytes = c.off;
+  return w;
+}
+
+int check_args(const ffca_run_args* a) {
+  if (!a || a->M < 1 || a->N < 1 || a->F < 1 || a->I < 1 || a->I > kMaxOrder ||
+      a->iterations < 0 || a->iterations > 65000 || a->chunk_frames < 0 || !a->y || !a->v || !a->S0 || !a->v_floor ||
+      !a->S_out || !a->workspace)
+    return FFCA_ERR_INVALID;
+  if (a->dtype != FFCA_C128 && a->dtype != FFCA_C64) return FFCA_ERR_INVALID;
+  if ((a->flags & FFCA_FLAG_IMAGES) && !a->images) return FFCA_ERR_INVALID;
+  if ((a->flags & FFCA_FLAG_LIKELIHOOD) && !a->loglik) return FFCA_ERR_INVALID;
+  if (((size_t)a->workspace) % kAlign) return FFCA_ERR_INVALID;
+  return FFCA_OK;
+}
+
+inline int cu(cudaError_t e) { return e == cudaSuccess ? FFCA_OK : FFCA_ERR_CUDA; }
+#define FFCA_TRY(expr)                 \
+  do {                                 \
+    int _rc = cu(expr);                \
+    if (_rc != FFCA_OK) return _rc;    \
+  } while (0)
+
+inline size_t real_size(int dtype) { return dtype == FFCA_C64 ? 4 : 8; }
+
+void decode(const ffca_status_dev& d, ffca_status* out) {
+  if (d.first == ~0ull) {
+    out->code = FFCA_OK;
+    out->iteration = 0;
+    out->index = -1;
+    out->value = 0.0;
+    return;
+  }
+  out->iteration = (int)((d.first >> 48) & 0xffff) - 1;
+  out->code = (int)((d.first >> 44) & 0xf);
+  out->index = (long long)(d.first & ((1ull << 44) - 1));
+  out->value = d.value;
+}
+
+__global__ void status_init_kernel(ffca_status_dev* st) {
+  st->first = ~0ull;
+  st->value = 1e308;
+}
+
+int reset_status(ffca_status_dev* st, cudaStream_t s) {
+  status_init_kernel<<<1, 1, 0, s>>>(st);
+  return cu(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ffca_version(void) { return "fastfca_b200 0.1.0 (sm_100a)"; }
+
+int ffca_device_arch(void) { return 100; }
+
+int ffca_plan_chunks(int64_t G, int64_t N, int64_t* chunk_frames, int* nchunk) {
+  if (G < 1 || N < 1 || !chunk_frames || !nchunk) return FFCA_ERR_INVALID;
+  plan_chunks(G, N, chunk_frames, nchunk);
+  return FFCA_OK;
+}
+
+size_t ffca_fastfca_workspace_size(int64_t M, int64_t N, int64_t F, int I, int iterations,
+                                   unsigned flags, int64_t chunk_frames) {
+  if (M < 1 || N < 1 || F < 1 || I < 1 || I > kMaxOrder || iterations < 0) return 0;
+  return carve_fast(nullptr, M, N, F, I, iterations, flags, chunk_frames).bytes;
+}
+
+size_t ffca_fca_workspace_size(int64_t M, int64_t N, int64_t F, int I, int iterations,
+                               unsigned flags, int64_t chunk_frames) {
+  if (M < 1 || N < 1 || F < 1 || I < 1 || I > kMaxOrder || iterations < 0) return 0;
+  return carve_fca(nullptr, M, N, F, I, iterations, flags, chunk_frames).bytes;
+}
+
+int ffca_fastfca_run(const ffca_run_args* a, void* stream) {
+  int rc = check_args(a);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t M = a->M, N = a->N, F = a->F, G = M * F;
+  const int I = a->I, L = a->iterations;
+  const unsigned fl = a->flags;
+  FastWs w = carve_fast(a->workspace, M, N, F, I, L, fl, a->chunk_frames);
+  if (w.bytes > a->workspace_bytes) return FFCA_ERR_INVALID;
+  const bool ll = fl & FFCA_FLAG_LIKELIHOOD;
+  const bool hist = (fl & FFCA_FLAG_HISTORY) != 0;
+  const size_t Sslice = (size_t)M * 2 * F * I * I;  // complex entries per S snapshot
+  const size_t vslice = (size_t)M * 2 * N * F;      // real entries per v snapshot
+  cudaEvent_t* ev = (cudaEvent_t*)a->iter_events;
+
+  if ((rc = reset_status(w.st, s))) return rc;
+  FFCA_TRY(launch_initial_pencil((const double2*)a->S0, w.P, w.W, w.lam, w.logdet2, G, F, I,
+                                 w.st, s));
+  FastIterParams p{};
+  p.y = a->y;
+  p.v = a->v;
+  p.P = w.P;
+  p.W = w.W;
+  p.lam = w.lam;
+  p.floor = a->v_floor;
+  p.Spart = w.Spart;
+  p.llbin = ll ? w.llbin : nullptr;
+  p.M = M;
+  p.N = N;
+  p.F = F;
+  p.G = G;
+  p.chunk_frames = w.chunk_frames;
+  p.nchunk = w.nchunk;
+  p.st = w.st;
+
+  if (L == 0) {
+    if (ev) FFCA_TRY(cudaEventRecord(ev[0], s));
+    p.update = 0;
+    p.mu_out = (fl & FFCA_FLAG_IMAGES) ? a->images : nullptr;
+    p.mu_back = 1;
+    p.iter = 0;
+    if (p.mu_out || p.llbin) FFCA_TRY(launch_fast_em(p, I, a->dtype, s));
+    if (ll) FFCA_TRY(launch_ll_collect(w.llbin, w.nchunk, w.logdet2, N, G, w.llg, s));
+    FFCA_TRY(cudaMemcpyAsync(a->S_out, a->S0, Sslice * sizeof(double2),
+                             cudaMemcpyDeviceToDevice, s));
+  } else {
+    for (int l = 0; l < L; ++l) {
+      if (ev) FFCA_TRY(cudaEventRecord(ev[l], s));
+      p.update = 1;
+      const bool last = (l == L - 1);
+      p.mu_out = (last && (fl & FFCA_FLAG_IMAGES)) ? a->images : nullptr;
+      p.mu_back = 1;
+      p.iter = l + 1;
+      FFCA_TRY(launch_fast_em(p, I, a->dtype, s));
+      if (hist && a->v_hist)
+        FFCA_TRY(cudaMemcpyAsync((char*)a->v_hist + (size_t)l * vslice * real_size(a->dtype),
+                                 a->v, vslice * real_size(a->dtype), cudaMemcpyDeviceToDevice,
+                                 s));
+      PencilParams q{};
+      q.Spart = w.Spart;
+      q.nchunk = w.nchunk;
+      q.N = N;
+      q.G = G;
+      q.F = F;
+      q.P = w.P;
+      q.W = w.W;
+      q.lam = w.lam;
+      q.logdet2 = w.logdet2;
+      q.S_model = (double2*)a->S_out;
+      q.S_hist = (hist && a->S_hist) ? (double2*)a->S_hist + (size_t)l * Sslice : nullptr;
+      q.llbin = ll ? w.llbin : nullptr;
+      q.llg = ll ? w.llg + (size_t)l * G : nullptr;
+      q.st = w.st;
+      q.iter = l + 1;
+      FFCA_TRY(launch_pencil_update(q, I, s));
+    }
+    if (ev) FFCA_TRY(cudaEventRecord(ev[L], s));
+    if (ll) {
+      p.update = 0;
+      p.mu_out = nullptr;
+      p.iter = L + 1;
+      FFCA_TRY(launch_fast_em(p, I, a->dtype, s));
+      FFCA_TRY(launch_ll_collect(w.llbin, w.nchunk, w.logdet2, N, G, w.llg + (size_t)L * G, s));
+    }
+  }
+  if (ll) FFCA_TRY(launch_ll_reduce(w.llg, M, F, N, I, L + 1, L + 1, a->loglik, s));
+  return FFCA_OK;
+}
+
+int ffca_fca_run(const ffca_run_args* a, void* stream) {
+  int rc = check_args(a);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t M = a->M, N = a->N, F = a->F, G = M * F;
+  const int I = a->I, L = a->iterations;
+  const unsigned fl = a->flags;
+  FcaWs w = carve_fca(a->workspace, M, N, F, I, L, fl, a->chunk_frames);
+  if (w.bytes > a->workspace_bytes) return FFCA_ERR_INVALID;
+  const bool ll = fl & FFCA_FLAG_LIKELIHOOD;
+  const bool hist = (fl & FFCA_FLAG_HISTORY) != 0;
+  const size_t Sslice = (size_t)M * 2 * F * I * I;
+  const size_t vslice = (size_t)M * 2 * N * F;
+  cudaEvent_t* ev = (cudaEvent_t*)a->iter_events;
+
+  if ((rc = reset_status(w.st, s))) return rc;
+  FFCA_TRY(launch_fca_prepare((const double2*)a->S0, w.Sp, G, F, I, w.st, 0, s));
+  FcaIterParams p{};
+  p.y = a->y;
+  p.v = a->v;
+  p.Sp = w.Sp;
+  p.floor = a->v_floor;
+  p.Spart = w.Spart;
+  p.llbin = ll ? w.llbin : nullptr;
+  p.M = M;
+  p.N = N;
+  p.F = F;
+  p.G = G;
+  p.chunk_frames = w.chunk_frames;
+  p.nchunk = w.nchunk;
+  p.st = w.st;
+  if (L == 0) {
+    if (ev) FFCA_TRY(cudaEventRecord(ev[0], s));
+    p.update = 0;
+    p.mu_out = (fl & FFCA_FLAG_IMAGES) ? a->images : nullptr;
+    p.iter = 0;
+    if (p.mu_out || p.llbin) FFCA_TRY(launch_fca_em(p, I, a->dtype, s));
+    if (ll) FFCA_TRY(launch_ll_collect(w.llbin, w.nchunk, nullptr, N, G, w.llg, s));
+    FFCA_TRY(cudaMemcpyAsync(a->S_out, a->S0, Sslice * sizeof(double2),
+                             cudaMemcpyDeviceToDevice, s));
+  } else {
+    for (int l = 0; l < L; ++l) {
+      if (ev) FFCA_TRY(cudaEventRecord(ev[l], s));
+      p.update = 1;
+      const bool last = (l == L - 1);
+      p.mu_out = (last && (fl & FFCA_FLAG_IMAGES)) ? a->images : nullptr;
+      p.iter = l + 1;
+      FFCA_TRY(launch_fca_em(p, I, a->dtype, s));
+      if (hist && a->v_hist)
+        FFCA_TRY(cudaMemcpyAsync((char*)a->v_hist + (size_t)l * vslice * real_size(a->dtype),
+                                 a->v, vslice * real_size(a->dtype), cudaMemcpyDeviceToDevice,
+                                 s));
+      FFCA_TRY(launch_fca_finish(
+          w.Spart, w.nchunk, N, G, F, w.Sp, (double2*)a->S_out,
+          (hist && a->S_hist) ? (double2*)a->S_hist + (size_t)l * Sslice : nullptr,
+          ll ? w.llbin : nullptr, ll ? w.llg + (size_t)l * G : nullptr, I, w.st, l + 1, s));
+    }
+    if (ev) FFCA_TRY(cudaEventRecord(ev[L], s));
+    if (ll) {
+      p.update = 0;
+      p.mu_out = nullptr;
+      p.iter = L + 1;
+      FFCA_TRY(launch_fca_em(p, I, a->dtype, s));
+      FFCA_TRY(launch_ll_collect(w.llbin, w.nchunk, nullptr, N, G, w.llg + (size_t)L * G, s));
+    }
+  }
+  if (ll) FFCA_TRY(launch_ll_reduce(w.llg, M, F, N, I, L + 1, L + 1, a->loglik, s));
+  return FFCA_OK;
+}
+
+int ffca_run_status(const void* workspace, void* stream, ffca_status* out) {
+  if (!workspace || !out) return FFCA_ERR_INVALID;
+  return ffca_status_read((const ffca_status_dev*)workspace, stream, out);
+}
+
+int ffca_status_reset(ffca_status_dev* st, void* stream) {
+  if (!st) return FFCA_ERR_INVALID;
+  return reset_status(st, (cudaStream_t)stream);
+}
+
+int ffca_status_read(const ffca_status_dev* st, void* stream, ffca_status* out) {
+  if (!st || !out) return FFCA_ERR_INVALID;
+  ffca_status_dev h;
+  cudaStream_t s = (cudaStream_t)stream;
+  FFCA_TRY(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
+  FFCA_TRY(cudaStreamSynchronize(s));
+  decode(h, out);
+  return FFCA_OK;
+}
+
+// ---- per-bin batched routines ---------------------------------------------
+int ffca_gevd_hpd(const double* Phi, const double* Psi, double* lam, double* P, int64_t batch,
+                  int D, int check_hermitian, ffca_status_dev* st, void* stream) {
+  if (!Phi || !Psi || !lam || !P || batch < 0 || D < 1 || D > kMaxOrder) return FFCA_ERR_INVALID;
+  if (batch == 0) return FFCA_OK;
+  return cu(launch_gevd_batch((const double2*)Phi, (const double2*)Psi, lam, (double2*)P, nullptr,
+                              batch, D, check_hermitian, st, (cudaStream_t)stream));
+}
+
+int ffca_propagate_pencil(const double* St1, const double* St2, const double* P_prev,
+                          double* P_next, double* lam, int64_t batch, int D,
+                          ffca_status_dev* st, void* stream) {
+  if (!St1 || !St2 || !P_prev || !P_next || !lam || batch < 0 || D < 1 || D > kMaxOrder)
+    return FFCA_ERR_INVALID;
+  if (batch == 0) return FFCA_OK;
+  return cu(launch_gevd_batch((const double2*)St1, (const double2*)St2, lam, (double2*)P_next,
+                              (const double2*)P_prev, batch, D, 1, st, (cudaStream_t)stream));
+}
+
+int ffca_cholesky_inverse(const double* S, double* Sinv, int64_t batch, int D,
+                          ffca_status_dev* st, void* stream) {
+  if (!S || !Sinv || batch < 0 || D < 1 || D > kMaxOrder) return FFCA_ERR_INVALID;
+  if (batch == 0) return FFCA_OK;
+  return cu(launch_cholinv((const double2*)S, (double2*)Sinv, batch, D, st,
+                           (cudaStream_t)stream));
+}
+
+int ffca_regularize_covariances(const double* S, double* out, int64_t batch, int D,
+                                void* stream) {
+  if (!S || !out || batch < 0 || D < 1 || D > kMaxOrder) return FFCA_ERR_INVALID;
+  if (batch == 0) return FFCA_OK;
+  return cu(launch_regularize((const double2*)S, (double2*)out, batch, D, (cudaStream_t)stream));
+}
+
+int ffca_regularize_transformed(const double* S_raw, const double* gram, double* out,
+                                int64_t batch, int D, void* stream) {
+  if (!S_raw || !out || batch < 0 || D < 1 || D > kMaxOrder) return FFCA_ERR_INVALID;
+  if (batch == 0) return FFCA_OK;
+  return cu(launch_reg_transformed((const double2*)S_raw, (const double2*)gram, (double2*)out,
+                                   batch, D, (cudaStream_t)stream));
+}
+
+int ffca_logdet2(const double* P, double* out, int64_t batch, int D, void* stream) {
+  if (!P || !out || batch < 0 || D < 1 || D > kMaxOrder) return FFCA_ERR_INVALID;
+  if (batch == 0) return FFCA_OK;
+  return cu(launch_inverse_h((const double2*)P, nullptr, out, batch, D, nullptr,
+                             (cudaStream_t)stream));
+}
+
+int ffca_back_transform_images(const double* mu_t, const double* P, double* out, int64_t Src,
+                               int64_t N, int64_t F, int I, ffca_status_dev* st, void* stream) {
+  if (!mu_t || !P || !out || Src < 0 || N < 0 || F < 1 || I < 1 || I > kMaxOrder)
+    return FFCA_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  double2* W = nullptr;
+  FFCA_TRY(cudaMallocAsync((void**)&W, (size_t)F * I * I * sizeof(double2), s));
+  int rc = cu(launch_inverse_h((const double2*)P, W, nullptr, F, I, st, s));
+  if (rc == FFCA_OK && Src * N > 0)
+    rc = cu(launch_apply_w((const double2*)mu_t, W, (double2*)out, Src, N, F, I, s));
+  cudaFreeAsync(W, s);
+  return rc;
+}
+
+int ffca_back_transform_covariances(const double* S_t, const double* P, double* out,
+                                    int64_t Src, int64_t F, int I, ffca_status_dev* st,
+                                    void* stream) {
+  if (!S_t || !P || !out || Src < 0 || F < 1 || I < 1 || I > kMaxOrder) return FFCA_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  double2* W = nullptr;
+  FFCA_TRY(cudaMallocAsync((void**)&W, (size_t)F * I * I * sizeof(double2), s));
+  int rc = cu(launch_inverse_h((const double2*)P, W, nullptr, F, I, st, s));
+  if (rc == FFCA_OK && Src > 0)
+    rc = cu(launch_conj_w((const double2*)S_t, W, (double2*)out, Src, F, I, s));
+  cudaFreeAsync(W, s);
+  return rc;
+}
+
+int ffca_init_powers(const void* y, void* v, double* v_floor, int64_t M, int64_t N, int64_t F,
+                     int I, int dtype, void* stream) {
+  if (!y || !v || !v_floor || M < 1 || N < 1 || F < 1 || I < 1) return FFCA_ERR_INVALID;
+  return cu(launch_init_powers(y, v, v_floor, M, N, F, I, dtype, (cudaStream_t)stream));
+}
+
+}  // extern "C"

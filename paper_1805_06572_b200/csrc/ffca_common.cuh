@@ -1,0 +1,469 @@
+// Common device helpers for the B200 FCA / FastFCA EM kernels.
+//
+// Complex numbers are double2 / float2 (x = re, y = im). Small per-bin
+// matrices (order I <= 8) live in per-thread arrays indexed by compile-time
+// constants (every loop over I is unrolled), so for I <= 4 they stay in
+// registers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fastfca_b200.h"
+
+#define FFCA_DEV __device__ __forceinline__
+
+namespace ffca {
+
+constexpr int kMaxOrder = 8;
+constexpr double kLogPi = 1.1447298858494002;  // log(pi)
+constexpr double kCovEps = 1e-9;               // reference modelops.py:9
+constexpr double kDefFloor = 1e-12;            // reference pencil.py:25
+constexpr double kHermRtol = 1e-10;            // reference pencil.py:22
+
+// ---- complex arithmetic --------------------------------------------------
+FFCA_DEV double2 cmk(double re, double im) { return make_double2(re, im); }
+FFCA_DEV double2 cadd(double2 a, double2 b) { return cmk(a.x + b.x, a.y + b.y); }
+FFCA_DEV double2 csub(double2 a, double2 b) { return cmk(a.x - b.x, a.y - b.y); }
+FFCA_DEV double2 cconj(double2 a) { return cmk(a.x, -a.y); }
+FFCA_DEV double2 cscale(double2 a, double s) { return cmk(a.x * s, a.y * s); }
+FFCA_DEV double2 cmul(double2 a, double2 b) {
+  return cmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+FFCA_DEV double2 cmulc(double2 a, double2 b) {
+  return cmk(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+// conj(a) * b
+FFCA_DEV double2 cconjmul(double2 a, double2 b) {
+  return cmk(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+FFCA_DEV double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+FFCA_DEV double2 cdiv(double2 a, double2 b) {
+  // Smith's algorithm
+  if (fabs(b.x) >= fabs(b.y)) {
+    double r = b.y / b.x, d = b.x + b.y * r;
+    return cmk((a.x + a.y * r) / d, (a.y - a.x * r) / d);
+  } else {
+    double r = b.x / b.y, d = b.x * r + b.y;
+    return cmk((a.x * r + a.y) / d, (a.y * r - a.x) / d);
+  }
+}
+FFCA_DEV double2 to_c128(double2 a) { return a; }
+FFCA_DEV double2 to_c128(float2 a) { return cmk((double)a.x, (double)a.y); }
+
+template <typename C>
+struct CplxOf;
+template <>
+struct CplxOf<double> {
+  using type = double2;
+};
+template <>
+struct CplxOf<float> {
+  using type = float2;
+};
+
+template <typename R>
+FFCA_DEV typename CplxOf<R>::type from_c128(double2 a);
+template <>
+FFCA_DEV double2 from_c128<double>(double2 a) {
+  return a;
+}
+template <>
+FFCA_DEV float2 from_c128<float>(double2 a) {
+  return make_float2((float)a.x, (float)a.y);
+}
+
+// ---- packed Hermitian storage ---------------------------------------------
+// I real diagonal entries followed by the strictly-upper entries (row-major
+// a < b) as (re, im) pairs: exactly I*I doubles.
+template <int I>
+struct Herm {
+  static constexpr int NP = I * I;
+  static constexpr int NOFF = I * (I - 1) / 2;
+  FFCA_DEV static constexpr int off(int a, int b) {
+    // index of pair (a, b), a < b, in row-major upper order
+    return a * I - a * (a + 1) / 2 + (b - a - 1);
+  }
+  FFCA_DEV static constexpr int re(int a, int b) { return I + 2 * off(a, b); }
+  FFCA_DEV static constexpr int im(int a, int b) { return I + 2 * off(a, b) + 1; }
+};
+
+template <int I>
+FFCA_DEV void unpack_herm(const double (&p)[I * I], double2 (&A)[I][I]) {
+#pragma unroll
+  for (int a = 0; a < I; ++a) {
+    A[a][a] = cmk(p[a], 0.0);
+#pragma unroll
+    for (int b = a + 1; b < I; ++b) {
+      A[a][b] = cmk(p[Herm<I>::re(a, b)], p[Herm<I>::im(a, b)]);
+      A[b][a] = cconj(A[a][b]);
+    }
+  }
+}
+
+// ---- error reporting -------------------------------------------------------
+// First error wins by (iteration, code, index) order through a 64-bit
+// atomicMin on  iter<<48 | code<<44 | index  (index < 2^44).
+FFCA_DEV void report_error(ffca_status_dev* st, int iter, int code, unsigned long long index) {
+  unsigned long long key = ((unsigned long long)(iter & 0xffff) << 48) |
+                           ((unsigned long long)(code & 0xf) << 44) |
+                           (index & ((1ull << 44) - 1));
+  atomicMin(&st->first, key);
+}
+FFCA_DEV void report_min_value(ffca_status_dev* st, double val) {
+  // running minimum of a double (definiteness: worst minimum eigenvalue)
+  unsigned long long* addr = (unsigned long long*)&st->value;
+  unsigned long long old = *addr, assumed;
+  do {
+    assumed = old;
+    if (!(val < __longlong_as_double((long long)assumed))) break;
+    old = atomicCAS(addr, assumed, (unsigned long long)__double_as_longlong(val));
+  } while (assumed != old);
+}
+
+// ---- small dense routines (order I, compile-time) ---------------------------
+template <int I>
+FFCA_DEV void set_identity(double2 (&A)[I][I]) {
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) A[a][b] = cmk(a == b ? 1.0 : 0.0, 0.0);
+}
+
+// C = A * B
+template <int I>
+FFCA_DEV void matmul(const double2 (&A)[I][I], const double2 (&B)[I][I], double2 (&C)[I][I]) {
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      double2 acc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < I; ++k) {
+        acc.x += A[a][k].x * B[k][b].x - A[a][k].y * B[k][b].y;
+        acc.y += A[a][k].x * B[k][b].y + A[a][k].y * B[k][b].x;
+      }
+      C[a][b] = acc;
+    }
+}
+
+// C = A^H * B
+template <int I>
+FFCA_DEV void matmul_hn(const double2 (&A)[I][I], const double2 (&B)[I][I], double2 (&C)[I][I]) {
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      double2 acc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < I; ++k) {
+        acc.x += A[k][a].x * B[k][b].x + A[k][a].y * B[k][b].y;
+        acc.y += A[k][a].x * B[k][b].y - A[k][a].y * B[k][b].x;
+      }
+      C[a][b] = acc;
+    }
+}
+
+// C = A * B^H
+template <int I>
+FFCA_DEV void matmul_nh(const double2 (&A)[I][I], const double2 (&B)[I][I], double2 (&C)[I][I]) {
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      double2 acc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < I; ++k) {
+        acc.x += A[a][k].x * B[b][k].x + A[a][k].y * B[b][k].y;
+        acc.y += A[a][k].y * B[b][k].x - A[a][k].x * B[b][k].y;
+      }
+      C[a][b] = acc;
+    }
+}
+
+// Cyclic complex Jacobi on a Hermitian matrix (full storage). On exit A is
+// diagonal (eigenvalues on the diagonal, real parts) and V holds the
+// eigenvectors in its columns: A_in = V diag(A_out) V^H.
+template <int I>
+FFCA_DEV void jacobi_herm(double2 (&A)[I][I], double2 (&V)[I][I]) {
+  set_identity<I>(V);
+  if (I == 1) return;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    double off = 0.0, dia = 0.0;
+#pragma unroll
+    for (int p = 0; p < I; ++p) {
+      dia += A[p][p].x * A[p][p].x;
+#pragma unroll
+      for (int q = p + 1; q < I; ++q) off += cabs2(A[p][q]);
+    }
+    if (!(off > 1e-36 * dia)) break;  // converged (also exits on NaN)
+#pragma unroll
+    for (int p = 0; p < I - 1; ++p) {
+#pragma unroll
+      for (int q = p + 1; q < I; ++q) {
+        const double2 apq = A[p][q];
+        const double mag2 = cabs2(apq);
+        if (mag2 > 0.0) {
+          const double mag = sqrt(mag2);
+          // e^{-i phi} where apq = |apq| e^{i phi}
+          const double2 emi = cmk(apq.x / mag, -apq.y / mag);
+          const double app = A[p][p].x, aqq = A[q][q].x;
+          const double theta = (aqq - app) / (2.0 * mag);
+          double t;
+          if (fabs(theta) > 1e150) {
+            t = 0.5 / theta;
+          } else {
+            t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
+            if (theta < 0.0) t = -t;
+          }
+          const double c = 1.0 / sqrt(t * t + 1.0);
+          const double s = t * c;
+          // columns p, q of A (rows k != p, q), mirrored into rows p, q
+#pragma unroll
+          for (int k = 0; k < I; ++k) {
+            if (k == p || k == q) continue;
+            const double2 akp = A[k][p];
+            const double2 akq_r = cmul(A[k][q], emi);
+            const double2 nkp = cmk(c * akp.x - s * akq_r.x, c * akp.y - s * akq_r.y);
+            const double2 nkq = cmk(s * akp.x + c * akq_r.x, s * akp.y + c * akq_r.y);
+            A[k][p] = nkp;
+            A[k][q] = nkq;
+            A[p][k] = cconj(nkp);
+            A[q][k] = cconj(nkq);
+          }
+          A[p][p] = cmk(app - t * mag, 0.0);
+          A[q][q] = cmk(aqq + t * mag, 0.0);
+          A[p][q] = cmk(0.0, 0.0);
+          A[q][p] = cmk(0.0, 0.0);
+#pragma unroll
+          for (int k = 0; k < I; ++k) {
+            const double2 vkp = V[k][p];
+            const double2 vkq_r = cmul(V[k][q], emi);
+            V[k][p] = cmk(c * vkp.x - s * vkq_r.x, c * vkp.y - s * vkq_r.y);
+            V[k][q] = cmk(s * vkp.x + c * vkq_r.x, s * vkp.y + c * vkq_r.y);
+          }
+        }
+      }
+    }
+  }
+}
+
+// Sort eigenpairs descending (stable for equal keys is not needed).
+template <int I>
+FFCA_DEV void sort_desc(double (&w)[I], double2 (&V)[I][I]) {
+#pragma unroll
+  for (int i = 0; i < I; ++i) {
+#pragma unroll
+    for (int j = 0; j < I - 1 - i; ++j) {
+      const bool sw = w[j] < w[j + 1];
+      const double a = w[j], b = w[j + 1];
+      w[j] = sw ? b : a;
+      w[j + 1] = sw ? a : b;
+#pragma unroll
+      for (int k = 0; k < I; ++k) {
+        const double2 x = V[k][j], y = V[k][j + 1];
+        V[k][j] = sw ? y : x;
+        V[k][j + 1] = sw ? x : y;
+      }
+    }
+  }
+}
+
+// Rotate each column so its largest-magnitude entry (first on ties) is real
+// positive (reference pencil.py:76-82).
+template <int I>
+FFCA_DEV void fix_column_phases(double2 (&P)[I][I]) {
+#pragma unroll
+  for (int k = 0; k < I; ++k) {
+    double best = cabs2(P[0][k]);
+    double2 lead = P[0][k];
+#pragma unroll
+    for (int i = 1; i < I; ++i) {
+      const double m = cabs2(P[i][k]);
+      if (m > best) {
+        best = m;
+        lead = P[i][k];
+      }
+    }
+    const double mag = sqrt(best);
+    if (mag > 0.0) {
+      const double2 cph = cmk(lead.x / mag, -lead.y / mag);  // conj(phase)
+#pragma unroll
+      for (int i = 0; i < I; ++i) P[i][k] = cmul(P[i][k], cph);
+    }
+  }
+}
+
+// Hermitian-definite pencil decomposition (reference pencil.py:85-135):
+// eig(Psi) -> definiteness floor -> whiten Phi -> eig -> descending ->
+// P = U Sigma^{-1/2} Q -> column phases. Psi is read from its lower triangle
+// (as LAPACK zheevd does for numpy.linalg.eigh); Phi is used in full.
+// Returns 0, or 3 (definiteness) with *min_sigma set.
+template <int I>
+FFCA_DEV int gevd_hpd(const double2 (&Phi)[I][I], const double2 (&Psi)[I][I], double (&lam)[I],
+                      double2 (&P)[I][I], double* min_sigma) {
+  double2 A[I][I];
+  double tr = 0.0;
+#pragma unroll
+  for (int a = 0; a < I; ++a) {
+    tr += Psi[a][a].x;
+#pragma unroll
+    for (int b = 0; b < I; ++b) A[a][b] = (a > b) ? Psi[a][b] : (a == b ? cmk(Psi[a][a].x, 0.0) : cconj(Psi[b][a]));
+  }
+  double2 U[I][I];
+  jacobi_herm<I>(A, U);
+  double sig[I];
+  double smin = 1e308;
+#pragma unroll
+  for (int a = 0; a < I; ++a) {
+    sig[a] = A[a][a].x;
+    smin = fmin(smin, sig[a]);
+  }
+  *min_sigma = smin;
+  if (!(smin > kDefFloor * tr / I)) return FFCA_ERR_DEFINITENESS;
+  double isq[I];
+#pragma unroll
+  for (int a = 0; a < I; ++a) isq[a] = 1.0 / sqrt(sig[a]);
+  // W = diag(isq) U^H Phi U diag(isq), then re-symmetrise
+  double2 T[I][I];
+  matmul<I>(Phi, U, T);
+  matmul_hn<I>(U, T, A);
+  double2 W[I][I];
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) W[a][b] = cscale(A[a][b], isq[a] * isq[b]);
+#pragma unroll
+  for (int a = 0; a < I; ++a) {
+    W[a][a] = cmk(W[a][a].x, 0.0);
+#pragma unroll
+    for (int b = a + 1; b < I; ++b) {
+      const double2 h = cmk(0.5 * (W[a][b].x + W[b][a].x), 0.5 * (W[a][b].y - W[b][a].y));
+      W[a][b] = h;
+      W[b][a] = cconj(h);
+    }
+  }
+  double2 Q[I][I];
+  jacobi_herm<I>(W, Q);
+#pragma unroll
+  for (int a = 0; a < I; ++a) lam[a] = W[a][a].x;
+  sort_desc<I>(lam, Q);
+  // P = U diag(isq) Q
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) T[a][b] = cscale(U[a][b], isq[b]);
+  matmul<I>(T, Q, P);
+  fix_column_phases<I>(P);
+  return 0;
+}
+
+// Gauss-Jordan inverse with partial pivoting; also log|det A|.
+// Returns false when a pivot is exactly zero or non-finite.
+template <int I>
+FFCA_DEV bool lu_inverse(const double2 (&A)[I][I], double2 (&Inv)[I][I], double* logabsdet) {
+  double2 M[I][I];
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) M[a][b] = A[a][b];
+  set_identity<I>(Inv);
+  double lad = 0.0;
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < I; ++k) {
+    int r = k;
+    double best = cabs2(M[k][k]);
+#pragma unroll
+    for (int i = k + 1; i < I; ++i) {
+      const double m = cabs2(M[i][k]);
+      if (m > best) {
+        best = m;
+        r = i;
+      }
+    }
+#pragma unroll
+    for (int i = k + 1; i < I; ++i) {
+      if (i == r) {
+#pragma unroll
+        for (int j = 0; j < I; ++j) {
+          double2 t = M[k][j];
+          M[k][j] = M[i][j];
+          M[i][j] = t;
+          t = Inv[k][j];
+          Inv[k][j] = Inv[i][j];
+          Inv[i][j] = t;
+        }
+      }
+    }
+    if (!(best > 0.0) || !isfinite(best)) ok = false;
+    lad += 0.5 * log(best);
+    const double2 ip = cdiv(cmk(1.0, 0.0), M[k][k]);
+#pragma unroll
+    for (int j = 0; j < I; ++j) {
+      M[k][j] = cmul(M[k][j], ip);
+      Inv[k][j] = cmul(Inv[k][j], ip);
+    }
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      if (i == k) continue;
+      const double2 fct = M[i][k];
+#pragma unroll
+      for (int j = 0; j < I; ++j) {
+        M[i][j] = csub(M[i][j], cmul(fct, M[k][j]));
+        Inv[i][j] = csub(Inv[i][j], cmul(fct, Inv[k][j]));
+      }
+    }
+  }
+  *logabsdet = lad;
+  return ok;
+}
+
+// Cholesky A = L L^H of a Hermitian matrix given in full storage (lower
+// triangle used). Returns false if a pivot is not strictly positive.
+template <int I>
+FFCA_DEV bool cholesky(const double2 (&A)[I][I], double2 (&L)[I][I]) {
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < I; ++j) {
+    double d = A[j][j].x;
+#pragma unroll
+    for (int k = 0; k < j; ++k) d -= cabs2(L[j][k]);
+    if (!(d > 0.0)) ok = false;
+    const double ljj = sqrt(fmax(d, 0.0));
+    L[j][j] = cmk(ljj, 0.0);
+    const double il = 1.0 / ljj;
+#pragma unroll
+    for (int i = j + 1; i < I; ++i) {
+      double2 s = A[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) s = csub(s, cmulc(L[i][k], L[j][k]));
+      L[i][j] = cscale(s, il);
+    }
+#pragma unroll
+    for (int i = 0; i < j; ++i) L[i][j] = cmk(0.0, 0.0);
+  }
+  return ok;
+}
+
+// Inverse of a lower-triangular matrix (forward substitution per column).
+template <int I>
+FFCA_DEV void tril_inverse(const double2 (&L)[I][I], double2 (&Li)[I][I]) {
+#pragma unroll
+  for (int c = 0; c < I; ++c) {
+#pragma unroll
+    for (int r = 0; r < I; ++r) {
+      if (r < c) {
+        Li[r][c] = cmk(0.0, 0.0);
+        continue;
+      }
+      double2 s = cmk(r == c ? 1.0 : 0.0, 0.0);
+#pragma unroll
+      for (int k = c; k < r; ++k) s = csub(s, cmul(L[r][k], Li[k][c]));
+      Li[r][c] = cscale(s, 1.0 / L[r][r].x);
+    }
+  }
+}
+
+}  // namespace ffca

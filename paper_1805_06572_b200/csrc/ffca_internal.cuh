@@ -1,0 +1,100 @@
+// Internal launch interfaces shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ffca_common.cuh"
+
+namespace ffca {
+
+constexpr int kWarps = 4;  // warps per CTA in the frame-streaming kernels
+
+// ---- K3: fused FastFCA transform + E + M (+ likelihood, + images) ----------
+struct FastIterParams {
+  const void* y;        // (M,N,F,I) complex R
+  void* v;              // (M,2,N,F) R, read (and written when update)
+  const double2* P;     // (G,I,I)
+  const double2* W;     // (G,I,I) = P^{-H}; needed when mu_back
+  const double* lam;    // (G,I)
+  const double* floor;  // (G)
+  double* Spart;        // [nchunk][2*I*I][G] partial sums (update)
+  double* llbin;        // [nchunk][G] sum_n sum_i log den + |z|^2/den, or null
+  void* mu_out;         // (M,2,N,F,I) complex R or null
+  int mu_back;          // 1: write W m (images); 0: write m (transformed posterior mean)
+  int update;           // v update + S accumulation
+  int64_t M, N, F, G;
+  int64_t chunk_frames;
+  int nchunk;
+  ffca_status_dev* st;
+  int iter;
+};
+cudaError_t launch_fast_em(const FastIterParams& p, int I, int dtype, cudaStream_t s);
+
+// ---- K4: fused conventional FCA iteration (+ likelihood, + mu) -------------
+struct FcaIterParams {
+  const void* y;        // (M,N,F,I)
+  void* v;              // (M,2,N,F)
+  const double* Sp;     // [4][I*I][G] packed S1,S2,Sinv1,Sinv2 (SoA)
+  const double* floor;  // (G)
+  double* Spart;        // [nchunk][2*I*I][G]
+  double* llbin;        // [nchunk][G] sum log det R + y^H R^-1 y, or null
+  void* mu_out;         // (M,2,N,F,I) or null
+  int update;
+  int64_t M, N, F, G;
+  int64_t chunk_frames;
+  int nchunk;
+  ffca_status_dev* st;
+  int iter;
+};
+cudaError_t launch_fca_em(const FcaIterParams& p, int I, int dtype, cudaStream_t s);
+
+// ---- K1: per-bin pencil update ----------------------------------------------
+struct PencilParams {
+  const double* Spart;  // [nchunk][2*I*I][G]
+  int nchunk;
+  int64_t N, G;
+  double2* P;        // (G,I,I) in: P_e, out: P_next
+  double2* W;        // (G,I,I) in: P_e^{-H}, out: P_next^{-H}
+  double* lam;       // (G,I) out
+  double* logdet2;   // (G) in: logdet2(P_e), out: logdet2(P_next)
+  double2* S_model;  // (M,2,F,I,I) out: back-transformed regularised S (model S)
+  double2* S_hist;   // (M,2,F,I,I) slice for this iteration or null
+  const double* llbin;  // [nchunk][G] or null
+  double* llg;          // (G) out or null: N logdet2(P_e) - sum llbin
+  int64_t F;
+  ffca_status_dev* st;
+  int iter;
+};
+cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s);
+
+// initial pencil from S0 (M,2,F,I,I): P, W, lam, logdet2 (fast.py:127-130)
+cudaError_t launch_initial_pencil(const double2* S0, double2* P, double2* W, double* lam,
+                                  double* logdet2, int64_t G, int64_t F, int I,
+                                  ffca_status_dev* st, cudaStream_t s);
+
+// ---- FCA per-bin steps ------------------------------------------------------
+// pack S (M,2,F,I,I) -> Sp [4][I*I][G] with S1,S2 and their Cholesky inverses
+cudaError_t launch_fca_prepare(const double2* S, double* Sp, int64_t G, int64_t F, int I,
+                               ffca_status_dev* st, int iter, cudaStream_t s);
+// reduce partials, regularise (modelops.py:29-39), write S_model (+hist), and
+// refresh Sp (S and S^{-1}) for the next iteration; llg (G) collect.
+cudaError_t launch_fca_finish(const double* Spart, int nchunk, int64_t N, int64_t G, int64_t F,
+                              double* Sp, double2* S_model, double2* S_hist,
+                              const double* llbin, double* llg, int I, ffca_status_dev* st,
+                              int iter, cudaStream_t s);
+
+// ---- likelihood bookkeeping -------------------------------------------------
+// llg[g] = coef_logdet * N * logdet2[g] - sum_c llbin[c][g]   (logdet2 may be null)
+cudaError_t launch_ll_collect(const double* llbin, int nchunk, const double* logdet2, int64_t N,
+                              int64_t G, double* llg, cudaStream_t s);
+// loglik[m*(L+1)+l] = sum_f llg[l][m*F+f] - N F I log(pi)
+cudaError_t launch_ll_reduce(const double* llg, int64_t M, int64_t F, int64_t N, int I,
+                             int nlev, int Lp1, double* loglik, cudaStream_t s);
+
+// chunking of the frame axis so that the grid fills the GPU
+void plan_chunks(int64_t G, int64_t N, int64_t* chunk_frames, int* nchunk);
+
+int sm_count();
+
+}  // namespace ffca

@@ -1,0 +1,494 @@
+// K1 — per-bin pencil refresh for FastFCA, one thread per (mixture, bin):
+//   sum the frame-chunk partials of S~ (fixed order) and divide by N,
+//   ridge with eps * P^H P (fast.py:80-90: the image of FCA's eps*I ridge),
+//   back-transform S = P^{-H} S~ P^{-1} for the model / history
+//   (fast.py:144-148), Hermitian-definite GEVD of (S~1, S~2)
+//   (pencil.py:85-135), P <- P Q (fast.py:107-113), P^{-H} and log|det P|^2
+//   for the next pass (fast.py:151-153).
+// Plus the stand-alone batched per-bin routines of the C ABI.
+#include "ffca_internal.cuh"
+
+namespace ffca {
+
+template <int I>
+__global__ void __launch_bounds__(64) pencil_update_kernel(const PencilParams p) {
+  constexpr int NP = I * I;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= p.G) return;
+  const int64_t G = p.G;
+  const int64_t m = g / p.F, f = g - m * p.F;
+
+  // 1. reduce partials
+  double2 S1[I][I], S2[I][I];
+  {
+    double s[2][NP];
+#pragma unroll
+    for (int e = 0; e < NP; ++e) s[0][e] = s[1][e] = 0.0;
+    for (int c = 0; c < p.nchunk; ++c) {
+      const double* sp = p.Spart + (size_t)c * 2 * NP * G + g;
+#pragma unroll
+      for (int e = 0; e < NP; ++e) {
+        s[0][e] += sp[(size_t)e * G];
+        s[1][e] += sp[(size_t)(NP + e) * G];
+      }
+    }
+    const double invN = 1.0 / (double)p.N;
+    bool fin = true;
+#pragma unroll
+    for (int e = 0; e < NP; ++e) {
+      s[0][e] *= invN;
+      s[1][e] *= invN;
+      fin = fin && isfinite(s[0][e]) && isfinite(s[1][e]);
+    }
+    if (!fin && p.st) report_error(p.st, p.iter, FFCA_ERR_SINGULAR_MATRIX, (unsigned long long)g);
+    unpack_herm<I>(s[0], S1);
+    unpack_herm<I>(s[1], S2);
+  }
+  // likelihood of the model this pass used (P_e, logdet2(P_e))
+  if (p.llg) {
+    double s = 0.0;
+    for (int c = 0; c < p.nchunk; ++c) s += p.llbin[(size_t)c * G + g];
+    p.llg[g] = (double)p.N * p.logdet2[g] - s;
+  }
+
+  double2 Pe[I][I], We[I][I];
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      Pe[a][b] = p.P[g * NP + a * I + b];
+      We[a][b] = p.W[g * NP + a * I + b];
+    }
+
+  // 2. ridge eps_j = 1e-9 tr(gram^{-1} S~_j)/I = 1e-9 tr(W S~_j W^H)/I, and
+  //    the back-transformed model covariance W (S~_j + eps_j gram) W^H
+  //    = W S~_j W^H + eps_j Id.
+  double eps[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    double2 T[I][I], Sb[I][I];
+    matmul_nh<I>(j == 0 ? S1 : S2, We, T);  // S~ W^H
+    matmul<I>(We, T, Sb);                   // W S~ W^H
+    double tr = 0.0;
+#pragma unroll
+    for (int a = 0; a < I; ++a) tr += Sb[a][a].x;
+    eps[j] = kCovEps * tr / I;
+    double2* dst = p.S_model + ((m * 2 + j) * p.F + f) * NP;
+    double2* hst = p.S_hist ? p.S_hist + ((m * 2 + j) * p.F + f) * NP : nullptr;
+#pragma unroll
+    for (int a = 0; a < I; ++a)
+#pragma unroll
+      for (int b = 0; b < I; ++b) {
+        double2 val = Sb[a][b];
+        if (a == b) val.x += eps[j];
+        dst[a * I + b] = val;
+        if (hst) hst[a * I + b] = val;
+      }
+  }
+  {
+    double2 gram[I][I];
+    matmul_hn<I>(Pe, Pe, gram);
+#pragma unroll
+    for (int a = 0; a < I; ++a)
+#pragma unroll
+      for (int b = 0; b < I; ++b) {
+        // use the upper triangle of gram for both halves (exactly Hermitian)
+        const double2 gab = (a <= b) ? gram[a][b] : cconj(gram[b][a]);
+        S1[a][b] = cadd(S1[a][b], cscale(gab, eps[0]));
+        S2[a][b] = cadd(S2[a][b], cscale(gab, eps[1]));
+      }
+  }
+
+  // 3. GEVD of the transformed pencil, P <- P Q
+  double lam[I];
+  double2 Q[I][I];
+  double msig = 0.0;
+  const int rc = gevd_hpd<I>(S1, S2, lam, Q, &msig);
+  if (rc != 0 && p.st) {
+    report_error(p.st, p.iter, rc, (unsigned long long)g);
+    report_min_value(p.st, msig);
+  }
+  double2 Pn[I][I];
+  matmul<I>(Pe, Q, Pn);
+  double2 Inv[I][I];
+  double lad = 0.0;
+  lu_inverse<I>(Pn, Inv, &lad);
+#pragma unroll
+  for (int a = 0; a < I; ++a) {
+    p.lam[g * I + a] = lam[a];
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      p.P[g * NP + a * I + b] = Pn[a][b];
+      p.W[g * NP + a * I + b] = cconj(Inv[b][a]);
+    }
+  }
+  p.logdet2[g] = 2.0 * lad;
+}
+
+template <int I>
+__global__ void __launch_bounds__(64)
+    initial_pencil_kernel(const double2* __restrict__ S0, double2* P, double2* W, double* lam,
+                          double* logdet2, int64_t G, int64_t F, ffca_status_dev* st) {
+  constexpr int NP = I * I;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G) return;
+  const int64_t m = g / F, f = g - m * F;
+  double2 A[I][I], B[I][I];
+  const double2* s1 = S0 + ((m * 2 + 0) * F + f) * NP;
+  const double2* s2 = S0 + ((m * 2 + 1) * F + f) * NP;
+  double sc1 = 0.0, sc2 = 0.0, as1 = 0.0, as2 = 0.0;
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      A[a][b] = s1[a * I + b];
+      B[a][b] = s2[a * I + b];
+    }
+  // _check_hermitian (pencil.py:40-51)
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      sc1 = fmax(sc1, sqrt(cabs2(A[a][b])));
+      sc2 = fmax(sc2, sqrt(cabs2(B[a][b])));
+      as1 = fmax(as1, sqrt(cabs2(csub(A[a][b], cconj(A[b][a])))));
+      as2 = fmax(as2, sqrt(cabs2(csub(B[a][b], cconj(B[b][a])))));
+    }
+  if ((as1 > kHermRtol * fmax(sc1, 1e-300)) || (as2 > kHermRtol * fmax(sc2, 1e-300))) {
+    if (st) report_error(st, 0, FFCA_ERR_NON_HERMITIAN, (unsigned long long)g);
+  }
+  double l[I];
+  double2 Pn[I][I];
+  double msig = 0.0;
+  const int rc = gevd_hpd<I>(A, B, l, Pn, &msig);
+  if (rc != 0 && st) {
+    report_error(st, 0, rc, (unsigned long long)g);
+    report_min_value(st, msig);
+  }
+  double2 Inv[I][I];
+  double lad = 0.0;
+  lu_inverse<I>(Pn, Inv, &lad);
+#pragma unroll
+  for (int a = 0; a < I; ++a) {
+    lam[g * I + a] = l[a];
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      P[g * NP + a * I + b] = Pn[a][b];
+      W[g * NP + a * I + b] = cconj(Inv[b][a]);
+    }
+  }
+  logdet2[g] = 2.0 * lad;
+}
+
+#define FFCA_DISPATCH_I(I, CALL)   \
+  switch (I) {                     \
+    case 1: {                      \
+      constexpr int II = 1;        \
+      CALL;                        \
+    } break;                       \
+    case 2: {                      \
+      constexpr int II = 2;        \
+      CALL;                        \
+    } break;                       \
+    case 3: {                      \
+      constexpr int II = 3;        \
+      CALL;                        \
+    } break;                       \
+    case 4: {                      \
+      constexpr int II = 4;        \
+      CALL;                        \
+    } break;                       \
+    case 5: {                      \
+      constexpr int II = 5;        \
+      CALL;                        \
+    } break;                       \
+    case 6: {                      \
+      constexpr int II = 6;        \
+      CALL;                        \
+    } break;                       \
+    case 7: {                      \
+      constexpr int II = 7;        \
+      CALL;                        \
+    } break;                       \
+    case 8: {                      \
+      constexpr int II = 8;        \
+      CALL;                        \
+    } break;                       \
+    default:                       \
+      return cudaErrorInvalidValue; \
+  }
+
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s) {
+  FFCA_DISPATCH_I(I, (pencil_update_kernel<II><<<nblk(p.G, 64), 64, 0, s>>>(p)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_initial_pencil(const double2* S0, double2* P, double2* W, double* lam,
+                                  double* logdet2, int64_t G, int64_t F, int I,
+                                  ffca_status_dev* st, cudaStream_t s) {
+  FFCA_DISPATCH_I(I, (initial_pencil_kernel<II><<<nblk(G, 64), 64, 0, s>>>(S0, P, W, lam,
+                                                                            logdet2, G, F, st)));
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Stand-alone batched per-bin routines (C ABI stage level)
+// ---------------------------------------------------------------------------
+template <int I>
+__global__ void gevd_batch_kernel(const double2* Phi, const double2* Psi, double* lam,
+                                  double2* P, const double2* Pprev, int64_t B, int check,
+                                  ffca_status_dev* st) {
+  constexpr int NP = I * I;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= B) return;
+  double2 A[I][I], Bm[I][I];
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      A[a][b] = Phi[g * NP + a * I + b];
+      Bm[a][b] = Psi[g * NP + a * I + b];
+    }
+  if (check) {
+    double sc1 = 0.0, sc2 = 0.0, as1 = 0.0, as2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < I; ++a)
+#pragma unroll
+      for (int b = 0; b < I; ++b) {
+        sc1 = fmax(sc1, sqrt(cabs2(A[a][b])));
+        sc2 = fmax(sc2, sqrt(cabs2(Bm[a][b])));
+        as1 = fmax(as1, sqrt(cabs2(csub(A[a][b], cconj(A[b][a])))));
+        as2 = fmax(as2, sqrt(cabs2(csub(Bm[a][b], cconj(Bm[b][a])))));
+      }
+    if ((as1 > kHermRtol * fmax(sc1, 1e-300)) || (as2 > kHermRtol * fmax(sc2, 1e-300))) {
+      if (st) report_error(st, 0, FFCA_ERR_NON_HERMITIAN, (unsigned long long)g);
+      return;
+    }
+  }
+  double l[I];
+  double2 Q[I][I];
+  double msig = 0.0;
+  const int rc = gevd_hpd<I>(A, Bm, l, Q, &msig);
+  if (rc != 0 && st) {
+    report_error(st, 0, rc, (unsigned long long)g);
+    report_min_value(st, msig);
+  }
+  if (Pprev) {
+    double2 Pp[I][I], Pn[I][I];
+#pragma unroll
+    for (int a = 0; a < I; ++a)
+#pragma unroll
+      for (int b = 0; b < I; ++b) Pp[a][b] = Pprev[g * NP + a * I + b];
+    matmul<I>(Pp, Q, Pn);
+#pragma unroll
+    for (int a = 0; a < I; ++a)
+#pragma unroll
+      for (int b = 0; b < I; ++b) Q[a][b] = Pn[a][b];
+  }
+#pragma unroll
+  for (int a = 0; a < I; ++a) {
+    lam[g * I + a] = l[a];
+#pragma unroll
+    for (int b = 0; b < I; ++b) P[g * NP + a * I + b] = Q[a][b];
+  }
+}
+
+template <int I>
+__global__ void cholinv_kernel(const double2* S, double2* Sinv, int64_t B, ffca_status_dev* st) {
+  constexpr int NP = I * I;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= B) return;
+  double2 A[I][I], L[I][I], Li[I][I];
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) A[a][b] = S[g * NP + a * I + b];
+  if (!cholesky<I>(A, L) && st) report_error(st, 0, FFCA_ERR_NOT_PD, (unsigned long long)g);
+  tril_inverse<I>(L, Li);
+  // Sinv = Li^H Li
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      double2 acc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < I; ++k) {
+        if (k < a || k < b) continue;
+        acc = cadd(acc, cconjmul(Li[k][a], Li[k][b]));
+      }
+      Sinv[g * NP + a * I + b] = acc;
+    }
+}
+
+template <int I>
+__global__ void regularize_kernel(const double2* S, double2* out, int64_t B) {
+  constexpr int NP = I * I;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= B) return;
+  double2 H[I][I];
+  double tr = 0.0;
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      const double2 x = S[g * NP + a * I + b], y = S[g * NP + b * I + a];
+      H[a][b] = cmk(0.5 * (x.x + y.x), 0.5 * (x.y - y.y));
+    }
+#pragma unroll
+  for (int a = 0; a < I; ++a) tr += H[a][a].x;
+  const double eps = kCovEps * tr / I;
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      double2 v = H[a][b];
+      if (a == b) v.x += eps;
+      out[g * NP + a * I + b] = v;
+    }
+}
+
+// S_t = herm(S_raw) + eps gram, eps = 1e-9 tr(gram^{-1} herm(S_raw))/I  (fast.py:80-90)
+template <int I>
+__global__ void reg_transformed_kernel(const double2* S, const double2* gram, double2* out,
+                                       int64_t B) {
+  constexpr int NP = I * I;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= B) return;
+  double2 H[I][I], Gm[I][I];
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      const double2 x = S[g * NP + a * I + b], y = S[g * NP + b * I + a];
+      H[a][b] = cmk(0.5 * (x.x + y.x), 0.5 * (x.y - y.y));
+      Gm[a][b] = gram ? gram[g * NP + a * I + b] : cmk(a == b ? 1.0 : 0.0, 0.0);
+    }
+  double tr = 0.0;
+  if (gram) {
+    double2 Gi[I][I];
+    double lad;
+    lu_inverse<I>(Gm, Gi, &lad);
+#pragma unroll
+    for (int a = 0; a < I; ++a)
+#pragma unroll
+      for (int k = 0; k < I; ++k) tr += Gi[a][k].x * H[k][a].x - Gi[a][k].y * H[k][a].y;
+  } else {
+#pragma unroll
+    for (int a = 0; a < I; ++a) tr += H[a][a].x;
+  }
+  const double eps = kCovEps * tr / I;
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) out[g * NP + a * I + b] = cadd(H[a][b], cscale(Gm[a][b], eps));
+}
+
+// W = (P^{-1})^H per bin; logdet2 optional
+template <int I>
+__global__ void inverse_h_kernel(const double2* P, double2* W, double* logdet2, int64_t B,
+                                 ffca_status_dev* st) {
+  constexpr int NP = I * I;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= B) return;
+  double2 A[I][I], Inv[I][I];
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) A[a][b] = P[g * NP + a * I + b];
+  double lad = 0.0;
+  const bool ok = lu_inverse<I>(A, Inv, &lad);
+  if (!ok && st) report_error(st, 0, FFCA_ERR_SINGULAR_BASIS, (unsigned long long)g);
+  if (W) {
+#pragma unroll
+    for (int a = 0; a < I; ++a)
+#pragma unroll
+      for (int b = 0; b < I; ++b) W[g * NP + a * I + b] = cconj(Inv[b][a]);
+  }
+  if (logdet2) logdet2[g] = 2.0 * lad;
+}
+
+// out(s,n,f,:) = W(f) mu_t(s,n,f,:)
+template <int I>
+__global__ void apply_w_kernel(const double2* mu_t, const double2* W, double2* out, int64_t Src,
+                               int64_t N, int64_t F) {
+  constexpr int NP = I * I;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= Src * N * F) return;
+  const int64_t f = t % F;
+  double2 x[I];
+#pragma unroll
+  for (int a = 0; a < I; ++a) x[a] = mu_t[t * I + a];
+#pragma unroll
+  for (int a = 0; a < I; ++a) {
+    double2 s = cmk(0.0, 0.0);
+#pragma unroll
+    for (int b = 0; b < I; ++b) s = cadd(s, cmul(W[f * NP + a * I + b], x[b]));
+    out[t * I + a] = s;
+  }
+}
+
+// out(s,f) = W(f) S(s,f) W(f)^H
+template <int I>
+__global__ void conj_w_kernel(const double2* S, const double2* W, double2* out, int64_t Src,
+                              int64_t F) {
+  constexpr int NP = I * I;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= Src * F) return;
+  const int64_t f = t % F;
+  double2 A[I][I], Wm[I][I], T[I][I], R[I][I];
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      A[a][b] = S[t * NP + a * I + b];
+      Wm[a][b] = W[f * NP + a * I + b];
+    }
+  matmul_nh<I>(A, Wm, T);
+  matmul<I>(Wm, T, R);
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) out[t * NP + a * I + b] = R[a][b];
+}
+
+cudaError_t launch_gevd_batch(const double2* Phi, const double2* Psi, double* lam, double2* P,
+                              const double2* Pprev, int64_t B, int I, int check,
+                              ffca_status_dev* st, cudaStream_t s) {
+  FFCA_DISPATCH_I(I, (gevd_batch_kernel<II><<<nblk(B, 64), 64, 0, s>>>(Phi, Psi, lam, P, Pprev,
+                                                                        B, check, st)));
+  return cudaGetLastError();
+}
+cudaError_t launch_cholinv(const double2* S, double2* Sinv, int64_t B, int I, ffca_status_dev* st,
+                           cudaStream_t s) {
+  FFCA_DISPATCH_I(I, (cholinv_kernel<II><<<nblk(B, 64), 64, 0, s>>>(S, Sinv, B, st)));
+  return cudaGetLastError();
+}
+cudaError_t launch_regularize(const double2* S, double2* out, int64_t B, int I, cudaStream_t s) {
+  FFCA_DISPATCH_I(I, (regularize_kernel<II><<<nblk(B, 128), 128, 0, s>>>(S, out, B)));
+  return cudaGetLastError();
+}
+cudaError_t launch_reg_transformed(const double2* S, const double2* gram, double2* out,
+                                   int64_t B, int I, cudaStream_t s) {
+  FFCA_DISPATCH_I(I, (reg_transformed_kernel<II><<<nblk(B, 64), 64, 0, s>>>(S, gram, out, B)));
+  return cudaGetLastError();
+}
+cudaError_t launch_inverse_h(const double2* P, double2* W, double* logdet2, int64_t B, int I,
+                             ffca_status_dev* st, cudaStream_t s) {
+  FFCA_DISPATCH_I(I, (inverse_h_kernel<II><<<nblk(B, 64), 64, 0, s>>>(P, W, logdet2, B, st)));
+  return cudaGetLastError();
+}
+cudaError_t launch_apply_w(const double2* mu_t, const double2* W, double2* out, int64_t Src,
+                           int64_t N, int64_t F, int I, cudaStream_t s) {
+  FFCA_DISPATCH_I(I, (apply_w_kernel<II><<<nblk(Src * N * F, 128), 128, 0, s>>>(mu_t, W, out,
+                                                                                Src, N, F)));
+  return cudaGetLastError();
+}
+cudaError_t launch_conj_w(const double2* S, const double2* W, double2* out, int64_t Src,
+                          int64_t F, int I, cudaStream_t s) {
+  FFCA_DISPATCH_I(I, (conj_w_kernel<II><<<nblk(Src * F, 64), 64, 0, s>>>(S, W, out, Src, F)));
+  return cudaGetLastError();
+}
+
+}  // namespace ffca

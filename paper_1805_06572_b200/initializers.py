@@ -1,0 +1,45 @@
+"""Seeded random initial model (reference initializers.py:20-39).
+
+``S_j = A A^H + I`` with one complex Gaussian I x I draw per source shared
+across bins (drawn on the host with numpy's PCG64 so the stream is
+bit-identical to the reference's), powers ``||y||^2/(2I)`` floored per bin,
+computed on the device by ``ffca_init_powers``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _device as D
+from .types import SpatialModel
+
+
+def draw_covariances(seed, n_bins, n_chan):
+    gen = np.random.default_rng(seed)
+    S = np.empty((2, n_bins, n_chan, n_chan), dtype=np.complex128)
+    for j in range(2):
+        re = gen.standard_normal((n_chan, n_chan))
+        im = gen.standard_normal((n_chan, n_chan))
+        A = re + 1j * im
+        S[j] = (A @ A.conj().T + np.eye(n_chan))[None]
+    return S
+
+
+def init_random(y, seed, dtype="c128"):
+    """Reference ``init_random(y, seed)``; device tensors in -> device tensors out."""
+    lib = D.require()
+    torch = D.torch
+    data = y if (D.is_tensor(y) or isinstance(y, np.ndarray)) else y.data
+    ctype, rtype = (torch.complex128, torch.float64) if dtype == "c128" else (torch.complex64,
+                                                                             torch.float32)
+    yd = D.to_device(data, ctype)
+    N, F, I = (int(s) for s in yd.shape[-3:])
+    v = D.empty((1, 2, N, F), rtype)
+    floor = D.empty((1, F), torch.float64)
+    D.check_rc(lib.ffca_init_powers(D.ptr(yd), D.ptr(v), D.ptr(floor), 1, N, F, I,
+                                    0 if dtype == "c128" else 1, D.stream_handle()),
+               "ffca_init_powers")
+    S = draw_covariances(seed, F, I)
+    if D.is_tensor(y):
+        return SpatialModel(v=v[0], S=torch.as_tensor(S, device=yd.device), v_floor=floor[0])
+    return SpatialModel(v=D.host(v[0]), S=S, v_floor=D.host(floor[0]))

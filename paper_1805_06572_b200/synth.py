@@ -109,7 +109,7 @@ def make_mixture(seed, I, F, N, rank=None, eps=1e-3, sigma=1.5, envelope=False,
             gre = gen.standard_normal((nb, F, I))
             gim = gen.standard_normal((nb, F, I))
             g = (gre + 1j * gim) * inv_sqrt2
-            x = np.einsum("fab,nfb->nfa", C[j], g)
+            x = np.matmul(C[j], g.transpose(1, 2, 0)).transpose(2, 0, 1)  # chol(R_j) g
             blk += sv[j, n0:n1, :, None] * x
         y[n0:n1] = blk
     if return_truth:

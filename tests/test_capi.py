@@ -1,0 +1,108 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library exists, loads,
+and exports every symbol include/fastfca_b200.h declares (no compute calls —
+there is no GPU here), and the Python host logic behaves without a device.
+"""
+
+import ctypes
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_1805_06572_b200 import _backend, _lib
+from paper_1805_06572_b200.errors import BackendUnavailableError
+
+REPO = Path(__file__).resolve().parents[1]
+HEADER = REPO / "include" / "fastfca_b200.h"
+
+
+def header_symbols():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ffca_[A-Za-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_contract():
+    syms = header_symbols()
+    # the 11 kernel-module functions of the reference plugin + run level
+    for name in ("fast_transform", "fast_e_step", "fast_v_update", "S_update",
+                 "fast_log_likelihood", "fast_iteration", "fca_e_step", "fca_v_update",
+                 "fca_log_likelihood", "fca_iteration", "fastfca_run", "fca_run", "gevd_hpd"):
+        assert f"ffca_{name}" in syms
+
+
+def test_library_loads_and_exports_every_header_symbol():
+    lib = _lib.load()
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+    assert lib.ffca_version().decode().startswith("fastfca_b200")
+    assert lib.ffca_device_arch() == 100
+
+
+def test_ctypes_signatures_cover_the_header():
+    declared = set(header_symbols())
+    bound = {name for name, _, _ in _lib.SIGNATURES}
+    assert declared == bound
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_run_args_layout_matches_c():
+    # 3 int64 + 4 int32 + 10 pointers + size_t + pointer + int64
+    assert ctypes.sizeof(_lib.RunArgs) == 24 + 16 + 8 * 10 + 8 + 8 + 8
+
+
+def test_workspace_size_query_needs_no_device():
+    lib = _lib.load()
+    n = lib.ffca_fastfca_workspace_size(1, 500, 257, 2, 10, 7, 0)
+    assert n > 0
+    assert lib.ffca_fastfca_workspace_size(1, 500, 257, 9, 10, 7, 0) == 0  # I > 8 rejected
+    assert lib.ffca_fca_workspace_size(256, 1250, 257, 4, 20, 1, 0) > 0
+
+
+def test_backend_selector_is_cuda_only(monkeypatch):
+    assert _backend.select_backend("cuda") == "cuda"
+    assert _backend.select_backend("auto") == "cuda"
+    with pytest.raises(ValueError):
+        _backend.select_backend("numpy")
+    monkeypatch.setenv("FASTFCA_BACKEND", "numba")
+    with pytest.raises(ValueError):
+        _backend.select_backend(None)
+    monkeypatch.setenv("FASTFCA_BACKEND", "cuda")
+    assert _backend.select_backend(None) == "cuda"
+
+
+def test_product_path_fails_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1805_06572_b200 import fastfca_run, init_random
+
+    y = np.ones((4, 3, 2), dtype=complex)
+    with pytest.raises(BackendUnavailableError):
+        init_random(y, 0)
+    with pytest.raises(BackendUnavailableError):
+        from paper_1805_06572_b200.types import SpatialModel
+
+        fastfca_run(y, SpatialModel(np.ones((2, 4, 3)), np.stack([np.eye(2)] * 3)[None].repeat(
+            2, 0), np.ones(3) * 1e-9), 1)
+
+
+def test_package_never_imports_the_oracle():
+    pkg = REPO / "paper_1805_06572_b200"
+    for p in pkg.rglob("*.py"):
+        assert not re.search(r"^\s*(from|import)\s+oracle", p.read_text(), re.M), p
+
+
+def test_missing_library_raises(tmp_path):
+    with pytest.raises(BackendUnavailableError):
+        _lib.load(tmp_path / "nope.so")

@@ -1,0 +1,307 @@
+"""GPU parity: the CUDA path against the reference's golden vectors and the
+pinned CPU oracle on identical seeded inputs.
+
+Tolerances (north_star): relative error <= 1e-9 for complex128, <= 1e-4 for
+complex64 (against the complex128 reference), measured as the reference's
+``max|a-b| / max|b|`` per quantity (tests/test_acceptance.py:34-35) and
+per-entry relative error for the log-likelihood trace. Compared quantities
+are phase invariant: v, S (original basis), the likelihood trace, images.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import fastfca_oracle as O
+from tests.conftest import RUN_CASES, load_golden
+from tests.instances import kernel_instance, random_complex, random_instance
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+TOL_C64 = 1e-4
+
+
+def _pkg():
+    import paper_1805_06572_b200 as P
+
+    return P
+
+
+def _model(g):
+    return _pkg().SpatialModel(v=g["v0"], S=g["S0"], v_floor=g["floor"])
+
+
+def _ll_dev(a, b):
+    a = np.asarray(a, dtype=float)
+    b = np.asarray(b, dtype=float)
+    assert a.shape == b.shape
+    return float(np.max(np.abs(a - b) / np.abs(b))) if b.size else 0.0
+
+
+def _check(res, g, tag, tol):
+    stride = int(g["image_stride"])
+    assert O.scale_dev(res.images[:, ::stride], g[f"{tag}_images"]) <= tol
+    assert O.scale_dev(res.model.v, g[f"{tag}_v"]) <= tol
+    assert O.scale_dev(res.model.S, g[f"{tag}_S"]) <= tol
+    assert _ll_dev(res.loglik_trace, g[f"{tag}_ll"]) <= tol
+    L = int(g["L"])
+    assert len(res.history) == L
+    if L:
+        hist = np.stack([h["S"] for h in res.history])
+        assert O.scale_dev(hist, g[f"{tag}_Shist"]) <= tol
+        if f"{tag}_vhist" in g:
+            assert O.scale_dev(np.stack([h["v"] for h in res.history]), g[f"{tag}_vhist"]) <= tol
+    oc = res.op_counts
+    assert [oc.frame_matrix_inversions, oc.frame_matrix_products, oc.bin_gevd_count,
+            oc.bin_matrix_products] == list(g[f"{tag}_counts"])
+
+
+@pytest.mark.parametrize("case", RUN_CASES)
+def test_fastfca_run_matches_reference(case):
+    g = load_golden(f"runs_{case}")
+    res = _pkg().fastfca_run(g["y"], _model(g), int(g["L"]), record_history=True)
+    assert res.algorithm == "FastFCA"
+    _check(res, g, "fast", TOL)
+
+
+@pytest.mark.parametrize("case", RUN_CASES)
+def test_fca_run_matches_reference(case):
+    g = load_golden(f"runs_{case}")
+    res = _pkg().fca_run(g["y"], _model(g), int(g["L"]), record_history=True)
+    assert res.algorithm == "FCA"
+    _check(res, g, "fca", TOL)
+
+
+@pytest.mark.parametrize("case", ["cfg3m0", "cfg2", "acc2"])
+def test_complex64_within_1e4_of_reference(case):
+    g = load_golden(f"runs_{case}")
+    res = _pkg().fastfca_run(g["y"], _model(g), int(g["L"]), dtype="c64")
+    stride = int(g["image_stride"])
+    assert O.scale_dev(res.images[:, ::stride], g["fast_images"]) <= TOL_C64
+    assert O.scale_dev(res.model.v, g["fast_v"]) <= TOL_C64
+    assert O.scale_dev(res.model.S, g["fast_S"]) <= TOL_C64
+    assert _ll_dev(res.loglik_trace, g["fast_ll"]) <= TOL_C64
+
+
+@pytest.mark.parametrize("I", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_every_channel_count_matches_oracle(I):
+    y, v, S = random_instance(300 + I, n_frames=37, n_bins=6, n_chan=I)
+    floor = O.power_floor(y)
+    v = np.maximum(v, floor[None, None, :])
+    P = _pkg()
+    init = P.SpatialModel(v=v, S=S, v_floor=floor)
+    for run, orun in ((P.fastfca_run, O.fastfca_run), (P.fca_run, O.fca_run)):
+        res = run(y, init, 4, record_history=True)
+        ref = orun(y, v, S, floor, 4, record_history=True)
+        assert O.scale_dev(res.images, ref.images) <= TOL
+        assert O.scale_dev(res.model.v, ref.v) <= TOL
+        assert O.scale_dev(res.model.S, ref.S) <= TOL
+        assert _ll_dev(res.loglik_trace, ref.loglik_trace) <= TOL
+
+
+def test_batched_run_equals_single_runs():
+    P = _pkg()
+    ys, models = [], []
+    for m in range(3):
+        gen = np.random.default_rng(70 + m)
+        y = random_complex(gen, (50, 9, 3))
+        ys.append(y)
+        models.append(P.init_random(y, 5 + m))
+    Y = np.stack(ys)
+    batch = P.SpatialModel(v=np.stack([m.v for m in models]), S=np.stack([m.S for m in models]),
+                           v_floor=np.stack([m.v_floor for m in models]))
+    for run in (P.fastfca_run, P.fca_run):
+        rb = run(Y, batch, 6)
+        for m in range(3):
+            rs = run(ys[m], models[m], 6)
+            assert O.scale_dev(rb.images[m], rs.images) <= 1e-12
+            assert O.scale_dev(rb.model.v[m], rs.model.v) <= 1e-12
+            assert _ll_dev(rb.loglik_trace[m], rs.loglik_trace) <= 1e-12
+
+
+def test_bin_shards_are_bitwise_identical_to_the_full_run():
+    """Frequency bins are independent; with equal frame chunking the per-bin
+    reduction order is the same, so 1-GPU and k-GPU runs agree bit for bit."""
+    from paper_1805_06572_b200._engine import run_device
+
+    P = _pkg()
+    gen = np.random.default_rng(9)
+    y = random_complex(gen, (300, 40, 4))
+    init = P.init_random(y, 3)
+    cf = 64
+    full = run_device("fast", y[None], init.v[None], init.S[None], init.v_floor[None], 5,
+                      chunk_frames=cf)
+    cuts = [0, 7, 23, 40]
+    for a, b in zip(cuts, cuts[1:]):
+        part = run_device("fast", np.ascontiguousarray(y[None, :, a:b]),
+                          np.ascontiguousarray(init.v[None, :, :, a:b]), init.S[None][:, :, a:b],
+                          init.v_floor[None][:, a:b], 5, chunk_frames=cf)
+        assert (part.v.cpu() == full.v[..., a:b].cpu()).all()
+        assert (part.images.cpu() == full.images[:, :, :, a:b].cpu()).all()
+        assert (part.S.cpu() == full.S[:, :, a:b].cpu()).all()
+
+
+def test_kernel_contract_matches_reference_backend():
+    """Template: reference tests/test_backend.py — CUDA vs numba at 1e-12."""
+    from paper_1805_06572_b200 import _kernels_cuda as K
+
+    k = load_golden("kernels")
+    y, v, S, Pm, lam, floor = k["y"], k["v"], k["S"], k["P"], k["lam"], k["floor"]
+    mu, Phi, ninv, nprod = K.fca_e_step(y, v, S)
+    assert O.scale_dev(mu, k["fca_e_mu"]) <= 1e-12
+    assert O.scale_dev(Phi, k["fca_e_Phi"]) <= 1e-12
+    assert [ninv, nprod] == list(k["fca_e_counts"])
+    assert O.scale_dev(K.fca_v_update(k["fca_e_Phi"], S), k["fca_v"]) <= 1e-12
+    assert O.scale_dev(K.fca_S_update(k["fca_e_Phi"], k["fca_v"]), k["fca_S"]) <= 1e-12
+    assert K.fca_log_likelihood(y, v, S) == pytest.approx(float(k["fca_ll"]), rel=1e-12)
+    assert O.scale_dev(K.fast_transform(y, Pm), k["yt"]) <= 1e-13
+    mu_t, Phi_t, _, _ = K.fast_e_step(k["yt"], v, lam)
+    assert O.scale_dev(mu_t, k["fast_e_mu"]) <= 1e-12
+    assert O.scale_dev(Phi_t, k["fast_e_Phi"]) <= 1e-12
+    assert O.scale_dev(K.fast_v_update(k["fast_e_Phi"], lam), k["fast_v"]) <= 1e-12
+    assert O.scale_dev(K.fast_S_update(k["fast_e_Phi"], k["fast_v"]), k["fast_S"]) <= 1e-12
+    ll = K.fast_log_likelihood(k["yt"], v, lam, k["logdet2"])
+    assert ll == pytest.approx(float(k["fast_ll"]), rel=1e-12)
+    mu, vn, Sr, ninv, nprod = K.fca_iteration(y, v, S, k["Sinv"], floor)
+    assert O.scale_dev(mu, k["fca_it_mu"]) <= 1e-12
+    assert O.scale_dev(vn, k["fca_it_v"]) <= 1e-12
+    assert O.scale_dev(Sr, k["fca_it_S"]) <= 1e-12
+    assert [ninv, nprod] == list(k["fca_it_counts"])
+    mu, vn, Sr, _, _ = K.fast_iteration(y, Pm, v, lam, floor)
+    assert O.scale_dev(mu, k["fast_it_mu"]) <= 1e-12
+    assert O.scale_dev(vn, k["fast_it_v"]) <= 1e-12
+    assert O.scale_dev(Sr, k["fast_it_S"]) <= 1e-12
+
+
+def test_gevd_matches_reference_pencils():
+    """Acceptance criterion 3 style (test_acceptance.py:97-154) on reference outputs."""
+    P = _pkg()
+    p = load_golden("pencils")
+    n = len([k for k in p if k.startswith("phi")])
+    for i in range(n):
+        phi, psi = p[f"phi{i}"], p[f"psi{i}"]
+        dec = P.gevd_hpd(phi, psi)
+        lam, Pm = dec.eigenvalues, dec.eigenvectors
+        d = lam.shape[0]
+        scale = max(np.abs(lam).max(), 1.0)
+        assert np.abs(lam - p[f"lam{i}"]).max() <= 1e-10 * scale
+        denom = np.linalg.norm(phi) + np.abs(lam).max() * np.linalg.norm(psi)
+        for k in range(d):
+            res = np.linalg.norm(phi @ Pm[:, k] - lam[k] * psi @ Pm[:, k])
+            assert res / denom <= 1e-10
+        assert np.abs(Pm.conj().T @ psi @ Pm - np.eye(d)).max() <= 1e-10
+        assert np.abs(Pm.conj().T @ phi @ Pm - np.diag(lam)).max() <= 1e-10 * scale
+        # phase convention: largest entry of each column real positive
+        for k in range(d):
+            lead = Pm[np.argmax(np.abs(Pm[:, k])), k]
+            assert lead.real > 0 and abs(lead.imag) <= 1e-12 * abs(lead)
+        gap = np.min(np.abs(np.diff(lam))) / scale
+        if gap > 1e-6:  # non-degenerate: eigenvectors unique up to the pinned phase
+            assert np.abs(Pm - p[f"P{i}"]).max() <= 1e-8 * np.abs(Pm).max()
+
+
+def test_gevd_errors_match_reference():
+    P = _pkg()
+    with pytest.raises(P.DefinitenessError) as exc:
+        P.gevd_hpd(np.eye(2, dtype=complex), np.diag([1.0, -0.5]).astype(complex))
+    assert exc.value.min_eigenvalue == pytest.approx(-0.5, abs=1e-12)
+    with pytest.raises(P.DefinitenessError):
+        P.gevd_hpd(np.eye(2, dtype=complex), np.diag([1.0, 1e-15]).astype(complex))
+    with pytest.raises(P.NonHermitianError):
+        P.gevd_hpd(np.array([[1.0, 1.0], [0.0, 1.0]], dtype=complex), np.eye(2, dtype=complex))
+
+
+def test_singular_mixture_names_the_point():
+    """reference test_conventional.py:111-120 and :51-60."""
+    P = _pkg()
+    y = np.ones((3, 2, 2), dtype=complex)
+    v = np.full((2, 3, 2), 1.0)
+    v[:, 1, 0] = 0.0
+    S = np.zeros((2, 2, 2, 2), dtype=complex)
+    S[:, :] = np.eye(2)
+    model = P.SpatialModel(v=v, S=S, v_floor=np.full(2, 0.0))
+    with pytest.raises(P.SingularMixtureError) as exc:
+        P.e_step(y, model)
+    assert (exc.value.frame, exc.value.bin) == (1, 0)
+    with pytest.raises(P.SingularMixtureError) as exc:
+        P.fca_run(y, model, 2)
+    assert (exc.value.frame, exc.value.bin) == (1, 0)
+    y = np.ones((2, 2, 2), dtype=complex)
+    S = np.zeros((2, 2, 2, 2), dtype=complex)
+    S[:, :] = np.eye(2)
+    S[:, 1] = 0.0
+    model = P.SpatialModel(v=np.full((2, 2, 2), 1.0), S=S, v_floor=np.full(2, 1e-12))
+    with pytest.raises(P.SingularMixtureError) as exc:
+        P.log_likelihood(y, model)
+    assert exc.value.bin == 1
+
+
+def test_silent_input_is_a_singular_matrix_error():
+    """reference test_cli.py silent input -> SingularMatrixError (fast.py:39-55)."""
+    P = _pkg()
+    y = np.zeros((8, 3, 2), dtype=complex)
+    init = P.init_random(y, 1)
+    with pytest.raises(P.SingularMatrixError):
+        P.fastfca_run(y, init, 2)
+
+
+def test_stage_api_matches_oracle():
+    """fast_e_step / fast_m_step_* / propagate_pencil / back transforms
+    (reference test_fast.py:70-182)."""
+    P = _pkg()
+    from paper_1805_06572_b200.fast import (back_transform_covariances, back_transform_images,
+                                            initial_pencil)
+
+    y, v, S = random_instance(26, n_frames=10, n_bins=2, n_chan=3)
+    floor = O.power_floor(y)
+    v = np.maximum(v, floor[None, None, :])
+    model = P.SpatialModel(v=v, S=S, v_floor=floor)
+    Pm, lam = initial_pencil(model)
+    lam_o, P_o = O.gevd_hpd(S[0], S[1])
+    assert np.abs(lam - lam_o).max() <= 1e-10 * np.abs(lam_o).max()
+    yt = P.transform_observations(y, Pm)
+    mu_t, phi_t = P.fast_e_step(yt, v, lam)
+    post = P.e_step(y, model)
+    mu_o, phi_o, _, _ = O.fca_e_step(y, v, S)
+    assert O.scale_dev(post.mu, mu_o) <= 1e-12
+    assert O.scale_dev(back_transform_images(mu_t, Pm), mu_o) <= 1e-10
+    new = P.m_step(post, model)
+    v_fast = np.maximum(P.fast_m_step_v(phi_t, lam), floor[None, None, :])
+    assert O.scale_dev(v_fast, new.v) <= 1e-10
+    gram = np.conj(np.swapaxes(Pm, -1, -2)) @ Pm
+    s_t = P.fast_m_step_S(phi_t, v_fast, gram=gram)
+    s_back = back_transform_covariances(s_t, Pm)
+    assert O.scale_dev(s_back, new.S) <= 1e-10
+    p_next, lam_next = P.propagate_pencil(s_t[0], s_t[1], Pm)
+    for f in range(2):
+        ph = p_next[f].conj().T
+        d1 = ph @ s_back[0, f] @ p_next[f]
+        d2 = ph @ s_back[1, f] @ p_next[f]
+        assert np.abs(d1 - np.diag(lam_next[f])).max() <= 1e-9 * max(np.abs(lam_next[f]).max(), 1)
+        assert np.abs(d2 - np.eye(3)).max() <= 1e-9
+
+
+def test_incremental_transform_close_to_literal():
+    """reference test_fast.py:239-245."""
+    P = _pkg()
+    y, v, S = random_instance(44, n_frames=8, n_bins=3, n_chan=2)
+    floor = O.power_floor(y)
+    model = P.SpatialModel(v=np.maximum(v, floor[None, None, :]), S=S, v_floor=floor)
+    lit = P.fastfca_run(y, model, 6)
+    inc = P.fastfca_run(y, model, 6, incremental_transform=True)
+    assert np.abs(inc.images - lit.images).max() <= 1e-8 * np.abs(lit.images).max()
+    assert _ll_dev(inc.loglik_trace, lit.loglik_trace) <= 1e-9
+
+
+def test_init_random_matches_oracle():
+    P = _pkg()
+    g = load_golden("runs_acc1")
+    m = P.init_random(g["y"], int(g["init_seed"]))
+    assert O.scale_dev(m.v, g["v0"]) <= 1e-14
+    assert O.scale_dev(m.S, g["S0"]) <= 1e-14
+    assert O.scale_dev(m.v_floor, g["floor"]) <= 1e-14
+
+
+def test_kernel_instance_shapes():
+    y, v, S, Pm, lam = kernel_instance()
+    assert y.shape == (9, 4, 3) and Pm.shape == (4, 3, 3)
