@@ -1,0 +1,357 @@
+#!/usr/bin/env python3
+"""Benchmark: EM TF-bin·iterations/s of the B200 FCA / FastFCA path.
+
+Workload (BASELINE.json configs[3], the largest single-GPU config the
+headline is quoted on): a batch of 256 independent 2-source mixtures,
+I=4, F=257, N=1250, L=20 EM iterations, complex128, FastFCA. One "step"
+is one complete ``fastfca_run`` over the batch — initial pencil, L fused
+iterations, separated images — with the likelihood off (the reference's
+``em_seconds`` boundary excludes it). Mixtures are sharded across ranks
+(``--gpus N`` under torchrun): no collective inside the EM loop.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--engine fast|fca] [--config 3] [--dtype c128|c64]
+
+Prints ONE JSON line on rank 0. ``value`` is measured with inputs resident
+in HBM; ``e2e`` goes through the public API with pinned host buffers (H2D of
+y and the init, D2H of images, v and S inside the timed region);
+``roofline`` is the fused FastFCA kernel's algorithmic bytes / its average
+launch time (CUDA events around the kernel inside the run); ``cpu_baseline``
+is the CPU oracle port timed on this host on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+from paper_1805_06572_b200.synth import CONFIGS, config_mixture, init_seed  # noqa: E402
+
+PEAKS = REPO / "MEASURED_PEAKS.json"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--engine", choices=["fast", "fca"], default="fast")
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--dtype", choices=["c128", "c64"], default="c128")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="mixtures/bins in the CPU sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def shard(cfg, rank, world):
+    """Mixture shard for config 3-like batches, bin shard for single mixtures."""
+    if cfg.M > 1:
+        per = cfg.M // world
+        extra = cfg.M % world
+        m0 = rank * per + min(rank, extra)
+        m1 = m0 + per + (1 if rank < extra else 0)
+        return ("mixtures", m0, m1)
+    per = cfg.F // world
+    extra = cfg.F % world
+    f0 = rank * per + min(rank, extra)
+    f1 = f0 + per + (1 if rank < extra else 0)
+    return ("bins", f0, f1)
+
+
+def make_inputs(cfg, sh, threads=16):
+    """Host inputs for this rank's shard: y (M,N,F,I), init v/S/floor (reference init_random)."""
+    from oracle.fastfca_oracle import init_random as host_init  # host-side init recipe
+
+    kind, a, b = sh
+    if kind == "mixtures":
+        mix = list(range(a, b))
+
+        def one(m):
+            y = config_mixture(cfg, m)
+            v, S, fl = host_init(y, init_seed(cfg, m))
+            return y, v, S, fl
+
+        with ThreadPoolExecutor(threads) as ex:
+            parts = list(ex.map(one, mix))
+        Y = np.stack([p[0] for p in parts])
+        V = np.stack([p[1] for p in parts])
+        S = np.stack([p[2] for p in parts])
+        FL = np.stack([p[3] for p in parts])
+        return Y, V, S, FL
+    y = config_mixture(cfg, 0)
+    v, S, fl = host_init(y, init_seed(cfg, 0))
+    return (np.ascontiguousarray(y[None, :, a:b]), np.ascontiguousarray(v[None, :, :, a:b]),
+            np.ascontiguousarray(S[None, :, a:b]), np.ascontiguousarray(fl[None, a:b]))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        d = json.loads(PEAKS.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_port_time(cfg, engine, sample, threads):
+    """Time the CPU oracle port (C restatement with OpenMP when built, else the
+    numpy restatement) on a bounded sample. Returns (tf_it_per_s, desc, kind, cores)."""
+    from oracle import cpu_port
+
+    return cpu_port.measure(cfg, engine, sample, threads)
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference algorithm on the host CPU (oracle port)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    from oracle import cpu_port
+
+    vals = []
+    desc = kind = None
+    for i in range(args.warmup + args.steps):
+        v, desc, kind, cores = cpu_port.measure(cfg, args.engine, args.cpu_sample, threads)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": f"EM TF-bin*iterations/s ({'FastFCA' if args.engine == 'fast' else 'FCA'}, config {cfg.index})",
+        "value": value, "unit": "TF-bin*it/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+        "dtype": "c128", "data": "synthetic (seeded, BASELINE.json recipe)",
+        "config": {"workload": cfg.description, "engine": args.engine, "iterations": cfg.L},
+        "cpu_baseline": {"value": value, "unit": "TF-bin*it/s", "cores": cores, "kind": kind,
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "TF-bin*it/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1805_06572_b200 import SpatialModel, fastfca_run, fca_run
+    from paper_1805_06572_b200._engine import run_device, torch_types
+
+    sh = shard(cfg, rank, world)
+    Y, V, S, FL = make_inputs(cfg, sh)
+    M, N, F, I = Y.shape
+    L = cfg.L
+    ctype, rtype = torch_types(args.dtype)
+    dev = torch.device("cuda", local)
+    y_d = torch.from_numpy(Y).to(dev).to(ctype)
+    v_d = torch.from_numpy(V).to(dev).to(rtype)
+    S_d = torch.from_numpy(S).to(dev)
+    fl_d = torch.from_numpy(FL).to(dev)
+    # the chunking the full (unsharded) problem would use -> identical per-bin sums
+    from paper_1805_06572_b200._engine import plan_chunks
+
+    cf, _ = plan_chunks(cfg.M * cfg.F, cfg.N)
+    tf_it_rank = M * F * N * L
+    tf_it_total = cfg.M * cfg.F * cfg.N * L
+
+    def step(timing=False):
+        return run_device(args.engine, y_d, v_d, S_d, fl_d, L, likelihood=False, history=False,
+                          images=True, dtype=args.dtype, timing=timing, check=False,
+                          chunk_frames=cf, kernel_timing=timing)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record()
+        runs = [step() for _ in range(args.steps)]
+        end.record()
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    from paper_1805_06572_b200._engine import status_of
+
+    status_of(runs[-1], N, F)
+    del runs
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_per_step = ms_max / args.steps
+    value = tf_it_total / (ms_per_step / 1e3)
+
+    # dominant-kernel roofline: events around each fused pass inside one run
+    kr = step(timing=True)
+    from paper_1805_06572_b200._engine import status_of as _st
+
+    _st(kr, N, F)
+    k_ms = kr.kernel_ms
+    k_avg = statistics.mean(k_ms) if k_ms else float("nan")
+    r = 8 if args.dtype == "c128" else 4  # bytes per real
+    bytes_per_tf = (2 * I + 4) * r  # read y (I complex), read v (2), write v (2)
+    alg_bytes = bytes_per_tf * M * F * N
+    achieved = alg_bytes / (k_avg / 1e3) / 1e9
+    peak, peak_kind = peaks()
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": "fast_em_kernel" if args.engine == "fast" else "fca_em_kernel",
+            "kernel_ms_avg": round(k_avg, 4), "bytes_per_tf_bin": bytes_per_tf,
+            "peak_source": peak_kind,
+            "iteration_ms_avg": round(statistics.mean(kr.iteration_ms), 4) if kr.iteration_ms
+            else None}
+    del kr
+    torch.cuda.empty_cache()
+
+    # end-to-end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        yh = torch.from_numpy(Y).to(ctype).pin_memory()
+        vh = torch.from_numpy(V).to(rtype).pin_memory()
+        Sh = torch.from_numpy(S).pin_memory()
+        flh = torch.from_numpy(FL).pin_memory()
+        model = SpatialModel(v=vh, S=Sh, v_floor=flh)
+        run = fastfca_run if args.engine == "fast" else fca_run
+        kw = dict(compute_likelihood=False, device_output=False, dtype=args.dtype,
+                  chunk_frames=cf)
+        run(yh, model, L, **kw)  # warm the pinned pools
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e_times = []
+        for _ in range(max(1, min(args.steps, 3))):
+            t0 = time.perf_counter()
+            res = run(yh, model, L, **kw)
+            e_times.append(time.perf_counter() - t0)
+        et = torch.tensor([statistics.median(e_times)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        h2d = yh.numel() * yh.element_size() + vh.numel() * vh.element_size() + \
+            Sh.numel() * Sh.element_size() + flh.numel() * flh.element_size()
+        d2h = res.images.nbytes + res.model.v.nbytes + res.model.S.nbytes
+        e2e = {"value": tf_it_total / float(et.item()), "unit": "TF-bin*it/s",
+               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+               "s_per_step": round(float(et.item()), 4)}
+        del res
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = len(os.sched_getaffinity(0))
+        v_cpu, desc, kind, cores = cpu_port_time(cfg, args.engine, args.cpu_sample, threads)
+        cpu = {"value": v_cpu, "unit": "TF-bin*it/s", "cores": cores, "kind": kind,
+               "sample": desc}
+
+    launches_per_step = 2 + 2 * L  # status init + initial pencil + L x (fused pass + pencil)
+    if rank == 0:
+        line = {
+            "metric": f"EM TF-bin*iterations/s ({'FastFCA' if args.engine == 'fast' else 'FCA'}, config {cfg.index})",
+            "value": value, "unit": "TF-bin*it/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic (seeded, BASELINE.json recipe)",
+            "config": {"workload": cfg.description, "engine": args.engine, "iterations": L,
+                       "M": cfg.M, "F": cfg.F, "N": cfg.N, "I": cfg.I,
+                       "parallelism": f"{sh[0]}-sharded x{world}",
+                       "l2": "inputs larger than L2 (y = %.2f GB)" % (Y.nbytes / 1e9 * world)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -96,6 +96,8 @@ typedef struct ffca_run_args {
   int64_t chunk_frames;     /* frames per reduction chunk; 0 = auto (ffca_plan_chunks).
                                Runs with equal chunk_frames give bitwise-identical per-bin
                                results however the bins / mixtures are sharded. */
+  void* const* kernel_events; /* optional cudaEvent_t[2L]: before/after each fused streaming
+                                 pass (the dominant kernel), for roofline timing */
 } ffca_run_args;
 
 /* ---- library info ------------------------------------------------------ */

@@ -41,10 +41,13 @@ class DeviceRun:
     v_hist: object = None  # (L,M,2,N,F)
     iteration_ms: list = field(default_factory=list)
     workspace: object = None
+    kernel_ms: list = field(default_factory=list)
+    floor: object = None
 
 
 def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, history=False,
-               images=True, dtype="c128", timing=True, check=True, out=None, chunk_frames=0):
+               images=True, dtype="c128", timing=True, check=True, out=None, chunk_frames=0,
+               kernel_timing=False):
     """Run ``iterations`` EM passes of FastFCA (``algorithm='fast'``) or
     conventional FCA (``'fca'``) entirely on the current CUDA stream.
 
@@ -103,6 +106,13 @@ def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, hi
         for e in evs:
             e.record()  # materialise the CUDA event handles
         ev_arr = (ctypes.c_void_p * (L + 1))(*[e.cuda_event for e in evs])
+    kevs = None
+    kev_arr = None
+    if kernel_timing and L:
+        kevs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * L)]
+        for e in kevs:
+            e.record()
+        kev_arr = (ctypes.c_void_p * (2 * L))(*[e.cuda_event for e in kevs])
     args = _lib.RunArgs(
         M=M, N=N, F=F, I=I, dtype=DTYPES[dtype], iterations=L, flags=flags,
         y=D.ptr(y).value, v=D.ptr(v).value, S0=D.ptr(S0).value, v_floor=D.ptr(fl).value,
@@ -110,7 +120,9 @@ def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, hi
         S_hist=D.ptr(S_hist).value, v_hist=D.ptr(v_hist).value,
         workspace=D.ptr(ws).value, workspace_bytes=wsz,
         iter_events=ctypes.cast(ev_arr, ctypes.c_void_p).value if ev_arr is not None else None,
-        chunk_frames=int(chunk_frames))
+        chunk_frames=int(chunk_frames),
+        kernel_events=ctypes.cast(kev_arr, ctypes.c_void_p).value if kev_arr is not None
+        else None)
     fn = lib.ffca_fastfca_run if fast else lib.ffca_fca_run
     D.check_rc(fn(ctypes.byref(args), D.stream_handle()), fn.__name__)
     run = DeviceRun("FastFCA" if fast else "FCA", img, v, S_out, ll, S_hist, v_hist, [], ws)
@@ -119,10 +131,21 @@ def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, hi
         D.check_rc(lib.ffca_run_status(D.ptr(ws), D.stream_handle(), ctypes.byref(st)),
                    "ffca_run_status")
         D.raise_for_status(st, N, F)
-        if evs is not None:
-            run.iteration_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(L)]
     run._events = evs
+    run._kevents = kevs
+    if check:
+        _collect_timings(run)
+    run._kevents = kevs
     return run
+
+
+def _collect_timings(run):
+    L = len(run._events) - 1 if run._events else 0
+    if run._events and not run.iteration_ms:
+        run.iteration_ms = [run._events[i].elapsed_time(run._events[i + 1]) for i in range(L)]
+    if run._kevents:
+        k = run._kevents
+        run.kernel_ms = [k[2 * i].elapsed_time(k[2 * i + 1]) for i in range(len(k) // 2)]
 
 
 def plan_chunks(G, N):
@@ -143,6 +166,7 @@ def status_of(run, N=None, F=None):
     D.check_rc(lib.ffca_run_status(D.ptr(run.workspace), D.stream_handle(), ctypes.byref(st)),
                "ffca_run_status")
     D.raise_for_status(st, N, F)
+    _collect_timings(run)
 
 
 def as_batch(y, init):

@@ -81,14 +81,15 @@ def _cholesky_inverse(S):
 
 
 def fca_run(y, init, iterations, record_history=False, compute_likelihood=True, dtype="c128",
-            device_output=None):
+            device_output=None, chunk_frames=0):
     """Conventional EM for ``iterations`` passes + MMSE images (conventional.py:104-164)."""
     yb, vb, Sb, fb, batched = as_batch(_data(y), init)
     if device_output is None:
         device_output = D.is_tensor(yb)
     L = int(iterations)
     run = run_device("fca", yb, vb, Sb, fb, L, likelihood=compute_likelihood,
-                     history=record_history, images=True, dtype=dtype)
+                     history=record_history, images=True, dtype=dtype,
+                     chunk_frames=chunk_frames)
     run.floor = D.to_device(fb, D.torch.float64)
     M, N, F = int(run.v.shape[0]), int(run.v.shape[2]), int(run.v.shape[3])
     mult = M if batched else 1

@@ -193,6 +193,7 @@ int ffca_fastfca_run(const ffca_run_args* a, void* stream) {
   const size_t Sslice = (size_t)M * 2 * F * I * I;  // complex entries per S snapshot
   const size_t vslice = (size_t)M * 2 * N * F;      // real entries per v snapshot
   cudaEvent_t* ev = (cudaEvent_t*)a->iter_events;
+  cudaEvent_t* kev = (cudaEvent_t*)a->kernel_events;
 
   if ((rc = reset_status(w.st, s))) return rc;
   FFCA_TRY(launch_initial_pencil((const double2*)a->S0, w.P, w.W, w.lam, w.logdet2, G, F, I,
@@ -232,7 +233,9 @@ int ffca_fastfca_run(const ffca_run_args* a, void* stream) {
       p.mu_out = (last && (fl & FFCA_FLAG_IMAGES)) ? a->images : nullptr;
       p.mu_back = 1;
       p.iter = l + 1;
+      if (kev) FFCA_TRY(cudaEventRecord(kev[2 * l], s));
       FFCA_TRY(launch_fast_em(p, I, a->dtype, s));
+      if (kev) FFCA_TRY(cudaEventRecord(kev[2 * l + 1], s));
       if (hist && a->v_hist)
         FFCA_TRY(cudaMemcpyAsync((char*)a->v_hist + (size_t)l * vslice * real_size(a->dtype),
                                  a->v, vslice * real_size(a->dtype), cudaMemcpyDeviceToDevice,
@@ -282,6 +285,7 @@ int ffca_fca_run(const ffca_run_args* a, void* stream) {
   const size_t Sslice = (size_t)M * 2 * F * I * I;
   const size_t vslice = (size_t)M * 2 * N * F;
   cudaEvent_t* ev = (cudaEvent_t*)a->iter_events;
+  cudaEvent_t* kev = (cudaEvent_t*)a->kernel_events;
 
   if ((rc = reset_status(w.st, s))) return rc;
   FFCA_TRY(launch_fca_prepare((const double2*)a->S0, w.Sp, G, F, I, w.st, 0, s));
@@ -315,7 +319,9 @@ int ffca_fca_run(const ffca_run_args* a, void* stream) {
       const bool last = (l == L - 1);
       p.mu_out = (last && (fl & FFCA_FLAG_IMAGES)) ? a->images : nullptr;
       p.iter = l + 1;
+      if (kev) FFCA_TRY(cudaEventRecord(kev[2 * l], s));
       FFCA_TRY(launch_fca_em(p, I, a->dtype, s));
+      if (kev) FFCA_TRY(cudaEventRecord(kev[2 * l + 1], s));
       if (hist && a->v_hist)
         FFCA_TRY(cudaMemcpyAsync((char*)a->v_hist + (size_t)l * vslice * real_size(a->dtype),
                                  a->v, vslice * real_size(a->dtype), cudaMemcpyDeviceToDevice,

@@ -169,7 +169,7 @@ def _finish(run, algorithm, L, batched, device_out, counts, record_history):
 
 
 def fastfca_run(y, init, iterations, record_history=False, compute_likelihood=True,
-                incremental_transform=False, dtype="c128", device_output=None):
+                incremental_transform=False, dtype="c128", device_output=None, chunk_frames=0):
     """Joint-diagonalisation EM + MMSE images (reference fast.py:156-260).
 
     ``dtype='c64'`` streams y / v / images in complex64 with float64 per-bin
@@ -183,7 +183,8 @@ def fastfca_run(y, init, iterations, record_history=False, compute_likelihood=Tr
         return _incremental_run(yb, vb, Sb, fb, L, batched, device_output, record_history,
                                 compute_likelihood)
     run = run_device("fast", yb, vb, Sb, fb, L, likelihood=compute_likelihood,
-                     history=record_history, images=True, dtype=dtype)
+                     history=record_history, images=True, dtype=dtype,
+                     chunk_frames=chunk_frames)
     run.floor = D.to_device(fb, D.torch.float64)
     M, F = int(run.v.shape[0]), int(run.v.shape[-1])
     counts = OpCounts()
