@@ -56,8 +56,8 @@ def test_library_is_sm100a():
 
 
 def test_run_args_layout_matches_c():
-    # 3 int64 + 4 int32 + 10 pointers + size_t + pointer + int64
-    assert ctypes.sizeof(_lib.RunArgs) == 24 + 16 + 8 * 10 + 8 + 8 + 8
+    # 3 int64 + 4 int32 + 10 pointers + size_t + pointer + int64 + pointer
+    assert ctypes.sizeof(_lib.RunArgs) == 24 + 16 + 8 * 10 + 8 + 8 + 8 + 8
 
 
 def test_workspace_size_query_needs_no_device():
