@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import argparse
 import os
+import re
 import subprocess
 import sys
 from concurrent.futures import ThreadPoolExecutor
@@ -42,15 +43,25 @@ def nvcc():
     return cand if Path(cand).exists() else "nvcc"
 
 
-def _deps():
-    return [*CSRC.glob("*.cuh"), INCLUDE / "fastfca_b200.h"]
+_INC = re.compile(r'^\s*#\s*include\s+"([^"]+)"', re.M)
+
+
+def _deps(src: Path, seen=None):
+    """Transitive quoted includes of ``src`` (for incremental rebuilds)."""
+    seen = set() if seen is None else seen
+    for name in _INC.findall(src.read_text()):
+        dep = (src.parent / name).resolve()
+        if dep.exists() and dep not in seen:
+            seen.add(dep)
+            _deps(dep, seen)
+    return seen
 
 
 def _needs(obj: Path, src: Path) -> bool:
     if not obj.exists():
         return True
     t = obj.stat().st_mtime
-    return any(p.stat().st_mtime > t for p in [src, *_deps()])
+    return any(p.stat().st_mtime > t for p in [src, *_deps(src)])
 
 
 def compile_one(src: Path, verbose_ptxas=False) -> Path:

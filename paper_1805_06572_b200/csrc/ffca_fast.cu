@@ -222,16 +222,24 @@ static cudaError_t launch_fast_em_t(const FastIterParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// v2 kernels for I <= 4 (ffca_fast2.cuh, instantiated in ffca_fast_i<I>.cu)
+template <int I, typename R>
+cudaError_t launch_fast2(const FastIterParams& p, cudaStream_t s);
+
 cudaError_t launch_fast_em(const FastIterParams& p, int I, int dtype, cudaStream_t s) {
+#define FFCA_CASE2(II)                                                      \
+  case II:                                                                  \
+    return dtype == FFCA_C64 ? launch_fast2<II, float>(p, s)                \
+                             : launch_fast2<II, double>(p, s);
 #define FFCA_CASE(II)                                                       \
   case II:                                                                  \
     return dtype == FFCA_C64 ? launch_fast_em_t<II, float>(p, s)            \
                              : launch_fast_em_t<II, double>(p, s);
   switch (I) {
-    FFCA_CASE(1)
-    FFCA_CASE(2)
-    FFCA_CASE(3)
-    FFCA_CASE(4)
+    FFCA_CASE2(1)
+    FFCA_CASE2(2)
+    FFCA_CASE2(3)
+    FFCA_CASE2(4)
     FFCA_CASE(5)
     FFCA_CASE(6)
     FFCA_CASE(7)
@@ -240,6 +248,7 @@ cudaError_t launch_fast_em(const FastIterParams& p, int I, int dtype, cudaStream
       return cudaErrorInvalidValue;
   }
 #undef FFCA_CASE
+#undef FFCA_CASE2
 }
 
 // ---- likelihood bookkeeping ------------------------------------------------

@@ -1,0 +1,7 @@
+// K3 v2 instantiations for I = 1 (separate TU so builds parallelise).
+#include "ffca_fast2.cuh"
+
+namespace ffca {
+template cudaError_t launch_fast2<1, double>(const FastIterParams&, cudaStream_t);
+template cudaError_t launch_fast2<1, float>(const FastIterParams&, cudaStream_t);
+}  // namespace ffca
