@@ -184,3 +184,97 @@ def as_batch(y, init):
     if nd == 4:
         return data, init.v, init.S, init.v_floor, True
     raise ConfigurationError("y must be (N, F, I) or (M, N, F, I)")
+
+
+def _host_tensor(x, dtype):
+    """numpy / CPU tensor -> contiguous CPU tensor of ``dtype`` (no copy when possible)."""
+    torch = D.torch
+    t = x if D.is_tensor(x) else torch.from_numpy(np.ascontiguousarray(x))
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.contiguous()
+
+
+def run_host_pipelined(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True,
+                       dtype="c128", chunk_frames=0, chunk_mixtures=None):
+    """Batched run from HOST buffers with transfers overlapped with compute.
+
+    The batch is split into mixture chunks; chunk k's EM run (compute stream)
+    overlaps the H2D copy of chunk k+1 and the D2H copy of chunk k-1's images
+    and model (two copy streams, double-buffered device slots). Results land
+    in pinned host memory. Inputs: y (M,N,F,I), v0 (M,2,N,F), S0 (M,2,F,I,I),
+    v_floor (M,F) as numpy or CPU tensors (pinned ones copy asynchronously).
+    Returns dict of numpy arrays: images, v, S, loglik (or None), iteration_ms.
+    """
+    torch = D.torch
+    D.require()
+    ctype, rtype = torch_types(dtype)
+    yh = _host_tensor(y, ctype)
+    vh = _host_tensor(v0, rtype)
+    Sh = _host_tensor(S0, torch.complex128)
+    fh = _host_tensor(v_floor, torch.float64)
+    M, N, F, I = (int(s) for s in yh.shape)
+    L = int(iterations)
+    if chunk_mixtures is None:
+        chunk_mixtures = max(1, min(M, (M + 7) // 8))
+    bounds = [(m0, min(M, m0 + chunk_mixtures)) for m0 in range(0, M, chunk_mixtures)]
+    cm = chunk_mixtures
+    dev = D.device()
+    pin = dict(pin_memory=True)
+    out_img = torch.empty((M, 2, N, F, I), dtype=ctype, **pin)
+    out_v = torch.empty((M, 2, N, F), dtype=rtype, **pin)
+    out_S = torch.empty((M, 2, F, I, I), dtype=torch.complex128, **pin)
+    out_ll = torch.empty((M, L + 1), dtype=torch.float64, **pin) if likelihood else None
+    pinned_in = yh.is_pinned() and vh.is_pinned()
+    s_h2d, s_cmp, s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    slots = []
+    for _ in range(2):
+        slots.append(dict(
+            y=torch.empty((cm, N, F, I), dtype=ctype, device=dev),
+            v=torch.empty((cm, 2, N, F), dtype=rtype, device=dev),
+            S0=torch.empty((cm, 2, F, I, I), dtype=torch.complex128, device=dev),
+            fl=torch.empty((cm, F), dtype=torch.float64, device=dev),
+            img=torch.empty((cm, 2, N, F, I), dtype=ctype, device=dev),
+            S=torch.empty((cm, 2, F, I, I), dtype=torch.complex128, device=dev),
+            free=torch.cuda.Event()))
+    runs = []
+    caller = torch.cuda.current_stream()
+    s_h2d.wait_stream(caller)
+    s_cmp.wait_stream(caller)
+    s_d2h.wait_stream(caller)
+    for k, (m0, m1) in enumerate(bounds):
+        sl = slots[k % 2]
+        c = m1 - m0
+        with torch.cuda.stream(s_h2d):
+            if k >= 2:
+                s_h2d.wait_event(sl["free"])
+            sl["y"][:c].copy_(yh[m0:m1], non_blocking=pinned_in)
+            sl["v"][:c].copy_(vh[m0:m1], non_blocking=pinned_in)
+            sl["S0"][:c].copy_(Sh[m0:m1], non_blocking=True)
+            sl["fl"][:c].copy_(fh[m0:m1], non_blocking=True)
+            ev_in = torch.cuda.Event()
+            ev_in.record(s_h2d)
+        with torch.cuda.stream(s_cmp):
+            s_cmp.wait_event(ev_in)
+            run = run_device(algorithm, sl["y"][:c], sl["v"][:c], sl["S0"][:c], sl["fl"][:c], L,
+                             likelihood=likelihood, history=False, images=True, dtype=dtype,
+                             timing=(k == 0), check=False, chunk_frames=chunk_frames,
+                             out={"images": sl["img"][:c], "S": sl["S"][:c]})
+            ev_cmp = torch.cuda.Event()
+            ev_cmp.record(s_cmp)
+        with torch.cuda.stream(s_d2h):
+            s_d2h.wait_event(ev_cmp)
+            out_img[m0:m1].copy_(sl["img"][:c], non_blocking=True)
+            out_v[m0:m1].copy_(run.v, non_blocking=True)
+            out_S[m0:m1].copy_(sl["S"][:c], non_blocking=True)
+            if likelihood:
+                out_ll[m0:m1].copy_(run.loglik, non_blocking=True)
+            sl["free"].record(s_d2h)
+        runs.append((run, c))
+    for s in (s_h2d, s_cmp, s_d2h):
+        s.synchronize()
+    for run, _ in runs:
+        status_of(run, N, F)
+    return {"images": out_img.numpy(), "v": out_v.numpy(), "S": out_S.numpy(),
+            "floor": fh.numpy(), "loglik": out_ll.numpy() if likelihood else None,
+            "iteration_ms": runs[0][0].iteration_ms, "chunks": len(bounds)}

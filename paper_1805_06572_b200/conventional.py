@@ -13,10 +13,10 @@ import numpy as np
 
 from . import _backend
 from . import _device as D
-from ._engine import as_batch, run_device
+from ._engine import as_batch, run_device, run_host_pipelined
 from ._kernels_cuda import SingularPointError
 from .errors import SingularMixtureError
-from .fast import _finish
+from .fast import _finish, _finish_host, _pipelined_ok
 from .modelops import regularize_covariances
 from .types import OpCounts, PosteriorMoments, SpatialModel
 
@@ -87,6 +87,10 @@ def fca_run(y, init, iterations, record_history=False, compute_likelihood=True, 
     if device_output is None:
         device_output = D.is_tensor(yb)
     L = int(iterations)
+    if _pipelined_ok(yb, batched, device_output, record_history):
+        return _finish_host(run_host_pipelined("fca", yb, vb, Sb, fb, L,
+                                               likelihood=compute_likelihood, dtype=dtype,
+                                               chunk_frames=chunk_frames), "FCA", L)
     run = run_device("fca", yb, vb, Sb, fb, L, likelihood=compute_likelihood,
                      history=record_history, images=True, dtype=dtype,
                      chunk_frames=chunk_frames)

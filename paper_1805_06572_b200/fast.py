@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _backend
 from . import _device as D
-from ._engine import as_batch, run_device, torch_types
+from ._engine import as_batch, run_device, run_host_pipelined, torch_types
 from .errors import SingularMatrixError
 from .modelops import COV_EPS_FACTOR  # noqa: F401  (re-exported like the reference)
 from .pencil import gevd_hpd, logdet2
@@ -182,6 +182,10 @@ def fastfca_run(y, init, iterations, record_history=False, compute_likelihood=Tr
     if incremental_transform:
         return _incremental_run(yb, vb, Sb, fb, L, batched, device_output, record_history,
                                 compute_likelihood)
+    if _pipelined_ok(yb, batched, device_output, record_history):
+        return _finish_host(run_host_pipelined("fast", yb, vb, Sb, fb, L,
+                                               likelihood=compute_likelihood, dtype=dtype,
+                                               chunk_frames=chunk_frames), "FastFCA", L)
     run = run_device("fast", yb, vb, Sb, fb, L, likelihood=compute_likelihood,
                      history=record_history, images=True, dtype=dtype,
                      chunk_frames=chunk_frames)
@@ -190,6 +194,30 @@ def fastfca_run(y, init, iterations, record_history=False, compute_likelihood=Tr
     counts = OpCounts()
     counts.add(gevds=L * F * (M if batched else 1), bin_products=2 * L * F * (M if batched else 1))
     return _finish(run, "FastFCA", L, batched, device_output, counts, record_history)
+
+
+def _pipelined_ok(yb, batched, device_output, record_history):
+    """Host-resident batches take the transfer/compute-overlapped path."""
+    on_host = not (D.is_tensor(yb) and yb.is_cuda)
+    return batched and on_host and not device_output and not record_history and \
+        int(yb.shape[0]) > 1
+
+
+def _finish_host(res, algorithm, L):
+    M, _, N, F = res["v"].shape
+    counts = OpCounts()
+    if algorithm == "FastFCA":
+        counts.add(gevds=L * F * M, bin_products=2 * L * F * M)
+    else:
+        counts.add(inversions=L * N * F * M, products=3 * L * N * F * M)
+        if L == 0:
+            counts.add(inversions=N * F * M, products=3 * N * F * M)
+    it_s = [ms / 1e3 for ms in res["iteration_ms"]]
+    return SeparationResult(
+        algorithm=algorithm, images=res["images"],
+        loglik_trace=res["loglik"] if res["loglik"] is not None else [],
+        iteration_seconds=it_s, em_seconds=float(sum(it_s)), op_counts=counts,
+        model=SpatialModel(v=res["v"], S=res["S"], v_floor=res["floor"]), history=[])
 
 
 def _incremental_run(yb, vb, Sb, fb, L, batched, device_output, record_history,
