@@ -66,44 +66,30 @@ def dist_env():
 
 
 def shard(cfg, rank, world):
-    """Mixture shard for config 3-like batches, bin shard for single mixtures."""
-    if cfg.M > 1:
-        per = cfg.M // world
-        extra = cfg.M % world
-        m0 = rank * per + min(rank, extra)
-        m1 = m0 + per + (1 if rank < extra else 0)
-        return ("mixtures", m0, m1)
-    per = cfg.F // world
-    extra = cfg.F % world
-    f0 = rank * per + min(rank, extra)
-    f1 = f0 + per + (1 if rank < extra else 0)
-    return ("bins", f0, f1)
+    """Mixture shard for config-3 batches, bin shard for single mixtures
+    (paper_1805_06572_b200.sharding)."""
+    from paper_1805_06572_b200.sharding import plan_shard
+
+    sh = plan_shard(cfg.M, cfg.F, rank, world)
+    return (sh.axis, sh.start, sh.stop)
 
 
 def make_inputs(cfg, sh, threads=16):
-    """Host inputs for this rank's shard: y (M,N,F,I), init v/S/floor (reference init_random)."""
-    from oracle.fastfca_oracle import init_random as host_init  # host-side init recipe
+    """This rank's shard: y (M,N,F,I) drawn on the host (seeded generator) and
+    the reference init_random model computed by the package on the device.
+    Returns host numpy arrays (y, v, S, floor)."""
+    from paper_1805_06572_b200.initializers import init_random_batch
+    from paper_1805_06572_b200.sharding import Shard, take
 
     kind, a, b = sh
     if kind == "mixtures":
-        mix = list(range(a, b))
-
-        def one(m):
-            y = config_mixture(cfg, m)
-            v, S, fl = host_init(y, init_seed(cfg, m))
-            return y, v, S, fl
-
         with ThreadPoolExecutor(threads) as ex:
-            parts = list(ex.map(one, mix))
-        Y = np.stack([p[0] for p in parts])
-        V = np.stack([p[1] for p in parts])
-        S = np.stack([p[2] for p in parts])
-        FL = np.stack([p[3] for p in parts])
-        return Y, V, S, FL
-    y = config_mixture(cfg, 0)
-    v, S, fl = host_init(y, init_seed(cfg, 0))
-    return (np.ascontiguousarray(y[None, :, a:b]), np.ascontiguousarray(v[None, :, :, a:b]),
-            np.ascontiguousarray(S[None, :, a:b]), np.ascontiguousarray(fl[None, a:b]))
+            Y = np.stack(list(ex.map(lambda m: config_mixture(cfg, m), range(a, b))))
+        model = init_random_batch(Y, [init_seed(cfg, m) for m in range(a, b)])
+        return Y, model.v, model.S, model.v_floor
+    y = config_mixture(cfg, 0)[None]
+    model = init_random_batch(y, [init_seed(cfg, 0)])
+    return take(Shard(kind, a, b), y, model.v, model.S, model.v_floor)
 
 
 class ClockSampler:
@@ -241,10 +227,17 @@ def main():
     tf_it_rank = M * F * N * L
     tf_it_total = cfg.M * cfg.F * cfg.N * L
 
+    # outputs and workspace are allocated once: a step is the EM run, not cudaMalloc
+    bufs = {"images": torch.empty((M, 2, N, F, I), dtype=ctype, device=dev),
+            "S": torch.empty((M, 2, F, I, I), dtype=torch.complex128, device=dev),
+            "v": torch.empty_like(v_d)}
+
     def step(timing=False):
         return run_device(args.engine, y_d, v_d, S_d, fl_d, L, likelihood=False, history=False,
                           images=True, dtype=args.dtype, timing=timing, check=False,
-                          chunk_frames=cf, kernel_timing=timing)
+                          chunk_frames=cf, kernel_timing=timing, out=bufs)
+
+    bufs["workspace"] = step().workspace
 
     for _ in range(args.warmup):
         step()
@@ -256,14 +249,15 @@ def main():
     end = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         start.record()
-        runs = [step() for _ in range(args.steps)]
+        for _ in range(args.steps):
+            last = step()
         end.record()
         torch.cuda.synchronize()
     ms = start.elapsed_time(end)
     from paper_1805_06572_b200._engine import status_of
 
-    status_of(runs[-1], N, F)
-    del runs
+    status_of(last, N, F)
+    del last
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -304,7 +298,11 @@ def main():
         run = fastfca_run if args.engine == "fast" else fca_run
         kw = dict(compute_likelihood=False, device_output=False, dtype=args.dtype,
                   chunk_frames=cf)
-        run(yh, model, L, **kw)  # warm the pinned pools
+        res = run(yh, model, L, **kw)  # warm the pinned pools
+        h2d = yh.numel() * yh.element_size() + vh.numel() * vh.element_size() + \
+            Sh.numel() * Sh.element_size() + flh.numel() * flh.element_size()
+        d2h = res.images.nbytes + res.model.v.nbytes + res.model.S.nbytes
+        del res  # results go back to the pinned cache: steady state, not cudaHostAlloc
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -313,16 +311,13 @@ def main():
             t0 = time.perf_counter()
             res = run(yh, model, L, **kw)
             e_times.append(time.perf_counter() - t0)
+            del res
         et = torch.tensor([statistics.median(e_times)], device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        h2d = yh.numel() * yh.element_size() + vh.numel() * vh.element_size() + \
-            Sh.numel() * Sh.element_size() + flh.numel() * flh.element_size()
-        d2h = res.images.nbytes + res.model.v.nbytes + res.model.S.nbytes
         e2e = {"value": tf_it_total / float(et.item()), "unit": "TF-bin*it/s",
                "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
                "s_per_step": round(float(et.item()), 4)}
-        del res
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -70,9 +70,13 @@ def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, hi
     L = int(iterations)
     if L < 0:
         raise ConfigurationError("iterations must be >= 0")
+    res = out or {}
     v = D.to_device(v0, rtype)
-    if D.is_tensor(v0) and v.data_ptr() == v0.data_ptr():
-        v = v.clone()  # the run updates v in place; never clobber the caller's init
+    if res.get("v") is not None:
+        res["v"].copy_(v)  # preallocated work buffer: the run updates v in place
+        v = res["v"]
+    elif D.is_tensor(v0) and v.data_ptr() == v0.data_ptr():
+        v = v.clone()  # never clobber the caller's init
     S0 = D.to_device(S0, torch.complex128)
     fl = D.to_device(v_floor, torch.float64)
     if tuple(v.shape) != (M, 2, N, F) or tuple(S0.shape) != (M, 2, F, I, I) or \
@@ -90,13 +94,15 @@ def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, hi
     fast = algorithm == "fast"
     wsz = (lib.ffca_fastfca_workspace_size if fast else lib.ffca_fca_workspace_size)(
         M, N, F, I, L, flags, int(chunk_frames))
-    ws = D.workspace(wsz)
-    res = out or {}
+    ws = res.get("workspace")
+    if ws is None or ws.numel() < wsz:
+        ws = D.workspace(wsz)
     img = res.get("images") if images else None
     if images and img is None:
         img = D.empty((M, 2, N, F, I), ctype)
     S_out = res.get("S") if res.get("S") is not None else D.empty((M, 2, F, I, I), torch.complex128)
-    ll = D.empty((M, L + 1), torch.float64) if likelihood else None
+    ll = (res.get("loglik") if res.get("loglik") is not None else
+          D.empty((M, L + 1), torch.float64)) if likelihood else None
     S_hist = D.empty((L, M, 2, F, I, I), torch.complex128) if (history and L) else None
     v_hist = D.empty((L, M, 2, N, F), rtype) if (history and L) else None
     evs = None

@@ -49,7 +49,7 @@ struct Carve {
 
 struct FastWs {
   ffca_status_dev* st;
-  double2 *P, *W;
+  double2 *P, *W, *St;
   double *lam, *logdet2, *Spart, *llbin, *llg;
   int64_t chunk_frames;
   int nchunk;
@@ -80,6 +80,7 @@ FastWs carve_fast(void* base, int64_t M, int64_t N, int64_t F, int I, int L, uns
   const bool ll = flags & FFCA_FLAG_LIKELIHOOD;
   w.llbin = ll ? c.take<double>((size_t)w.nchunk * G) : nullptr;
   w.llg = ll ? c.take<double>((size_t)(L + 1) * G) : nullptr;
+  w.St = I >= 5 ? c.take<double2>((size_t)2 * G * I * I) : nullptr;
   w.bytes = c.off;
   return w;
 }
@@ -250,12 +251,13 @@ int ffca_fastfca_run(const ffca_run_args* a, void* stream) {
       q.W = w.W;
       q.lam = w.lam;
       q.logdet2 = w.logdet2;
-      q.S_model = (double2*)a->S_out;
+      q.S_model = (l == L - 1) ? (double2*)a->S_out : nullptr;  // model S = last iteration's
       q.S_hist = (hist && a->S_hist) ? (double2*)a->S_hist + (size_t)l * Sslice : nullptr;
       q.llbin = ll ? w.llbin : nullptr;
       q.llg = ll ? w.llg + (size_t)l * G : nullptr;
       q.st = w.st;
       q.iter = l + 1;
+      q.St = w.St;
       FFCA_TRY(launch_pencil_update(q, I, s));
     }
     if (ev) FFCA_TRY(cudaEventRecord(ev[L], s));

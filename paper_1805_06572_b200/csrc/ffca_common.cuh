@@ -189,22 +189,22 @@ template <int I>
 FFCA_DEV void jacobi_herm(double2 (&A)[I][I], double2 (&V)[I][I]) {
   set_identity<I>(V);
   if (I == 1) return;
-  for (int sweep = 0; sweep < 40; ++sweep) {
-    double off = 0.0, dia = 0.0;
-#pragma unroll
-    for (int p = 0; p < I; ++p) {
-      dia += A[p][p].x * A[p][p].x;
-#pragma unroll
-      for (int q = p + 1; q < I; ++q) off += cabs2(A[p][q]);
-    }
-    if (!(off > 1e-36 * dia)) break;  // converged (also exits on NaN)
+  // Rotate (p, q) only while |a_pq| exceeds eps * sqrt(|a_pp a_qq|) (the
+  // Demmel-Veselic threshold: every eigenvalue then carries high relative
+  // accuracy); stop after a sweep without rotations. A fixed "off(A) < tiny"
+  // test would never trigger: rotations keep re-creating roundoff-level
+  // off-diagonal entries.
+  constexpr double kTol2 = 1e-32;  // (1e-16)^2
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    bool rotated = false;
 #pragma unroll
     for (int p = 0; p < I - 1; ++p) {
 #pragma unroll
       for (int q = p + 1; q < I; ++q) {
         const double2 apq = A[p][q];
         const double mag2 = cabs2(apq);
-        if (mag2 > 0.0) {
+        if (mag2 > kTol2 * fabs(A[p][p].x * A[q][q].x) && mag2 > 0.0) {
+          rotated = true;
           const double mag = sqrt(mag2);
           // e^{-i phi} where apq = |apq| e^{i phi}
           const double2 emi = cmk(apq.x / mag, -apq.y / mag);
@@ -246,6 +246,7 @@ FFCA_DEV void jacobi_herm(double2 (&A)[I][I], double2 (&V)[I][I]) {
         }
       }
     }
+    if (!rotated) break;  // converged (NaN input also stops: comparisons fail)
   }
 }
 
@@ -295,14 +296,16 @@ FFCA_DEV void fix_column_phases(double2 (&P)[I][I]) {
   }
 }
 
-// Hermitian-definite pencil decomposition (reference pencil.py:85-135):
-// eig(Psi) -> definiteness floor -> whiten Phi -> eig -> descending ->
-// P = U Sigma^{-1/2} Q -> column phases. Psi is read from its lower triangle
-// (as LAPACK zheevd does for numpy.linalg.eigh); Phi is used in full.
-// Returns 0, or 3 (definiteness) with *min_sigma set.
+// Hermitian-definite pencil decomposition, eigen-whitening variant (the
+// reference's own construction, pencil.py:85-135): eig(Psi) -> definiteness
+// floor -> whiten Phi -> eig -> descending -> P = U Sigma^{-1/2} Q -> column
+// phases. Psi is read from its lower triangle (as LAPACK zheevd does for
+// numpy.linalg.eigh); Phi is used in full. Returns 0, or 3 (definiteness)
+// with *min_sigma set. Used when the Cholesky path below cannot certify
+// definiteness cheaply.
 template <int I>
-FFCA_DEV int gevd_hpd(const double2 (&Phi)[I][I], const double2 (&Psi)[I][I], double (&lam)[I],
-                      double2 (&P)[I][I], double* min_sigma) {
+FFCA_DEV int gevd_hpd_eig(const double2 (&Phi)[I][I], const double2 (&Psi)[I][I], double (&lam)[I],
+                          double2 (&P)[I][I], double* min_sigma) {
   double2 A[I][I];
   double tr = 0.0;
 #pragma unroll
@@ -355,6 +358,84 @@ FFCA_DEV int gevd_hpd(const double2 (&Phi)[I][I], const double2 (&Psi)[I][I], do
 #pragma unroll
     for (int b = 0; b < I; ++b) T[a][b] = cscale(U[a][b], isq[b]);
   matmul<I>(T, Q, P);
+  fix_column_phases<I>(P);
+  return 0;
+}
+
+template <int I>
+FFCA_DEV bool cholesky(const double2 (&A)[I][I], double2 (&L)[I][I]);
+template <int I>
+FFCA_DEV void tril_inverse(const double2 (&L)[I][I], double2 (&Li)[I][I]);
+
+// Hermitian-definite pencil decomposition (reference pencil.py:85-135),
+// Cholesky-whitened like LAPACK zhegv: Psi = L L^H, eig(L^-1 Phi L^-H) = Q
+// diag(lam) Q^H, P = L^-H Q, descending order, column phases pinned. The
+// generalized eigenpairs are the reference's (unique up to the pinned phase
+// for distinct lam); one Jacobi eigensolve instead of two. Definiteness
+// (reference: min eig(Psi) > 1e-12 tr(Psi)/D) is certified by the bound
+// lambda_min(Psi) >= 1 / tr(Psi^-1) = 1 / ||L^-1||_F^2; when the bound cannot
+// certify it, the exact eigenvalues decide (gevd_hpd_eig).
+template <int I>
+FFCA_DEV int gevd_hpd(const double2 (&Phi)[I][I], const double2 (&Psi)[I][I], double (&lam)[I],
+                      double2 (&P)[I][I], double* min_sigma) {
+  double tr = 0.0;
+#pragma unroll
+  for (int a = 0; a < I; ++a) tr += Psi[a][a].x;
+  const double thr = kDefFloor * tr / I;
+  double2 L[I][I], Li[I][I];
+  bool certified = cholesky<I>(Psi, L);
+  if (certified) {
+    tril_inverse<I>(L, Li);
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < I; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b) s += cabs2(Li[a][b]);
+    certified = (1.0 / s) > thr;
+  }
+  if (!certified) return gevd_hpd_eig<I>(Phi, Psi, lam, P, min_sigma);
+  *min_sigma = 0.0;
+  // Wh = Li Phi Li^H (Li lower triangular), re-symmetrised
+  double2 T[I][I], Wh[I][I];
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      double2 acc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k <= a; ++k) acc = cadd(acc, cmul(Li[a][k], Phi[k][b]));
+      T[a][b] = acc;
+    }
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = a; b < I; ++b) {
+      double2 acc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k <= b; ++k) acc = cadd(acc, cmulc(T[a][k], Li[b][k]));
+      Wh[a][b] = acc;
+    }
+#pragma unroll
+  for (int a = 0; a < I; ++a) {
+    Wh[a][a] = cmk(Wh[a][a].x, 0.0);
+#pragma unroll
+    for (int b = a + 1; b < I; ++b) Wh[b][a] = cconj(Wh[a][b]);
+  }
+  double2 Q[I][I];
+  jacobi_herm<I>(Wh, Q);
+#pragma unroll
+  for (int a = 0; a < I; ++a) lam[a] = Wh[a][a].x;
+  sort_desc<I>(lam, Q);
+  // P = Li^H Q (Li^H upper triangular)
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      double2 acc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int k = a; k < I; ++k) acc = cadd(acc, cconjmul(Li[k][a], Q[k][b]));
+      P[a][b] = acc;
+    }
   fix_column_phases<I>(P);
   return 0;
 }

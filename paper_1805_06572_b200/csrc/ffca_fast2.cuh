@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) fast_em2_kernel(const FastIterP
         lprod *= den;
         quad = fma(pz, rden, quad);
       }
-      bad |= (den == 0.0);
+      // den == 0 needs no test: rcp_nr(0) is NaN and poisons w below
     }
     if (LL) llacc += log(lprod) + quad;
     if (UPDATE) {
@@ -202,7 +202,11 @@ __global__ void __launch_bounds__(WARPS * 32, 3) fast_em2_kernel(const FastIterP
         vb[n * p.F] = (R)w1;
         vb[NF + n * p.F] = (R)w2;
       }
-      bad |= !(isfinite(w1) && isfinite(w2) && w1 > 0.0 && w2 > 0.0);
+      {  // non-finite or non-positive w (integer tests keep the FP64 pipe free)
+        const long long b1 = __double_as_longlong(w1), b2 = __double_as_longlong(w2);
+        bad |= (((b1 >> 52) & 0x7ff) == 0x7ff) | (((b2 >> 52) & 0x7ff) == 0x7ff) | (b1 <= 0) |
+               (b2 <= 0);
+      }
       const double iw1 = rcp_nr(w1), iw2 = rcp_nr(w2);
       double h1[I], h2[I];
 #pragma unroll

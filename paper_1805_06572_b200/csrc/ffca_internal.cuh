@@ -65,6 +65,7 @@ struct PencilParams {
   int64_t F;
   ffca_status_dev* st;
   int iter;
+  double2* St;  // [2][G][I][I] scratch for the split path (I >= 5)
 };
 cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s);
 

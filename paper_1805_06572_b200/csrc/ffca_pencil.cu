@@ -10,16 +10,18 @@
 
 namespace ffca {
 
+// Steps shared by the fused (I <= 4) and split (I >= 5) pencil updates:
+// chunk partials -> S~ (/N), ridge with eps*gram, model / history covariances,
+// likelihood collect. Leaves S_t in S1/S2 and P_e in Pe.
 template <int I>
-__global__ void __launch_bounds__(64) pencil_update_kernel(const PencilParams p) {
+FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
+                          double2 (&S2)[I][I], double2 (&Pe)[I][I]) {
   constexpr int NP = I * I;
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= p.G) return;
   const int64_t G = p.G;
   const int64_t m = g / p.F, f = g - m * p.F;
 
+
   // 1. reduce partials
-  double2 S1[I][I], S2[I][I];
   {
     double s[2][NP];
 #pragma unroll
@@ -51,7 +53,7 @@ __global__ void __launch_bounds__(64) pencil_update_kernel(const PencilParams p)
     p.llg[g] = (double)p.N * p.logdet2[g] - s;
   }
 
-  double2 Pe[I][I], We[I][I];
+  double2 We[I][I];
 #pragma unroll
   for (int a = 0; a < I; ++a)
 #pragma unroll
@@ -60,30 +62,25 @@ __global__ void __launch_bounds__(64) pencil_update_kernel(const PencilParams p)
       We[a][b] = p.W[g * NP + a * I + b];
     }
 
-  // 2. ridge eps_j = 1e-9 tr(gram^{-1} S~_j)/I = 1e-9 tr(W S~_j W^H)/I, and
-  //    the back-transformed model covariance W (S~_j + eps_j gram) W^H
-  //    = W S~_j W^H + eps_j Id.
+  // 2. ridge eps_j = 1e-9 tr(gram^{-1} S~_j)/I with gram^{-1} = W^H W
+  //    (W = P^{-H}), then S_t = S~ + eps_j gram (fast.py:80-90).
   double eps[2];
+  {
+    double2 H[I][I];
+    matmul_hn<I>(We, We, H);
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    double2 T[I][I], Sb[I][I];
-    matmul_nh<I>(j == 0 ? S1 : S2, We, T);  // S~ W^H
-    matmul<I>(We, T, Sb);                   // W S~ W^H
-    double tr = 0.0;
+    for (int j = 0; j < 2; ++j) {
+      const double2(&Sj)[I][I] = j == 0 ? S1 : S2;
+      double tr = 0.0;
 #pragma unroll
-    for (int a = 0; a < I; ++a) tr += Sb[a][a].x;
-    eps[j] = kCovEps * tr / I;
-    double2* dst = p.S_model + ((m * 2 + j) * p.F + f) * NP;
-    double2* hst = p.S_hist ? p.S_hist + ((m * 2 + j) * p.F + f) * NP : nullptr;
+      for (int a = 0; a < I; ++a) {
+        tr += Sj[a][a].x * H[a][a].x;
 #pragma unroll
-    for (int a = 0; a < I; ++a)
-#pragma unroll
-      for (int b = 0; b < I; ++b) {
-        double2 val = Sb[a][b];
-        if (a == b) val.x += eps[j];
-        dst[a * I + b] = val;
-        if (hst) hst[a * I + b] = val;
+        for (int b = a + 1; b < I; ++b)  // S_ab H_ba + S_ba H_ab = 2 Re(S_ab H_ba)
+          tr += 2.0 * (Sj[a][b].x * H[b][a].x - Sj[a][b].y * H[b][a].y);
       }
+      eps[j] = kCovEps * tr / I;
+    }
   }
   {
     double2 gram[I][I];
@@ -91,13 +88,49 @@ __global__ void __launch_bounds__(64) pencil_update_kernel(const PencilParams p)
 #pragma unroll
     for (int a = 0; a < I; ++a)
 #pragma unroll
-      for (int b = 0; b < I; ++b) {
-        // use the upper triangle of gram for both halves (exactly Hermitian)
-        const double2 gab = (a <= b) ? gram[a][b] : cconj(gram[b][a]);
-        S1[a][b] = cadd(S1[a][b], cscale(gab, eps[0]));
-        S2[a][b] = cadd(S2[a][b], cscale(gab, eps[1]));
+      for (int b = a; b < I; ++b) {
+        // upper triangle of gram, mirrored: S_t stays exactly Hermitian
+        S1[a][b] = cadd(S1[a][b], cscale(gram[a][b], eps[0]));
+        S2[a][b] = cadd(S2[a][b], cscale(gram[a][b], eps[1]));
+        if (b > a) {
+          S1[b][a] = cconj(S1[a][b]);
+          S2[b][a] = cconj(S2[a][b]);
+        } else {
+          S1[a][a].y = 0.0;
+          S2[a][a].y = 0.0;
+        }
       }
   }
+  // model / history covariance back in the original basis: W S_t W^H
+  // (fast.py:144-148), only when someone reads it
+  if (p.S_model || p.S_hist) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double2 T[I][I], Sb[I][I];
+      matmul_nh<I>(j == 0 ? S1 : S2, We, T);
+      matmul<I>(We, T, Sb);
+      double2* dst = p.S_model ? p.S_model + ((m * 2 + j) * p.F + f) * NP : nullptr;
+      double2* hst = p.S_hist ? p.S_hist + ((m * 2 + j) * p.F + f) * NP : nullptr;
+#pragma unroll
+      for (int a = 0; a < I; ++a)
+#pragma unroll
+        for (int b = 0; b < I; ++b) {
+          if (dst) dst[a * I + b] = Sb[a][b];
+          if (hst) hst[a * I + b] = Sb[a][b];
+        }
+    }
+  }
+
+  return true;
+}
+
+template <int I>
+__global__ void __launch_bounds__(64) pencil_update_kernel(const PencilParams p) {
+  constexpr int NP = I * I;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= p.G) return;
+  double2 S1[I][I], S2[I][I], Pe[I][I];
+  pencil_prep<I>(p, g, S1, S2, Pe);
 
   // 3. GEVD of the transformed pencil, P <- P Q
   double lam[I];
@@ -123,6 +156,23 @@ __global__ void __launch_bounds__(64) pencil_update_kernel(const PencilParams p)
     }
   }
   p.logdet2[g] = 2.0 * lad;
+}
+
+// split path, step 1: S_t -> scratch [2][G][I][I]
+template <int I>
+__global__ void __launch_bounds__(64) pencil_prep_kernel(const PencilParams p) {
+  constexpr int NP = I * I;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= p.G) return;
+  double2 S1[I][I], S2[I][I], Pe[I][I];
+  pencil_prep<I>(p, g, S1, S2, Pe);
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      p.St[g * NP + a * I + b] = S1[a][b];
+      p.St[(p.G + g) * NP + a * I + b] = S2[a][b];
+    }
 }
 
 template <int I>
@@ -220,8 +270,34 @@ __global__ void __launch_bounds__(64)
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+template <int I>
+__global__ void gevd_batch_kernel(const double2* Phi, const double2* Psi, double* lam,
+                                  double2* P, const double2* Pprev, int64_t B, int check,
+                                  ffca_status_dev* st, int iter);
+template <int I>
+__global__ void inverse_h_kernel(const double2* P, double2* W, double* logdet2, int64_t B,
+                                 ffca_status_dev* st, int iter);
+
 cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s) {
-  FFCA_DISPATCH_I(I, (pencil_update_kernel<II><<<nblk(p.G, 64), 64, 0, s>>>(p)));
+  if (I <= 4) {  // fused single kernel; only instantiated for I <= 4
+    const unsigned nb = nblk(p.G, 64);
+    switch (I) {
+      case 1: pencil_update_kernel<1><<<nb, 64, 0, s>>>(p); break;
+      case 2: pencil_update_kernel<2><<<nb, 64, 0, s>>>(p); break;
+      case 3: pencil_update_kernel<3><<<nb, 64, 0, s>>>(p); break;
+      default: pencil_update_kernel<4><<<nb, 64, 0, s>>>(p); break;
+    }
+    return cudaGetLastError();
+  }
+  // I >= 5: three leaner kernels (S_t, GEVD + P Q, P^{-H} + log|det P|^2)
+  const unsigned nb = nblk(p.G, 64);
+  const double2* St1 = p.St;
+  const double2* St2 = p.St + p.G * (int64_t)I * I;
+  FFCA_DISPATCH_I(I, (pencil_prep_kernel<II><<<nb, 64, 0, s>>>(p)));
+  FFCA_DISPATCH_I(I, (gevd_batch_kernel<II><<<nb, 64, 0, s>>>(St1, St2, p.lam, p.P, p.P, p.G, 0,
+                                                              p.st, p.iter)));
+  FFCA_DISPATCH_I(I, (inverse_h_kernel<II><<<nb, 64, 0, s>>>(p.P, p.W, p.logdet2, p.G, p.st,
+                                                             p.iter)));
   return cudaGetLastError();
 }
 
@@ -239,7 +315,7 @@ cudaError_t launch_initial_pencil(const double2* S0, double2* P, double2* W, dou
 template <int I>
 __global__ void gevd_batch_kernel(const double2* Phi, const double2* Psi, double* lam,
                                   double2* P, const double2* Pprev, int64_t B, int check,
-                                  ffca_status_dev* st) {
+                                  ffca_status_dev* st, int iter) {
   constexpr int NP = I * I;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= B) return;
@@ -263,7 +339,7 @@ __global__ void gevd_batch_kernel(const double2* Phi, const double2* Psi, double
         as2 = fmax(as2, sqrt(cabs2(csub(Bm[a][b], cconj(Bm[b][a])))));
       }
     if ((as1 > kHermRtol * fmax(sc1, 1e-300)) || (as2 > kHermRtol * fmax(sc2, 1e-300))) {
-      if (st) report_error(st, 0, FFCA_ERR_NON_HERMITIAN, (unsigned long long)g);
+      if (st) report_error(st, iter, FFCA_ERR_NON_HERMITIAN, (unsigned long long)g);
       return;
     }
   }
@@ -272,7 +348,7 @@ __global__ void gevd_batch_kernel(const double2* Phi, const double2* Psi, double
   double msig = 0.0;
   const int rc = gevd_hpd<I>(A, Bm, l, Q, &msig);
   if (rc != 0 && st) {
-    report_error(st, 0, rc, (unsigned long long)g);
+    report_error(st, iter, rc, (unsigned long long)g);
     report_min_value(st, msig);
   }
   if (Pprev) {
@@ -388,7 +464,7 @@ __global__ void reg_transformed_kernel(const double2* S, const double2* gram, do
 // W = (P^{-1})^H per bin; logdet2 optional
 template <int I>
 __global__ void inverse_h_kernel(const double2* P, double2* W, double* logdet2, int64_t B,
-                                 ffca_status_dev* st) {
+                                 ffca_status_dev* st, int iter) {
   constexpr int NP = I * I;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= B) return;
@@ -399,7 +475,7 @@ __global__ void inverse_h_kernel(const double2* P, double2* W, double* logdet2, 
     for (int b = 0; b < I; ++b) A[a][b] = P[g * NP + a * I + b];
   double lad = 0.0;
   const bool ok = lu_inverse<I>(A, Inv, &lad);
-  if (!ok && st) report_error(st, 0, FFCA_ERR_SINGULAR_BASIS, (unsigned long long)g);
+  if (!ok && st) report_error(st, iter, FFCA_ERR_SINGULAR_BASIS, (unsigned long long)g);
   if (W) {
 #pragma unroll
     for (int a = 0; a < I; ++a)
@@ -457,7 +533,7 @@ cudaError_t launch_gevd_batch(const double2* Phi, const double2* Psi, double* la
                               const double2* Pprev, int64_t B, int I, int check,
                               ffca_status_dev* st, cudaStream_t s) {
   FFCA_DISPATCH_I(I, (gevd_batch_kernel<II><<<nblk(B, 64), 64, 0, s>>>(Phi, Psi, lam, P, Pprev,
-                                                                        B, check, st)));
+                                                                        B, check, st, 0)));
   return cudaGetLastError();
 }
 cudaError_t launch_cholinv(const double2* S, double2* Sinv, int64_t B, int I, ffca_status_dev* st,
@@ -476,7 +552,7 @@ cudaError_t launch_reg_transformed(const double2* S, const double2* gram, double
 }
 cudaError_t launch_inverse_h(const double2* P, double2* W, double* logdet2, int64_t B, int I,
                              ffca_status_dev* st, cudaStream_t s) {
-  FFCA_DISPATCH_I(I, (inverse_h_kernel<II><<<nblk(B, 64), 64, 0, s>>>(P, W, logdet2, B, st)));
+  FFCA_DISPATCH_I(I, (inverse_h_kernel<II><<<nblk(B, 64), 64, 0, s>>>(P, W, logdet2, B, st, 0)));
   return cudaGetLastError();
 }
 cudaError_t launch_apply_w(const double2* mu_t, const double2* W, double2* out, int64_t Src,

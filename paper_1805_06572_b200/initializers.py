@@ -43,3 +43,26 @@ def init_random(y, seed, dtype="c128"):
     if D.is_tensor(y):
         return SpatialModel(v=v[0], S=torch.as_tensor(S, device=yd.device), v_floor=floor[0])
     return SpatialModel(v=D.host(v[0]), S=S, v_floor=D.host(floor[0]))
+
+
+def init_random_batch(Y, seeds, dtype="c128"):
+    """``init_random`` for a batch Y (M, N, F, I): mixture m uses ``seeds[m]``.
+    Powers and floors for the whole batch come from one ``ffca_init_powers``
+    launch; CUDA input -> CUDA outputs, host input -> host outputs."""
+    lib = D.require()
+    torch = D.torch
+    ctype, rtype = (torch.complex128, torch.float64) if dtype == "c128" else (torch.complex64,
+                                                                             torch.float32)
+    yd = D.to_device(Y, ctype)
+    M, N, F, I = (int(s) for s in yd.shape)
+    if len(seeds) != M:
+        raise ValueError("one seed per mixture")
+    v = D.empty((M, 2, N, F), rtype)
+    floor = D.empty((M, F), torch.float64)
+    D.check_rc(lib.ffca_init_powers(D.ptr(yd), D.ptr(v), D.ptr(floor), M, N, F, I,
+                                    0 if dtype == "c128" else 1, D.stream_handle()),
+               "ffca_init_powers")
+    S = np.stack([draw_covariances(int(s), F, I) for s in seeds])
+    if D.is_tensor(Y) and Y.is_cuda:
+        return SpatialModel(v=v, S=torch.as_tensor(S, device=yd.device), v_floor=floor)
+    return SpatialModel(v=D.host(v), S=S, v_floor=D.host(floor))
