@@ -270,8 +270,11 @@ def main():
     from paper_1805_06572_b200._engine import status_of as _st
 
     _st(kr, N, F)
+    # launches 0..L-2 are the update-only pass (the dominant kernel); the last
+    # one also writes the 10.5 GB of images and is reported on its own
     k_ms = kr.kernel_ms
-    k_avg = statistics.mean(k_ms) if k_ms else float("nan")
+    hot = k_ms[:-1] if len(k_ms) > 1 else k_ms
+    k_avg = statistics.mean(hot) if hot else float("nan")
     r = 8 if args.dtype == "c128" else 4  # bytes per real
     bytes_per_tf = (2 * I + 4) * r  # read y (I complex), read v (2), write v (2)
     alg_bytes = bytes_per_tf * M * F * N
@@ -279,8 +282,11 @@ def main():
     peak, peak_kind = peaks()
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": "fast_em_kernel" if args.engine == "fast" else "fca_em_kernel",
-            "kernel_ms_avg": round(k_avg, 4), "bytes_per_tf_bin": bytes_per_tf,
+            "kernel": ("fast_em2_kernel (update pass)" if args.engine == "fast"
+                       else "fca_em_kernel (update pass)"),
+            "kernel_ms_avg": round(k_avg, 4), "launches_averaged": len(hot),
+            "last_pass_with_images_ms": round(k_ms[-1], 4) if k_ms else None,
+            "bytes_per_tf_bin": bytes_per_tf,
             "peak_source": peak_kind,
             "iteration_ms_avg": round(statistics.mean(kr.iteration_ms), 4) if kr.iteration_ms
             else None}

@@ -59,17 +59,18 @@ struct RingSlot {
   static constexpr int BYTES = 16 * ((U16 % 2) ? U16 : U16 + 1);  // odd # of 16-B units
 };
 
-template <int I, typename R, int WARPS, int STAGES>
+template <int I, typename R, int WARPS, int STAGES, bool MU = false>
 struct Fast2Smem {
   static constexpr int NE = 2 * I * I + 1;
   static constexpr size_t RING = (size_t)STAGES * WARPS * 32 * RingSlot<I, R>::BYTES;
   static constexpr size_t RED = (size_t)(WARPS - 1) * NE * 32 * sizeof(double);
   static constexpr size_t PB = (size_t)I * I * 32 * sizeof(double2);  // P tile, after RING
-  static constexpr size_t BYTES = (RING + PB) > RED ? (RING + PB) : RED;
+  static constexpr size_t WB = MU ? PB : 0;                           // W tile, after P
+  static constexpr size_t BYTES = (RING + PB + WB) > RED ? (RING + PB + WB) : RED;
 };
 
 template <int I, typename R, int WARPS, int STAGES, bool UPDATE, bool LL, bool MU>
-__global__ void __launch_bounds__(WARPS * 32, 3) fast_em2_kernel(const FastIterParams p) {
+__global__ void __launch_bounds__(WARPS * 32, MU ? 2 : 3) fast_em2_kernel(const FastIterParams p) {
   using C = typename CplxOf<R>::type;
   using Slot = RingSlot<I, R>;
   constexpr int NP = I * I;
@@ -93,8 +94,12 @@ __global__ void __launch_bounds__(WARPS * 32, 3) fast_em2_kernel(const FastIterP
   // P lives in shared memory (bin-minor SoA after the frame ring): the 4
   // warps of the CTA work on the same 32 bins, so one 16*I*I-byte column per
   // lane serves all of them and frees the registers for the accumulators.
-  double2* sP = (double2*)(smem_raw + Fast2Smem<I, R, WARPS, STAGES>::RING);
+  double2* sP = (double2*)(smem_raw + Fast2Smem<I, R, WARPS, STAGES, MU>::RING);
   for (int e = warp; e < NP; e += WARPS) sP[e * 32 + lane] = p.P[g * NP + e];
+  // W = P^{-H} for the image write (last pass only), same bin-minor tile layout
+  double2* sW = sP + NP * 32;
+  if (MU && p.mu_back)
+    for (int e = warp; e < NP; e += WARPS) sW[e * 32 + lane] = p.W[g * NP + e];
   __syncthreads();
   double lam[I], il[I];
 #pragma unroll
@@ -234,28 +239,30 @@ __global__ void __launch_bounds__(WARPS * 32, 3) fast_em2_kernel(const FastIterP
     }
     if (MU && active) {
       C* mo = (C*)p.mu_out;
+      C* d1 = mo + (((m * 2 + 0) * p.N + n) * p.F + f) * I;
+      C* d2 = mo + (((m * 2 + 1) * p.N + n) * p.F + f) * I;
+      if (p.mu_back) {
+        // images (fast.py:133-141): mu_1 = P^{-H} (g1 z); mu_2 = y - mu_1, the
+        // posterior partition mu_1 + mu_2 = y (g1 + g2 = 1, P^{-H} P^H = I),
+        // exact up to rounding (reference test_fast.py:247-252)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        double2 mm[I];
+        for (int a = 0; a < I; ++a) {
+          double sx = 0.0, sy = 0.0;
 #pragma unroll
-        for (int a = 0; a < I; ++a) mm[a] = cscale(z[a], j == 0 ? g1[a] : g2[a]);
-        C* dst = mo + (((m * 2 + j) * p.N + n) * p.F + f) * I;
-        if (p.mu_back) {
-          const double2* Wg = p.W + g * NP;
-#pragma unroll
-          for (int a = 0; a < I; ++a) {
-            double2 s = cmk(0.0, 0.0);
-#pragma unroll
-            for (int b = 0; b < I; ++b) {
-              const double2 w = Wg[a * I + b];
-              s.x += w.x * mm[b].x - w.y * mm[b].y;
-              s.y += w.x * mm[b].y + w.y * mm[b].x;
-            }
-            dst[a] = from_c128<R>(s);
+          for (int b = 0; b < I; ++b) {
+            const double2 w = sW[(a * I + b) * 32 + lane];
+            const double mx = g1[b] * z[b].x, my = g1[b] * z[b].y;
+            sx = fma(w.x, mx, fma(-w.y, my, sx));
+            sy = fma(w.x, my, fma(w.y, mx, sy));
           }
-        } else {
+          d1[a] = from_c128<R>(cmk(sx, sy));
+          d2[a] = from_c128<R>(cmk(yv[a].x - sx, yv[a].y - sy));
+        }
+      } else {
 #pragma unroll
-          for (int a = 0; a < I; ++a) dst[a] = from_c128<R>(mm[a]);
+        for (int a = 0; a < I; ++a) {
+          d1[a] = from_c128<R>(cscale(z[a], g1[a]));
+          d2[a] = from_c128<R>(cscale(z[a], g2[a]));
         }
       }
     }
@@ -310,7 +317,7 @@ template <int I, typename R, bool UPDATE, bool LL, bool MU>
 cudaError_t launch_fast2_variant(const FastIterParams& p, cudaStream_t s) {
   constexpr int WARPS = kWarps;
   constexpr int STAGES = 6;
-  using Sm = Fast2Smem<I, R, WARPS, STAGES>;
+  using Sm = Fast2Smem<I, R, WARPS, STAGES, MU>;
   auto kern = fast_em2_kernel<I, R, WARPS, STAGES, UPDATE, LL, MU>;
   static bool configured = false;
   if (!configured) {
