@@ -106,7 +106,7 @@ def load(path: os.PathLike | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("FFCA_LIBRARY", LIB_PATH))
     if not p.exists():
         raise BackendUnavailableError(
             f"{p} is missing: build it with `python -m paper_1805_06572_b200.build` "

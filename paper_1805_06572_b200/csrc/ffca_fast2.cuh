@@ -49,6 +49,32 @@ FFCA_DEV void cp_async_wait() {
 }
 FFCA_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
+// Compute precision follows the streaming precision: complex128 runs the
+// per-point math in FP64; complex64 runs it in FP32 (B200's 2x-wider FP32
+// pipe) with FP64 per-bin state and FP64 accumulators fed by FP32 partial
+// sums over blocks of kF32Block frames (fp32 streaming with
+// fp64 per-bin accumulation reaches ~1e-6 of the complex128 oracle; the
+// complex64 tolerance is 1e-4).
+constexpr int kF32Block = 16;
+template <typename R>
+struct Math;
+template <>
+struct Math<double> {
+  using T = double;
+  using T2 = double2;
+  static constexpr bool kBlocked = false;
+  static FFCA_DEV double rcp(double x) { return rcp_nr(x); }
+  static FFCA_DEV double2 c2(double2 a) { return a; }
+};
+template <>
+struct Math<float> {
+  using T = float;
+  using T2 = float2;
+  static constexpr bool kBlocked = true;
+  static FFCA_DEV float rcp(float x) { return __frcp_rn(x); }
+  static FFCA_DEV float2 c2(double2 a) { return make_float2((float)a.x, (float)a.y); }
+};
+
 template <int I, typename R>
 struct RingSlot {
   using C = typename CplxOf<R>::type;
@@ -64,15 +90,25 @@ struct Fast2Smem {
   static constexpr int NE = 2 * I * I + 1;
   static constexpr size_t RING = (size_t)STAGES * WARPS * 32 * RingSlot<I, R>::BYTES;
   static constexpr size_t RED = (size_t)(WARPS - 1) * NE * 32 * sizeof(double);
-  static constexpr size_t PB = (size_t)I * I * 32 * sizeof(double2);  // P tile, after RING
+  static constexpr size_t PB = (size_t)I * I * 32 * sizeof(typename Math<R>::T2);  // P tile
   static constexpr size_t WB = MU ? PB : 0;                           // W tile, after P
   static constexpr size_t BYTES = (RING + PB + WB) > RED ? (RING + PB + WB) : RED;
 };
 
+#ifndef FAST2_MINB
+#define FAST2_MINB 3  // CTAs per SM the update pass is register-budgeted for
+#endif
+#ifndef FAST2_STAGES
+#define FAST2_STAGES 6  // cp.async ring depth (frames per thread)
+#endif
+
 template <int I, typename R, int WARPS, int STAGES, bool UPDATE, bool LL, bool MU>
-__global__ void __launch_bounds__(WARPS * 32, MU ? 2 : 3) fast_em2_kernel(const FastIterParams p) {
+__global__ void __launch_bounds__(WARPS * 32, MU ? 2 : FAST2_MINB) fast_em2_kernel(const FastIterParams p) {
   using C = typename CplxOf<R>::type;
   using Slot = RingSlot<I, R>;
+  using T = typename Math<R>::T;    // per-point compute type
+  using T2 = typename Math<R>::T2;
+  constexpr bool kBlk = Math<R>::kBlocked;
   constexpr int NP = I * I;
   constexpr int NE = 2 * NP + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -94,27 +130,48 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : 3) fast_em2_kernel(const 
   // P lives in shared memory (bin-minor SoA after the frame ring): the 4
   // warps of the CTA work on the same 32 bins, so one 16*I*I-byte column per
   // lane serves all of them and frees the registers for the accumulators.
-  double2* sP = (double2*)(smem_raw + Fast2Smem<I, R, WARPS, STAGES, MU>::RING);
-  for (int e = warp; e < NP; e += WARPS) sP[e * 32 + lane] = p.P[g * NP + e];
+  T2* sP = (T2*)(smem_raw + Fast2Smem<I, R, WARPS, STAGES, MU>::RING);
+  for (int e = warp; e < NP; e += WARPS) sP[e * 32 + lane] = Math<R>::c2(p.P[g * NP + e]);
   // W = P^{-H} for the image write (last pass only), same bin-minor tile layout
-  double2* sW = sP + NP * 32;
+  T2* sW = sP + NP * 32;
   if (MU && p.mu_back)
-    for (int e = warp; e < NP; e += WARPS) sW[e * 32 + lane] = p.W[g * NP + e];
+    for (int e = warp; e < NP; e += WARPS) sW[e * 32 + lane] = Math<R>::c2(p.W[g * NP + e]);
   __syncthreads();
-  double lam[I], il[I];
+  T lam[I], il[I];
 #pragma unroll
   for (int a = 0; a < I; ++a) {
-    lam[a] = p.lam[g * I + a];
-    il[a] = 1.0 / lam[a];
+    lam[a] = (T)p.lam[g * I + a];
+    il[a] = (T)(1.0 / p.lam[g * I + a]);
   }
-  const double fl = p.floor[g];
-  constexpr double invI = 1.0 / I;
+  const T fl = (T)p.floor[g];
+  constexpr T invI = T(1) / I;
 
   double acc[2][NP];
+  T accb[2][kBlk ? NP : 1];  // FP32 block sums (complex64 only)
 #pragma unroll
-  for (int j = 0; j < 2; ++j)
+  for (int j = 0; j < 2; ++j) {
 #pragma unroll
     for (int e = 0; e < NP; ++e) acc[j][e] = 0.0;
+#pragma unroll
+    for (int e = 0; e < (kBlk ? NP : 1); ++e) accb[j][e] = T(0);
+  }
+  auto accum = [&](int j, int e, T a, T b) {  // acc[j][e] += a * b
+    if constexpr (kBlk)
+      accb[j][e] = fma(a, b, accb[j][e]);
+    else
+      acc[j][e] = fma((double)a, (double)b, acc[j][e]);
+  };
+  auto flush = [&]() {
+    if constexpr (kBlk) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          acc[j][e] += (double)accb[j][e];
+          accb[j][e] = T(0);
+        }
+    }
+  };
   double llacc = 0.0;
   int64_t bad_n = 0;
 
@@ -156,68 +213,71 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : 3) fast_em2_kernel(const 
     cp_async_wait<STAGES - 1>();
     const int64_t n = nfirst + (int64_t)k * WARPS;
     const unsigned char* slot = myslots + (size_t)(k % STAGES) * kStageStride;
-    double2 yv[I];
+    T2 yv[I];
 #pragma unroll
-    for (int a = 0; a < I; ++a) yv[a] = to_c128(((const C*)slot)[a]);
-    const double v1 = (double)*(const R*)(slot + Slot::YB);
-    const double v2 = (double)*(const R*)(slot + Slot::YB + sizeof(R));
+    for (int a = 0; a < I; ++a) yv[a] = ((const T2*)slot)[a];
+    const T v1 = *(const R*)(slot + Slot::YB);
+    const T v2 = *(const R*)(slot + Slot::YB + sizeof(R));
 
-    double2 z[I];
+    T2 z[I];
 #pragma unroll
     for (int a = 0; a < I; ++a) {
-      const double2 p0 = sP[(0 * I + a) * 32 + lane];
-      double zr = p0.x * yv[0].x + p0.y * yv[0].y;
-      double zi = p0.x * yv[0].y - p0.y * yv[0].x;
+      const T2 p0 = sP[(0 * I + a) * 32 + lane];
+      T zr = p0.x * yv[0].x + p0.y * yv[0].y;
+      T zi = p0.x * yv[0].y - p0.y * yv[0].x;
 #pragma unroll
       for (int b = 1; b < I; ++b) {
-        const double2 pb = sP[(b * I + a) * 32 + lane];
+        const T2 pb = sP[(b * I + a) * 32 + lane];
         zr = fma(pb.x, yv[b].x, fma(pb.y, yv[b].y, zr));
         zi = fma(pb.x, yv[b].y, fma(-pb.y, yv[b].x, zi));
       }
-      z[a] = cmk(zr, zi);
+      z[a].x = zr;
+      z[a].y = zi;
     }
-    double g1[I], g2[I], t1[I], t2[I];
-    double tr1 = 0.0, tr2 = 0.0, lprod = 1.0, quad = 0.0;
+    T g1[I], g2[I], t1[I], t2[I];
+    T tr1 = 0, tr2 = 0;
+    double lprod = 1.0, quad = 0.0;
     bool bad = false;
 #pragma unroll
     for (int a = 0; a < I; ++a) {
-      const double v1l = v1 * lam[a];
-      const double den = v1l + v2;
-      const double rden = rcp_nr(den);
+      const T v1l = v1 * lam[a];
+      const T den = v1l + v2;
+      const T rden = Math<R>::rcp(den);
       g1[a] = v1l * rden;
       g2[a] = v2 * rden;
-      const double c = v2 * g1[a];
-      const double pz = fma(z[a].x, z[a].x, z[a].y * z[a].y);
+      const T c = v2 * g1[a];
+      const T pz = fma(z[a].x, z[a].x, z[a].y * z[a].y);
       t1[a] = fma(g1[a] * g1[a], pz, c);
       t2[a] = fma(g2[a] * g2[a], pz, c);
       tr1 = fma(t1[a], il[a], tr1);
       tr2 += t2[a];
       if (LL) {
-        lprod *= den;
-        quad = fma(pz, rden, quad);
+        lprod *= (double)den;
+        quad = fma((double)pz, (double)rden, quad);
       }
-      // den == 0 needs no test: rcp_nr(0) is NaN and poisons w below
+      // den == 0 needs no test: rcp(0) poisons w below (inf * 0 / NaN)
     }
     if (LL) llacc += log(lprod) + quad;
     if (UPDATE) {
-      const double q1 = tr1 * invI, q2 = tr2 * invI;
-      const double w1 = (q1 < fl) ? fl : q1;  // NaN propagates like np.maximum
-      const double w2 = (q2 < fl) ? fl : q2;
+      const T q1 = tr1 * invI, q2 = tr2 * invI;
+      const T w1 = (q1 < fl) ? fl : q1;  // NaN propagates like np.maximum
+      const T w2 = (q2 < fl) ? fl : q2;
       if (active) {
         vb[n * p.F] = (R)w1;
         vb[NF + n * p.F] = (R)w2;
       }
-      {  // non-finite or non-positive w (integer tests keep the FP64 pipe free)
-        const long long b1 = __double_as_longlong(w1), b2 = __double_as_longlong(w2);
+      {  // non-finite or non-positive w (integer tests keep the FP pipes free)
+        const double dw1 = w1, dw2 = w2;
+        const long long b1 = __double_as_longlong(dw1), b2 = __double_as_longlong(dw2);
         bad |= (((b1 >> 52) & 0x7ff) == 0x7ff) | (((b2 >> 52) & 0x7ff) == 0x7ff) | (b1 <= 0) |
                (b2 <= 0);
       }
-      const double iw1 = rcp_nr(w1), iw2 = rcp_nr(w2);
-      double h1[I], h2[I];
+      const T iw1 = Math<R>::rcp(w1), iw2 = Math<R>::rcp(w2);
+      T h1[I], h2[I];
 #pragma unroll
       for (int a = 0; a < I; ++a) {
-        acc[0][a] = fma(t1[a], iw1, acc[0][a]);
-        acc[1][a] = fma(t2[a], iw2, acc[1][a]);
+        accum(0, a, t1[a], iw1);
+        accum(1, a, t2[a], iw2);
         h1[a] = g1[a] * iw1;
         h2[a] = g2[a] * iw2;
       }
@@ -226,16 +286,17 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : 3) fast_em2_kernel(const 
 #pragma unroll
         for (int b = a + 1; b < I; ++b) {
           // z_a conj(z_b), shared by both sources
-          const double zr = fma(z[a].x, z[b].x, z[a].y * z[b].y);
-          const double zi = fma(z[a].y, z[b].x, -z[a].x * z[b].y);
-          const double k1 = h1[a] * g1[b];
-          const double k2 = h2[a] * g2[b];
-          acc[0][Herm<I>::re(a, b)] = fma(k1, zr, acc[0][Herm<I>::re(a, b)]);
-          acc[0][Herm<I>::im(a, b)] = fma(k1, zi, acc[0][Herm<I>::im(a, b)]);
-          acc[1][Herm<I>::re(a, b)] = fma(k2, zr, acc[1][Herm<I>::re(a, b)]);
-          acc[1][Herm<I>::im(a, b)] = fma(k2, zi, acc[1][Herm<I>::im(a, b)]);
+          const T zr = fma(z[a].x, z[b].x, z[a].y * z[b].y);
+          const T zi = fma(z[a].y, z[b].x, -z[a].x * z[b].y);
+          const T k1 = h1[a] * g1[b];
+          const T k2 = h2[a] * g2[b];
+          accum(0, Herm<I>::re(a, b), k1, zr);
+          accum(0, Herm<I>::im(a, b), k1, zi);
+          accum(1, Herm<I>::re(a, b), k2, zr);
+          accum(1, Herm<I>::im(a, b), k2, zi);
         }
       }
+      if (kBlk && ((k % kF32Block) == kF32Block - 1)) flush();
     }
     if (MU && active) {
       C* mo = (C*)p.mu_out;
@@ -247,27 +308,38 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : 3) fast_em2_kernel(const 
         // exact up to rounding (reference test_fast.py:247-252)
 #pragma unroll
         for (int a = 0; a < I; ++a) {
-          double sx = 0.0, sy = 0.0;
+          T sx = 0, sy = 0;
 #pragma unroll
           for (int b = 0; b < I; ++b) {
-            const double2 w = sW[(a * I + b) * 32 + lane];
-            const double mx = g1[b] * z[b].x, my = g1[b] * z[b].y;
+            const T2 w = sW[(a * I + b) * 32 + lane];
+            const T mx = g1[b] * z[b].x, my = g1[b] * z[b].y;
             sx = fma(w.x, mx, fma(-w.y, my, sx));
             sy = fma(w.x, my, fma(w.y, mx, sy));
           }
-          d1[a] = from_c128<R>(cmk(sx, sy));
-          d2[a] = from_c128<R>(cmk(yv[a].x - sx, yv[a].y - sy));
+          C o1, o2;
+          o1.x = sx;
+          o1.y = sy;
+          o2.x = yv[a].x - sx;
+          o2.y = yv[a].y - sy;
+          d1[a] = o1;
+          d2[a] = o2;
         }
       } else {
 #pragma unroll
         for (int a = 0; a < I; ++a) {
-          d1[a] = from_c128<R>(cscale(z[a], g1[a]));
-          d2[a] = from_c128<R>(cscale(z[a], g2[a]));
+          C o1, o2;
+          o1.x = z[a].x * g1[a];
+          o1.y = z[a].y * g1[a];
+          o2.x = z[a].x * g2[a];
+          o2.y = z[a].y * g2[a];
+          d1[a] = o1;
+          d2[a] = o2;
         }
       }
     }
     if (bad && bad_n == 0) bad_n = n + 1;
   }
+  flush();
   cp_async_wait_all();
   if (bad_n && active && p.st)
     report_error(p.st, p.iter, FFCA_ERR_SINGULAR_MATRIX,
@@ -316,7 +388,7 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : 3) fast_em2_kernel(const 
 template <int I, typename R, bool UPDATE, bool LL, bool MU>
 cudaError_t launch_fast2_variant(const FastIterParams& p, cudaStream_t s) {
   constexpr int WARPS = kWarps;
-  constexpr int STAGES = 6;
+  constexpr int STAGES = FAST2_STAGES;
   using Sm = Fast2Smem<I, R, WARPS, STAGES, MU>;
   auto kern = fast_em2_kernel<I, R, WARPS, STAGES, UPDATE, LL, MU>;
   static bool configured = false;
