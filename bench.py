@@ -223,7 +223,7 @@ def main():
     # the chunking the full (unsharded) problem would use -> identical per-bin sums
     from paper_1805_06572_b200._engine import plan_chunks
 
-    cf, _ = plan_chunks(cfg.M * cfg.F, cfg.N)
+    cf, _ = plan_chunks(cfg.M * cfg.F, cfg.N, cfg.I, args.dtype, args.engine)
     tf_it_rank = M * F * N * L
     tf_it_total = cfg.M * cfg.F * cfg.N * L
 

@@ -105,8 +105,10 @@ const char* ffca_version(void);
 int ffca_device_arch(void); /* compiled SM arch, e.g. 100 */
 
 /* ---- run level (fast.py:156-260, conventional.py:104-164) -------------- */
-/* Frame-axis chunking the drivers use for G = M*F bins and N frames. */
-int ffca_plan_chunks(int64_t G, int64_t N, int64_t* chunk_frames, int* nchunk);
+/* Frame-axis chunking the drivers use for G = M*F bins and N frames
+ * (algorithm 0 = FastFCA, 1 = FCA; needs a device for the occupancy query). */
+int ffca_plan_chunks(int64_t G, int64_t N, int I, int dtype, int algorithm,
+                     int64_t* chunk_frames, int* nchunk);
 size_t ffca_fastfca_workspace_size(int64_t M, int64_t N, int64_t F, int I, int iterations,
                                    unsigned flags, int64_t chunk_frames);
 int ffca_fastfca_run(const ffca_run_args* args, void* stream);

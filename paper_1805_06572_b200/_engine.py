@@ -154,14 +154,15 @@ def _collect_timings(run):
         run.kernel_ms = [k[2 * i].elapsed_time(k[2 * i + 1]) for i in range(len(k) // 2)]
 
 
-def plan_chunks(G, N):
+def plan_chunks(G, N, I=4, dtype="c128", algorithm="fast"):
     """The frame chunking the drivers pick for G bins x N frames (per-bin
     reduction order: equal chunking => bitwise-equal per-bin results)."""
-    lib = _lib.load()
+    lib = D.require()
     cf = ctypes.c_int64()
     nc = ctypes.c_int()
-    D.check_rc(lib.ffca_plan_chunks(int(G), int(N), ctypes.byref(cf), ctypes.byref(nc)),
-               "ffca_plan_chunks")
+    D.check_rc(lib.ffca_plan_chunks(int(G), int(N), int(I), DTYPES[dtype],
+                                    0 if algorithm == "fast" else 1, ctypes.byref(cf),
+                                    ctypes.byref(nc)), "ffca_plan_chunks")
     return int(cf.value), int(nc.value)
 
 

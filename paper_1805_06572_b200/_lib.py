@@ -62,7 +62,8 @@ class RunArgs(ctypes.Structure):
 SIGNATURES = [
     ("ffca_version", ctypes.c_char_p, []),
     ("ffca_device_arch", c_int, []),
-    ("ffca_plan_chunks", c_int, [c_i64, c_i64, ctypes.POINTER(c_i64), ctypes.POINTER(c_int)]),
+    ("ffca_plan_chunks", c_int,
+     [c_i64, c_i64, c_int, c_int, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_int)]),
     ("ffca_fastfca_workspace_size", c_sz,
      [c_i64, c_i64, c_i64, c_int, c_int, ctypes.c_uint, c_i64]),
     ("ffca_fastfca_run", c_int, [ctypes.POINTER(RunArgs), c_vp]),

@@ -56,20 +56,20 @@ struct FastWs {
   size_t bytes;
 };
 
-void chunking(int64_t G, int64_t N, int64_t cf_req, int64_t* cf, int* nc) {
+void chunking(int64_t G, int64_t N, int64_t cf_req, int bpsm, int64_t* cf, int* nc) {
   if (cf_req > 0) {
     *cf = cf_req < N ? cf_req : N;
     *nc = (int)((N + *cf - 1) / *cf);
   } else {
-    plan_chunks(G, N, cf, nc);
+    plan_chunks(G, N, bpsm, cf, nc);
   }
 }
 
 FastWs carve_fast(void* base, int64_t M, int64_t N, int64_t F, int I, int L, unsigned flags,
-                  int64_t cf_req) {
+                  int64_t cf_req, int dtype) {
   FastWs w{};
   const int64_t G = M * F;
-  chunking(G, N, cf_req, &w.chunk_frames, &w.nchunk);
+  chunking(G, N, cf_req, fast_blocks_per_sm(I, dtype), &w.chunk_frames, &w.nchunk);
   Carve c(base);
   w.st = c.take<ffca_status_dev>(1);
   w.P = c.take<double2>(G * I * I);
@@ -94,10 +94,10 @@ struct FcaWs {
 };
 
 FcaWs carve_fca(void* base, int64_t M, int64_t N, int64_t F, int I, int L, unsigned flags,
-                int64_t cf_req) {
+                int64_t cf_req, int dtype) {
   FcaWs w{};
   const int64_t G = M * F;
-  chunking(G, N, cf_req, &w.chunk_frames, &w.nchunk);
+  chunking(G, N, cf_req, fca_blocks_per_sm(I, dtype), &w.chunk_frames, &w.nchunk);
   Carve c(base);
   w.st = c.take<ffca_status_dev>(1);
   w.Sp = c.take<double>((size_t)4 * I * I * G);
@@ -162,22 +162,30 @@ const char* ffca_version(void) { return "fastfca_b200 0.1.0 (sm_100a)"; }
 
 int ffca_device_arch(void) { return 100; }
 
-int ffca_plan_chunks(int64_t G, int64_t N, int64_t* chunk_frames, int* nchunk) {
-  if (G < 1 || N < 1 || !chunk_frames || !nchunk) return FFCA_ERR_INVALID;
-  plan_chunks(G, N, chunk_frames, nchunk);
+int ffca_plan_chunks(int64_t G, int64_t N, int I, int dtype, int algorithm,
+                     int64_t* chunk_frames, int* nchunk) {
+  if (G < 1 || N < 1 || I < 1 || I > kMaxOrder || !chunk_frames || !nchunk)
+    return FFCA_ERR_INVALID;
+  const int bpsm = algorithm ? fca_blocks_per_sm(I, dtype) : fast_blocks_per_sm(I, dtype);
+  plan_chunks(G, N, bpsm, chunk_frames, nchunk);
   return FFCA_OK;
 }
 
 size_t ffca_fastfca_workspace_size(int64_t M, int64_t N, int64_t F, int I, int iterations,
                                    unsigned flags, int64_t chunk_frames) {
   if (M < 1 || N < 1 || F < 1 || I < 1 || I > kMaxOrder || iterations < 0) return 0;
-  return carve_fast(nullptr, M, N, F, I, iterations, flags, chunk_frames).bytes;
+  // chunk count is largest for the most-occupant dtype: size for both
+  const size_t a = carve_fast(nullptr, M, N, F, I, iterations, flags, chunk_frames, FFCA_C128).bytes;
+  const size_t b = carve_fast(nullptr, M, N, F, I, iterations, flags, chunk_frames, FFCA_C64).bytes;
+  return a > b ? a : b;
 }
 
 size_t ffca_fca_workspace_size(int64_t M, int64_t N, int64_t F, int I, int iterations,
                                unsigned flags, int64_t chunk_frames) {
   if (M < 1 || N < 1 || F < 1 || I < 1 || I > kMaxOrder || iterations < 0) return 0;
-  return carve_fca(nullptr, M, N, F, I, iterations, flags, chunk_frames).bytes;
+  const size_t a = carve_fca(nullptr, M, N, F, I, iterations, flags, chunk_frames, FFCA_C128).bytes;
+  const size_t b = carve_fca(nullptr, M, N, F, I, iterations, flags, chunk_frames, FFCA_C64).bytes;
+  return a > b ? a : b;
 }
 
 int ffca_fastfca_run(const ffca_run_args* a, void* stream) {
@@ -187,7 +195,7 @@ int ffca_fastfca_run(const ffca_run_args* a, void* stream) {
   const int64_t M = a->M, N = a->N, F = a->F, G = M * F;
   const int I = a->I, L = a->iterations;
   const unsigned fl = a->flags;
-  FastWs w = carve_fast(a->workspace, M, N, F, I, L, fl, a->chunk_frames);
+  FastWs w = carve_fast(a->workspace, M, N, F, I, L, fl, a->chunk_frames, a->dtype);
   if (w.bytes > a->workspace_bytes) return FFCA_ERR_INVALID;
   const bool ll = fl & FFCA_FLAG_LIKELIHOOD;
   const bool hist = (fl & FFCA_FLAG_HISTORY) != 0;
@@ -280,7 +288,7 @@ int ffca_fca_run(const ffca_run_args* a, void* stream) {
   const int64_t M = a->M, N = a->N, F = a->F, G = M * F;
   const int I = a->I, L = a->iterations;
   const unsigned fl = a->flags;
-  FcaWs w = carve_fca(a->workspace, M, N, F, I, L, fl, a->chunk_frames);
+  FcaWs w = carve_fca(a->workspace, M, N, F, I, L, fl, a->chunk_frames, a->dtype);
   if (w.bytes > a->workspace_bytes) return FFCA_ERR_INVALID;
   const bool ll = fl & FFCA_FLAG_LIKELIHOOD;
   const bool hist = (fl & FFCA_FLAG_HISTORY) != 0;

@@ -225,6 +225,48 @@ static cudaError_t launch_fast_em_t(const FastIterParams& p, cudaStream_t s) {
 // v2 kernels for I <= 4 (ffca_fast2.cuh, instantiated in ffca_fast_i<I>.cu)
 template <int I, typename R>
 cudaError_t launch_fast2(const FastIterParams& p, cudaStream_t s);
+template <int I, typename R>
+int fast2_blocks_per_sm();
+
+template <int I, typename R>
+static int fast_v1_blocks_per_sm() {
+  constexpr int NE = 2 * I * I + 1;
+  const size_t smem = (size_t)(kWarps - 1) * NE * 32 * sizeof(double);
+  auto kern = fast_em_kernel<I, R, kWarps>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kWarps * 32, smem);
+  return n > 0 ? n : 1;
+}
+
+int fast_blocks_per_sm(int I, int dtype) {
+  static int cache[2][9] = {};
+  const int d = dtype == FFCA_C64 ? 1 : 0;
+  if (I < 1 || I > 8) return 1;
+  if (cache[d][I]) return cache[d][I];
+  int n = 1;
+#define FFCA_OCC(II)                                                               \
+  case II:                                                                         \
+    if (II <= 4)                                                                   \
+      n = d ? fast2_blocks_per_sm<(II <= 4 ? II : 4), float>()                     \
+            : fast2_blocks_per_sm<(II <= 4 ? II : 4), double>();                   \
+    else                                                                           \
+      n = d ? fast_v1_blocks_per_sm<II, float>() : fast_v1_blocks_per_sm<II, double>(); \
+    break;
+  switch (I) {
+    FFCA_OCC(1)
+    FFCA_OCC(2)
+    FFCA_OCC(3)
+    FFCA_OCC(4)
+    FFCA_OCC(5)
+    FFCA_OCC(6)
+    FFCA_OCC(7)
+    FFCA_OCC(8)
+  }
+#undef FFCA_OCC
+  cache[d][I] = n;
+  return n;
+}
 
 cudaError_t launch_fast_em(const FastIterParams& p, int I, int dtype, cudaStream_t s) {
 #define FFCA_CASE2(II)                                                      \
@@ -307,21 +349,32 @@ int sm_count() {
   return n;
 }
 
-void plan_chunks(int64_t G, int64_t N, int64_t* chunk_frames, int* nchunk) {
-  // target >= 4 CTAs per SM, but keep >= 16 frames per warp in a chunk
+void plan_chunks(int64_t G, int64_t N, int blocks_per_sm, int64_t* chunk_frames, int* nchunk) {
+  // Pick the frame chunking that minimises the modelled makespan
+  //   waves(tiles * nchunk / resident CTAs) * (frames per chunk + per-CTA overhead)
+  // so that the grid does not end on a mostly idle last wave (config 4:
+  // 33 bin tiles; config 3: 2056). >= 16 frames per warp per chunk.
   const int64_t tiles = (G + 31) / 32;
-  const int64_t target = 4 * (int64_t)sm_count();
-  int64_t nc = (target + tiles - 1) / tiles;
+  const int64_t slots = (int64_t)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
   const int64_t min_frames = 16 * kWarps;
-  const int64_t max_nc = (N + min_frames - 1) / min_frames;
-  if (nc > max_nc) nc = max_nc;
-  if (nc < 1) nc = 1;
-  int64_t cf = (N + nc - 1) / nc;
-  nc = (N + cf - 1) / cf;
-  if (nc < 1) nc = 1;
-  if (cf < 1) cf = 1;
-  *chunk_frames = cf;
-  *nchunk = (int)nc;
+  int64_t max_nc = (N + min_frames - 1) / min_frames;
+  if (max_nc < 1) max_nc = 1;
+  if (max_nc > 4096) max_nc = 4096;
+  constexpr int64_t kOverhead = 24;  // frames-equivalent: P/W load, ring fill, reduction
+  int64_t best_cf = N, best_cost = -1;
+  for (int64_t nc = 1; nc <= max_nc; ++nc) {
+    const int64_t cf = (N + nc - 1) / nc;
+    const int64_t ncv = (N + cf - 1) / cf;
+    if (ncv != nc) continue;  // same chunking as a smaller nc
+    const int64_t waves = (tiles * ncv + slots - 1) / slots;
+    const int64_t cost = waves * (cf + kOverhead);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best_cf = cf;
+    }
+  }
+  *chunk_frames = best_cf;
+  *nchunk = (int)((N + best_cf - 1) / best_cf);
 }
 
 }  // namespace ffca

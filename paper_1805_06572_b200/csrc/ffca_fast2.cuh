@@ -404,6 +404,16 @@ cudaError_t launch_fast2_variant(const FastIterParams& p, cudaStream_t s) {
 }
 
 template <int I, typename R>
+int fast2_blocks_per_sm() {
+  using Sm = Fast2Smem<I, R, kWarps, FAST2_STAGES, false>;
+  auto kern = fast_em2_kernel<I, R, kWarps, FAST2_STAGES, true, false, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sm::BYTES);
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kWarps * 32, Sm::BYTES);
+  return n > 0 ? n : 1;
+}
+
+template <int I, typename R>
 cudaError_t launch_fast2(const FastIterParams& p, cudaStream_t s) {
   const bool ll = p.llbin != nullptr;
   const bool mu = p.mu_out != nullptr;

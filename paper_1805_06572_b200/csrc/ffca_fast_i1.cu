@@ -4,4 +4,6 @@
 namespace ffca {
 template cudaError_t launch_fast2<1, double>(const FastIterParams&, cudaStream_t);
 template cudaError_t launch_fast2<1, float>(const FastIterParams&, cudaStream_t);
+template int fast2_blocks_per_sm<1, double>();
+template int fast2_blocks_per_sm<1, float>();
 }  // namespace ffca

@@ -4,4 +4,6 @@
 namespace ffca {
 template cudaError_t launch_fast2<2, double>(const FastIterParams&, cudaStream_t);
 template cudaError_t launch_fast2<2, float>(const FastIterParams&, cudaStream_t);
+template int fast2_blocks_per_sm<2, double>();
+template int fast2_blocks_per_sm<2, float>();
 }  // namespace ffca

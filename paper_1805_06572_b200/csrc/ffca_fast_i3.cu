@@ -4,4 +4,6 @@
 namespace ffca {
 template cudaError_t launch_fast2<3, double>(const FastIterParams&, cudaStream_t);
 template cudaError_t launch_fast2<3, float>(const FastIterParams&, cudaStream_t);
+template int fast2_blocks_per_sm<3, double>();
+template int fast2_blocks_per_sm<3, float>();
 }  // namespace ffca

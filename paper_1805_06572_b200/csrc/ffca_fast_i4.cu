@@ -4,4 +4,6 @@
 namespace ffca {
 template cudaError_t launch_fast2<4, double>(const FastIterParams&, cudaStream_t);
 template cudaError_t launch_fast2<4, float>(const FastIterParams&, cudaStream_t);
+template int fast2_blocks_per_sm<4, double>();
+template int fast2_blocks_per_sm<4, float>();
 }  // namespace ffca

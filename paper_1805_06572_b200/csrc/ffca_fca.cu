@@ -267,6 +267,43 @@ static cudaError_t launch_fca_em_t(const FcaIterParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int I, typename R>
+static int fca_bpsm_t() {
+  constexpr int NP = I * I;
+  constexpr int NE = 2 * NP + 1;
+  const size_t smem = ((size_t)4 * NP * 32 + (size_t)(kWarps - 1) * NE * 32) * sizeof(double);
+  auto kern = fca_em_kernel<I, R, kWarps>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kWarps * 32, smem);
+  return n > 0 ? n : 1;
+}
+
+int fca_blocks_per_sm(int I, int dtype) {
+  static int cache[2][9] = {};
+  const int d = dtype == FFCA_C64 ? 1 : 0;
+  if (I < 1 || I > 8) return 1;
+  if (cache[d][I]) return cache[d][I];
+  int n = 1;
+  switch (I) {
+#define FFCA_OCC(II) \
+  case II:           \
+    n = d ? fca_bpsm_t<II, float>() : fca_bpsm_t<II, double>(); \
+    break;
+    FFCA_OCC(1)
+    FFCA_OCC(2)
+    FFCA_OCC(3)
+    FFCA_OCC(4)
+    FFCA_OCC(5)
+    FFCA_OCC(6)
+    FFCA_OCC(7)
+    FFCA_OCC(8)
+#undef FFCA_OCC
+  }
+  cache[d][I] = n;
+  return n;
+}
+
 cudaError_t launch_fca_em(const FcaIterParams& p, int I, int dtype, cudaStream_t s) {
 #define FFCA_CASE(II)                                                    \
   case II:                                                               \

@@ -93,8 +93,11 @@ cudaError_t launch_ll_collect(const double* llbin, int nchunk, const double* log
 cudaError_t launch_ll_reduce(const double* llg, int64_t M, int64_t F, int64_t N, int I,
                              int nlev, int Lp1, double* loglik, cudaStream_t s);
 
-// chunking of the frame axis so that the grid fills the GPU
-void plan_chunks(int64_t G, int64_t N, int64_t* chunk_frames, int* nchunk);
+// chunking of the frame axis so that the grid fills the GPU without a
+// mostly idle last wave; blocks_per_sm = resident CTAs of the streaming kernel
+void plan_chunks(int64_t G, int64_t N, int blocks_per_sm, int64_t* chunk_frames, int* nchunk);
+int fast_blocks_per_sm(int I, int dtype);
+int fca_blocks_per_sm(int I, int dtype);
 
 int sm_count();
 

@@ -6,6 +6,8 @@
 //   (pencil.py:85-135), P <- P Q (fast.py:107-113), P^{-H} and log|det P|^2
 //   for the next pass (fast.py:151-153).
 // Plus the stand-alone batched per-bin routines of the C ABI.
+#include <cstdlib>
+
 #include "ffca_internal.cuh"
 
 namespace ffca {
@@ -278,7 +280,28 @@ template <int I>
 __global__ void inverse_h_kernel(const double2* P, double2* W, double* logdet2, int64_t B,
                                  ffca_status_dev* st, int iter);
 
+cudaError_t launch_pencil_par(const PencilParams& p, int I, cudaStream_t s);
+cudaError_t launch_initial_par(const double2* S0, double2* P, double2* W, double* lam,
+                               double* logdet2, int64_t G, int64_t F, int I, ffca_status_dev* st,
+                               cudaStream_t s);
+
+// Which per-bin kernel: the lane-parallel one (ffca_pencil_par.cu) wins when
+// bins are few (latency-bound) and for I >= 5 (no register spills); the
+// one-thread-per-bin kernel keeps more bins in flight for big batches.
+// FFCA_K1=par|thread overrides (experiments).
+static bool use_par(int64_t G, int I) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("FFCA_K1");
+    mode = (e && e[0] == 'p') ? 1 : ((e && e[0] == 't') ? 2 : 0);
+  }
+  if (mode == 1) return true;
+  if (mode == 2) return I >= 5;
+  return I >= 5 || G < 16384;
+}
+
 cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s) {
+  if (use_par(p.G, I)) return launch_pencil_par(p, I, s);
   if (I <= 4) {  // fused single kernel; only instantiated for I <= 4
     const unsigned nb = nblk(p.G, 64);
     switch (I) {
@@ -304,6 +327,7 @@ cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s) {
 cudaError_t launch_initial_pencil(const double2* S0, double2* P, double2* W, double* lam,
                                   double* logdet2, int64_t G, int64_t F, int I,
                                   ffca_status_dev* st, cudaStream_t s) {
+  if (use_par(G, I)) return launch_initial_par(S0, P, W, lam, logdet2, G, F, I, st, s);
   FFCA_DISPATCH_I(I, (initial_pencil_kernel<II><<<nblk(G, 64), 64, 0, s>>>(S0, P, W, lam,
                                                                             logdet2, G, F, st)));
   return cudaGetLastError();

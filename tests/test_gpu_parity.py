@@ -133,7 +133,7 @@ def test_pipelined_host_path_equals_device_path():
     V = np.stack([i.v for i in inits])
     S = np.stack([i.S for i in inits])
     FL = np.stack([i.v_floor for i in inits])
-    cf, _ = plan_chunks(5 * 11, 120)
+    cf, _ = plan_chunks(5 * 11, 120, 4)
     ref = run_device("fast", Y, V, S, FL, 7, chunk_frames=cf)
     yp = torch.from_numpy(Y).pin_memory()
     vp = torch.from_numpy(V).pin_memory()
