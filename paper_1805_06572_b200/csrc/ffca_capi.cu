@@ -56,20 +56,19 @@ struct FastWs {
   size_t bytes;
 };
 
-void chunking(int64_t G, int64_t N, int64_t cf_req, int bpsm, int64_t* cf, int* nc) {
-  if (cf_req > 0) {
-    *cf = cf_req < N ? cf_req : N;
-    *nc = (int)((N + *cf - 1) / *cf);
-  } else {
-    plan_chunks(G, N, bpsm, cf, nc);
-  }
+bool chunk_override(int64_t N, int64_t cf_req, int64_t* cf, int* nc) {
+  if (cf_req <= 0) return false;
+  *cf = cf_req < N ? cf_req : N;
+  *nc = (int)((N + *cf - 1) / *cf);
+  return true;
 }
 
 FastWs carve_fast(void* base, int64_t M, int64_t N, int64_t F, int I, int L, unsigned flags,
                   int64_t cf_req, int dtype) {
   FastWs w{};
   const int64_t G = M * F;
-  chunking(G, N, cf_req, fast_blocks_per_sm(I, dtype), &w.chunk_frames, &w.nchunk);
+  if (!chunk_override(N, cf_req, &w.chunk_frames, &w.nchunk))
+    plan_chunks(G, N, fast_blocks_per_sm(I, dtype), &w.chunk_frames, &w.nchunk);
   Carve c(base);
   w.st = c.take<ffca_status_dev>(1);
   w.P = c.take<double2>(G * I * I);
@@ -97,7 +96,8 @@ FcaWs carve_fca(void* base, int64_t M, int64_t N, int64_t F, int I, int L, unsig
                 int64_t cf_req, int dtype) {
   FcaWs w{};
   const int64_t G = M * F;
-  chunking(G, N, cf_req, fca_blocks_per_sm(I, dtype), &w.chunk_frames, &w.nchunk);
+  if (!chunk_override(N, cf_req, &w.chunk_frames, &w.nchunk))
+    plan_fca_chunks(G, N, I, dtype, &w.chunk_frames, &w.nchunk);
   Carve c(base);
   w.st = c.take<ffca_status_dev>(1);
   w.Sp = c.take<double>((size_t)4 * I * I * G);
@@ -166,8 +166,10 @@ int ffca_plan_chunks(int64_t G, int64_t N, int I, int dtype, int algorithm,
                      int64_t* chunk_frames, int* nchunk) {
   if (G < 1 || N < 1 || I < 1 || I > kMaxOrder || !chunk_frames || !nchunk)
     return FFCA_ERR_INVALID;
-  const int bpsm = algorithm ? fca_blocks_per_sm(I, dtype) : fast_blocks_per_sm(I, dtype);
-  plan_chunks(G, N, bpsm, chunk_frames, nchunk);
+  if (algorithm)
+    plan_fca_chunks(G, N, I, dtype, chunk_frames, nchunk);
+  else
+    plan_chunks(G, N, fast_blocks_per_sm(I, dtype), chunk_frames, nchunk);
   return FFCA_OK;
 }
 

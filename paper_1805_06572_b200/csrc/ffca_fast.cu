@@ -349,14 +349,14 @@ int sm_count() {
   return n;
 }
 
-void plan_chunks(int64_t G, int64_t N, int blocks_per_sm, int64_t* chunk_frames, int* nchunk) {
+void plan_chunks(int64_t G, int64_t N, int blocks_per_sm, int64_t* chunk_frames, int* nchunk,
+                 int tile_bins, int64_t min_frames) {
   // Pick the frame chunking that minimises the modelled makespan
   //   waves(tiles * nchunk / resident CTAs) * (frames per chunk + per-CTA overhead)
   // so that the grid does not end on a mostly idle last wave (config 4:
   // 33 bin tiles; config 3: 2056). >= 16 frames per warp per chunk.
-  const int64_t tiles = (G + 31) / 32;
+  const int64_t tiles = (G + tile_bins - 1) / tile_bins;
   const int64_t slots = (int64_t)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
-  const int64_t min_frames = 16 * kWarps;
   int64_t max_nc = (N + min_frames - 1) / min_frames;
   if (max_nc < 1) max_nc = 1;
   if (max_nc > 4096) max_nc = 4096;

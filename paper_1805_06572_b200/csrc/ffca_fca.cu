@@ -279,6 +279,18 @@ static int fca_bpsm_t() {
   return n > 0 ? n : 1;
 }
 
+cudaError_t launch_fca_par(const FcaIterParams& p, int I, int dtype, cudaStream_t s);
+int fca_par_blocks_per_sm(int I, int dtype);
+int fca_par_bins_per_cta(int I);
+
+void plan_fca_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames, int* nchunk) {
+  if (I >= 5)
+    plan_chunks(G, N, fca_par_blocks_per_sm(I, dtype), chunk_frames, nchunk,
+                fca_par_bins_per_cta(I), 16);
+  else
+    plan_chunks(G, N, fca_blocks_per_sm(I, dtype), chunk_frames, nchunk);
+}
+
 int fca_blocks_per_sm(int I, int dtype) {
   static int cache[2][9] = {};
   const int d = dtype == FFCA_C64 ? 1 : 0;
@@ -305,6 +317,7 @@ int fca_blocks_per_sm(int I, int dtype) {
 }
 
 cudaError_t launch_fca_em(const FcaIterParams& p, int I, int dtype, cudaStream_t s) {
+  if (I >= 5) return launch_fca_par(p, I, dtype, s);  // lane-parallel (ffca_fca_par.cu)
 #define FFCA_CASE(II)                                                    \
   case II:                                                               \
     return dtype == FFCA_C64 ? launch_fca_em_t<II, float>(p, s)          \
@@ -314,10 +327,6 @@ cudaError_t launch_fca_em(const FcaIterParams& p, int I, int dtype, cudaStream_t
     FFCA_CASE(2)
     FFCA_CASE(3)
     FFCA_CASE(4)
-    FFCA_CASE(5)
-    FFCA_CASE(6)
-    FFCA_CASE(7)
-    FFCA_CASE(8)
     default:
       return cudaErrorInvalidValue;
   }

@@ -616,7 +616,7 @@ int ffca_fca_iteration(const double* y, const double* v, const double* S, const 
       cudaSuccess)
     return FFCA_ERR_CUDA;
   FcaIterParams p{};
-  plan_chunks(F, N, fca_blocks_per_sm(I, FFCA_C128), &p.chunk_frames, &p.nchunk);
+  plan_fca_chunks(F, N, I, FFCA_C128, &p.chunk_frames, &p.nchunk);
   double *Spart = nullptr, *Sp = nullptr;
   if (cudaMallocAsync((void**)&Spart, (size_t)p.nchunk * 2 * I * I * F * sizeof(double), s) !=
           cudaSuccess ||
