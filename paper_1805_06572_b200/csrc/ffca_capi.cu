@@ -68,7 +68,7 @@ FastWs carve_fast(void* base, int64_t M, int64_t N, int64_t F, int I, int L, uns
   FastWs w{};
   const int64_t G = M * F;
   if (!chunk_override(N, cf_req, &w.chunk_frames, &w.nchunk))
-    plan_chunks(G, N, fast_blocks_per_sm(I, dtype), &w.chunk_frames, &w.nchunk);
+    plan_fast_chunks(G, N, I, dtype, &w.chunk_frames, &w.nchunk);
   Carve c(base);
   w.st = c.take<ffca_status_dev>(1);
   w.P = c.take<double2>(G * I * I);
@@ -169,7 +169,7 @@ int ffca_plan_chunks(int64_t G, int64_t N, int I, int dtype, int algorithm,
   if (algorithm)
     plan_fca_chunks(G, N, I, dtype, chunk_frames, nchunk);
   else
-    plan_chunks(G, N, fast_blocks_per_sm(I, dtype), chunk_frames, nchunk);
+    plan_fast_chunks(G, N, I, dtype, chunk_frames, nchunk);
   return FFCA_OK;
 }
 

@@ -1,0 +1,273 @@
+// K3p — fused FastFCA pass for large orders (5 <= I <= 8), lane-parallel.
+//
+// At I = 8 one thread per bin would need P (64 complex) and 2 x 36 packed
+// accumulators in registers, so the v1 kernel (ffca_fast.cu) spills. Here a
+// group of 8 lanes owns one bin and streams its frames; lane r owns channel
+// r: column r of P (z_r = sum_b conj(P[b][r]) y_b), the scalar posterior of
+// channel r (den, g1, g2, t1, t2), and row r of both transformed covariance
+// accumulators. The power update needs sums over channels (group shuffles);
+// the rank-1 updates need every z_c, g1_c, g2_c (exchanged through a few
+// bytes of shared memory per bin). Same arithmetic as fast_em2_kernel
+// (reference _kernels_numba.py:328-391), same Spart / llbin / mu layouts.
+#include "ffca_fast2.cuh"
+#include "ffca_pencil_par.cuh"
+
+namespace ffca {
+
+namespace {
+template <int I>
+struct FastParLayout {
+  static constexpr int LB = 8;
+  static constexpr int WARPS = 2;
+  static constexpr int BPB = WARPS * 32 / LB;  // bins per CTA
+  // per group: y (2I), z (2I), g1 (I), g2 (I) doubles; odd # of 16-B units
+  static constexpr int RAW = 6 * I;
+  static constexpr int U16 = (RAW + 1) / 2;
+  static constexpr int GROUP_DOUBLES = 2 * ((U16 % 2) ? U16 : U16 + 1);
+  static constexpr size_t SMEM = (size_t)BPB * GROUP_DOUBLES * sizeof(double);
+};
+}  // namespace
+
+template <int I, typename R, bool UPDATE, bool LL, bool MU>
+__global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32) fast_par_kernel(const FastIterParams p) {
+  using Lay = FastParLayout<I>;
+  using C = typename CplxOf<R>::type;
+  constexpr int NP = I * I;
+  constexpr int LB = Lay::LB;
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = lane % LB;
+  const int grp = warp * (32 / LB) + lane / LB;
+  const int64_t G = p.G;
+  int64_t g = (int64_t)blockIdx.x * Lay::BPB + grp;
+  const bool active = g < G;
+  if (!active) g = G - 1;
+  const bool own = r < I;
+  const int rr = own ? r : 0;  // clamped channel for idle lanes
+  const int64_t m = g / p.F, f = g - m * p.F;
+  double* base = sm + (size_t)grp * Lay::GROUP_DOUBLES;
+  double2* sy = (double2*)base;      // y
+  double2* sz = sy + I;              // z
+  double* sg1 = (double*)(sz + I);   // g1
+  double* sg2 = sg1 + I;             // g2
+
+  double2 pc[I];  // column rr of P
+  double2 wr[I];  // row rr of W = P^-H (images only)
+#pragma unroll
+  for (int b = 0; b < I; ++b) {
+    pc[b] = p.P[g * NP + b * I + rr];
+    wr[b] = MU && p.mu_back ? p.W[g * NP + rr * I + b] : cmk(0.0, 0.0);
+  }
+  const double lam = p.lam[g * I + rr];
+  const double il = 1.0 / lam;
+  const double fl = p.floor[g];
+  const int64_t n0 = (int64_t)blockIdx.y * p.chunk_frames;
+  const int64_t n1 = min(p.N, n0 + p.chunk_frames);
+  const int64_t NF = p.N * p.F;
+  const C* __restrict__ yb = (const C*)p.y + (m * p.N * p.F + f) * I;
+  R* __restrict__ vb = (R*)p.v + m * 2 * NF + f;
+
+  double acc1[I], acc2[I];  // row rr: [c] = Re (c == rr) or (re, im) packed as below
+  double acc1i[I], acc2i[I];
+#pragma unroll
+  for (int c = 0; c < I; ++c) acc1[c] = acc2[c] = acc1i[c] = acc2i[c] = 0.0;
+  double llacc = 0.0;
+  int64_t bad_n = 0;
+
+  // two frames of register prefetch
+  double2 yq[2];
+  double v1q[2], v2q[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int64_t n = n0 + k;
+    yq[k] = cmk(0.0, 0.0);
+    v1q[k] = v2q[k] = 1.0;
+    if (n < n1) {
+      yq[k] = to_c128(yb[n * p.F * I + rr]);
+      v1q[k] = (double)vb[n * p.F];
+      v2q[k] = (double)vb[NF + n * p.F];
+    }
+  }
+#pragma unroll 1
+  for (int64_t n = n0; n < n1; ++n) {
+    const int slot = (int)((n - n0) & 1);
+    const double2 ycur = yq[slot];
+    const double v1 = v1q[slot], v2 = v2q[slot];
+    if (n + 2 < n1) {
+      yq[slot] = to_c128(yb[(n + 2) * p.F * I + rr]);
+      v1q[slot] = (double)vb[(n + 2) * p.F];
+      v2q[slot] = (double)vb[NF + (n + 2) * p.F];
+    }
+    if (own) sy[r] = ycur;
+    __syncwarp();
+    // channel r
+    double zr = 0.0, zi = 0.0;
+#pragma unroll
+    for (int b = 0; b < I; ++b) {
+      const double2 yb_ = sy[b];
+      zr = fma(pc[b].x, yb_.x, fma(pc[b].y, yb_.y, zr));
+      zi = fma(pc[b].x, yb_.y, fma(-pc[b].y, yb_.x, zi));
+    }
+    const double v1l = v1 * lam;
+    const double den = v1l + v2;
+    const double rden = rcp_nr(den);
+    const double g1 = v1l * rden, g2 = v2 * rden;
+    const double c = v2 * g1;
+    const double pz = fma(zr, zr, zi * zi);
+    const double t1 = fma(g1 * g1, pz, c);
+    const double t2 = fma(g2 * g2, pz, c);
+    if (LL && own) llacc += log(den) + pz * rden;
+    if (own) {
+      sz[r] = cmk(zr, zi);
+      sg1[r] = g1;
+      sg2[r] = g2;
+    }
+    double w1 = 0.0, w2 = 0.0;
+    if (UPDATE) {
+      const double tr1 = group_sum<LB>(own ? t1 * il : 0.0);
+      const double tr2 = group_sum<LB>(own ? t2 : 0.0);
+      const double q1 = tr1 / I, q2 = tr2 / I;
+      w1 = (q1 < fl) ? fl : q1;
+      w2 = (q2 < fl) ? fl : q2;
+      if (r == 0) {
+        if (active) {
+          vb[n * p.F] = (R)w1;
+          vb[NF + n * p.F] = (R)w2;
+        }
+        const long long b1 = __double_as_longlong(w1), b2 = __double_as_longlong(w2);
+        const bool bad = (((b1 >> 52) & 0x7ff) == 0x7ff) | (((b2 >> 52) & 0x7ff) == 0x7ff) |
+                         (b1 <= 0) | (b2 <= 0);
+        if (bad && bad_n == 0) bad_n = n + 1;
+      }
+    }
+    __syncwarp();
+    if (UPDATE && own) {
+      const double iw1 = rcp_nr(w1), iw2 = rcp_nr(w2);
+      const double h1 = g1 * iw1, h2 = g2 * iw2;
+      acc1[r] = fma(t1, iw1, acc1[r]);
+      acc2[r] = fma(t2, iw2, acc2[r]);
+#pragma unroll
+      for (int cc = 0; cc < I; ++cc) {
+        if (cc <= r) continue;
+        const double2 zc = sz[cc];
+        const double xr = fma(zr, zc.x, zi * zc.y);   // z_r conj(z_c)
+        const double xi = fma(zi, zc.x, -zr * zc.y);
+        const double k1 = h1 * sg1[cc], k2 = h2 * sg2[cc];
+        acc1[cc] = fma(k1, xr, acc1[cc]);
+        acc1i[cc] = fma(k1, xi, acc1i[cc]);
+        acc2[cc] = fma(k2, xr, acc2[cc]);
+        acc2i[cc] = fma(k2, xi, acc2i[cc]);
+      }
+    }
+    if (MU && own && active) {
+      C* mo = (C*)p.mu_out;
+      C o1, o2;
+      if (p.mu_back) {
+        double sx = 0.0, sy_ = 0.0;
+#pragma unroll
+        for (int b = 0; b < I; ++b) {
+          const double2 zb = sz[b];
+          const double gb = sg1[b];
+          const double mx = gb * zb.x, my = gb * zb.y;
+          sx = fma(wr[b].x, mx, fma(-wr[b].y, my, sx));
+          sy_ = fma(wr[b].x, my, fma(wr[b].y, mx, sy_));
+        }
+        o1.x = sx;
+        o1.y = sy_;
+        o2.x = ycur.x - sx;  // partition mu_1 + mu_2 = y
+        o2.y = ycur.y - sy_;
+      } else {
+        o1.x = zr * g1;
+        o1.y = zi * g1;
+        o2.x = zr * g2;
+        o2.y = zi * g2;
+      }
+      mo[(((m * 2 + 0) * p.N + n) * p.F + f) * I + r] = o1;
+      mo[(((m * 2 + 1) * p.N + n) * p.F + f) * I + r] = o2;
+    }
+    __syncwarp();  // sy / sz are rewritten by the next frame
+  }
+  if (bad_n && active && p.st)
+    report_error(p.st, p.iter, FFCA_ERR_SINGULAR_MATRIX,
+                 (unsigned long long)((m * p.N + (bad_n - 1)) * p.F + f));
+  if (LL) llacc = group_sum<LB>(llacc);
+  if (!active) return;
+  const int64_t ch = blockIdx.y;
+  if (UPDATE && own) {
+    double* sp = p.Spart + (size_t)ch * 2 * NP * G + g;
+    sp[(size_t)r * G] = acc1[r];
+    sp[(size_t)(NP + r) * G] = acc2[r];
+#pragma unroll
+    for (int cc = 0; cc < I; ++cc) {
+      if (cc <= r) continue;
+      sp[(size_t)Herm<I>::re(r, cc) * G] = acc1[cc];
+      sp[(size_t)Herm<I>::im(r, cc) * G] = acc1i[cc];
+      sp[(size_t)(NP + Herm<I>::re(r, cc)) * G] = acc2[cc];
+      sp[(size_t)(NP + Herm<I>::im(r, cc)) * G] = acc2i[cc];
+    }
+  }
+  if (LL && r == 0) p.llbin[(size_t)ch * G + g] = llacc;
+}
+
+template <int I, typename R, bool UPDATE, bool LL, bool MU>
+static cudaError_t launch_fast_par_v(const FastIterParams& p, cudaStream_t s) {
+  using Lay = FastParLayout<I>;
+  dim3 grid((unsigned)((p.G + Lay::BPB - 1) / Lay::BPB), (unsigned)p.nchunk);
+  fast_par_kernel<I, R, UPDATE, LL, MU><<<grid, Lay::WARPS * 32, Lay::SMEM, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int I, typename R>
+static cudaError_t launch_fast_par_t(const FastIterParams& p, cudaStream_t s) {
+  const bool ll = p.llbin != nullptr;
+  const bool mu = p.mu_out != nullptr;
+  if (p.update) {
+    if (!ll && !mu) return launch_fast_par_v<I, R, true, false, false>(p, s);
+    if (ll && !mu) return launch_fast_par_v<I, R, true, true, false>(p, s);
+    if (!ll && mu) return launch_fast_par_v<I, R, true, false, true>(p, s);
+    return launch_fast_par_v<I, R, true, true, true>(p, s);
+  }
+  if (ll && !mu) return launch_fast_par_v<I, R, false, true, false>(p, s);
+  if (!ll && mu) return launch_fast_par_v<I, R, false, false, true>(p, s);
+  if (ll && mu) return launch_fast_par_v<I, R, false, true, true>(p, s);
+  return cudaSuccess;
+}
+
+cudaError_t launch_fast_par(const FastIterParams& p, int I, int dtype, cudaStream_t s) {
+  const bool f32 = dtype == FFCA_C64;
+  switch (I) {
+    case 5: return f32 ? launch_fast_par_t<5, float>(p, s) : launch_fast_par_t<5, double>(p, s);
+    case 6: return f32 ? launch_fast_par_t<6, float>(p, s) : launch_fast_par_t<6, double>(p, s);
+    case 7: return f32 ? launch_fast_par_t<7, float>(p, s) : launch_fast_par_t<7, double>(p, s);
+    case 8: return f32 ? launch_fast_par_t<8, float>(p, s) : launch_fast_par_t<8, double>(p, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int fast_par_blocks_per_sm(int I, int dtype) {
+  int n = 0;
+  const bool f32 = dtype == FFCA_C64;
+  switch (I) {
+#define FFCA_OCC(II)                                                                            \
+  case II:                                                                                      \
+    if (f32)                                                                                    \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                            \
+          &n, fast_par_kernel<II, float, true, false, false>, FastParLayout<II>::WARPS * 32,    \
+          FastParLayout<II>::SMEM);                                                              \
+    else                                                                                        \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                            \
+          &n, fast_par_kernel<II, double, true, false, false>, FastParLayout<II>::WARPS * 32,   \
+          FastParLayout<II>::SMEM);                                                              \
+    break;
+    FFCA_OCC(5)
+    FFCA_OCC(6)
+    FFCA_OCC(7)
+    FFCA_OCC(8)
+#undef FFCA_OCC
+  }
+  return n > 0 ? n : 1;
+}
+
+int fast_par_bins_per_cta() { return FastParLayout<8>::BPB; }
+
+}  // namespace ffca

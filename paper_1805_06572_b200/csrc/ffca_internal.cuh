@@ -102,6 +102,7 @@ int fca_blocks_per_sm(int I, int dtype);
 // FCA plan: the lane-parallel kernel (I >= 5) tiles fewer bins per CTA and
 // streams every frame of a chunk in one lane group
 void plan_fca_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames, int* nchunk);
+void plan_fast_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames, int* nchunk);
 
 int sm_count();
 

@@ -561,7 +561,7 @@ int ffca_fast_iteration(const double* y, const double* P, const double* v, const
       cudaSuccess)
     return FFCA_ERR_CUDA;
   FastIterParams p{};
-  plan_chunks(F, N, fast_blocks_per_sm(I, FFCA_C128), &p.chunk_frames, &p.nchunk);
+  plan_fast_chunks(F, N, I, FFCA_C128, &p.chunk_frames, &p.nchunk);
   double* Spart = nullptr;
   if (cudaMallocAsync((void**)&Spart, (size_t)p.nchunk * 2 * I * I * F * sizeof(double), s) !=
       cudaSuccess)
