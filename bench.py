@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--dtype", choices=["c128", "c64"], default="c128")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-other", action="store_true", help="skip the second engine")
     ap.add_argument("--cpu-sample", type=int, default=0, help="mixtures/bins in the CPU sample")
     return ap.parse_args()
 
@@ -325,6 +326,43 @@ def main():
                "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
                "s_per_step": round(float(et.item()), 4)}
 
+    # the other engine on the same resident inputs (the metric names both)
+    other = "fca" if args.engine == "fast" else "fast"
+    other_line = None
+    if not args.no_other:
+        ocf, _ = plan_chunks(cfg.M * cfg.F, cfg.N, cfg.I, args.dtype, other)
+        obufs = {"images": bufs["images"], "S": bufs["S"], "v": bufs["v"]}
+
+        def ostep():
+            return run_device(other, y_d, v_d, S_d, fl_d, L, likelihood=False, history=False,
+                              images=True, dtype=args.dtype, timing=False, check=False,
+                              chunk_frames=ocf, out=obufs)
+
+        r0 = ostep()
+        status_of(r0, N, F)
+        obufs["workspace"] = r0.workspace
+        del r0
+        osteps = max(2, args.steps // 2)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        o0 = torch.cuda.Event(enable_timing=True)
+        o1 = torch.cuda.Event(enable_timing=True)
+        o0.record()
+        for _ in range(osteps):
+            last = ostep()
+        o1.record()
+        torch.cuda.synchronize()
+        status_of(last, N, F)
+        del last
+        ot = torch.tensor([o0.elapsed_time(o1)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(ot, op=dist.ReduceOp.MAX)
+        oms = float(ot.item()) / osteps
+        other_line = {"engine": other, "value": tf_it_total / (oms / 1e3),
+                      "unit": "TF-bin*it/s", "ms_per_step": oms, "steps": osteps}
+        del obufs
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
@@ -345,6 +383,7 @@ def main():
                        "parallelism": f"{sh[0]}-sharded x{world}",
                        "l2": "inputs larger than L2 (y = %.2f GB)" % (Y.nbytes / 1e9 * world)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            ("fca" if other == "fca" else "fastfca"): other_line,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
         }

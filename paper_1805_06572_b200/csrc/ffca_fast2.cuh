@@ -101,6 +101,9 @@ struct Fast2Smem {
 #ifndef FAST2_STAGES
 #define FAST2_STAGES 6  // cp.async ring depth (frames per thread)
 #endif
+#ifndef FAST2_UNROLL
+#define FAST2_UNROLL 1  // frames per loop trip (ILP experiments)
+#endif
 
 template <int I, typename R, int WARPS, int STAGES, bool UPDATE, bool LL, bool MU>
 __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : FAST2_MINB) fast_em2_kernel(const FastIterParams p) {
@@ -137,11 +140,11 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : FAST2_MINB) fast_em2_kern
   if (MU && p.mu_back)
     for (int e = warp; e < NP; e += WARPS) sW[e * 32 + lane] = Math<R>::c2(p.W[g * NP + e]);
   __syncthreads();
-  T lam[I], il[I];
+  T lam[I], il[I];  // il = 1 / (I lam): the 1/I of v1 = tr1 / I folded in
 #pragma unroll
   for (int a = 0; a < I; ++a) {
     lam[a] = (T)p.lam[g * I + a];
-    il[a] = (T)(1.0 / p.lam[g * I + a]);
+    il[a] = (T)(1.0 / ((double)I * p.lam[g * I + a]));
   }
   const T fl = (T)p.floor[g];
   constexpr T invI = T(1) / I;
@@ -206,7 +209,8 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : FAST2_MINB) fast_em2_kern
     cp_async_commit();
   }
 
-#pragma unroll 1
+  constexpr int kUnroll = FAST2_UNROLL;
+#pragma unroll kUnroll
   for (int k = 0; k < K; ++k) {
     if (k + STAGES - 1 < K) issue(k + STAGES - 1);
     cp_async_commit();
@@ -235,7 +239,7 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : FAST2_MINB) fast_em2_kern
       z[a].y = zi;
     }
     T g1[I], g2[I], t1[I], t2[I];
-    T tr1 = 0, tr2 = 0;
+    T tr1 = 0, tr2 = 0;  // already divided by I (folded into ilI / invI)
     double lprod = 1.0, quad = 0.0;
     bool bad = false;
 #pragma unroll
@@ -245,12 +249,13 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : FAST2_MINB) fast_em2_kern
       const T rden = Math<R>::rcp(den);
       g1[a] = v1l * rden;
       g2[a] = v2 * rden;
-      const T c = v2 * g1[a];
       const T pz = fma(z[a].x, z[a].x, z[a].y * z[a].y);
-      t1[a] = fma(g1[a] * g1[a], pz, c);
-      t2[a] = fma(g2[a] * g2[a], pz, c);
+      // t_j = g_j^2 |z|^2 + c with c = v2 g1 = v1 lam g2 (reference
+      // _kernels_numba.py:359-363), factored to save one multiply each
+      t1[a] = g1[a] * fma(g1[a], pz, v2);
+      t2[a] = g2[a] * fma(g2[a], pz, v1l);
       tr1 = fma(t1[a], il[a], tr1);
-      tr2 += t2[a];
+      tr2 = fma(t2[a], invI, tr2);
       if (LL) {
         lprod *= (double)den;
         quad = fma((double)pz, (double)rden, quad);
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : FAST2_MINB) fast_em2_kern
     }
     if (LL) llacc += log(lprod) + quad;
     if (UPDATE) {
-      const T q1 = tr1 * invI, q2 = tr2 * invI;
+      const T q1 = tr1, q2 = tr2;
       const T w1 = (q1 < fl) ? fl : q1;  // NaN propagates like np.maximum
       const T w2 = (q2 < fl) ? fl : q2;
       if (active) {
