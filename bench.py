@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-other", action="store_true", help="skip the second engine")
+    ap.add_argument("--streams", type=int, default=2,
+                    help="concurrent streams over independent mixtures (batched configs)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="mixtures/bins in the CPU sample")
     return ap.parse_args()
 
@@ -228,6 +230,8 @@ def main():
     tf_it_rank = M * F * N * L
     tf_it_total = cfg.M * cfg.F * cfg.N * L
 
+    from paper_1805_06572_b200._engine import status_of
+
     # outputs and workspace are allocated once: a step is the EM run, not cudaMalloc
     bufs = {"images": torch.empty((M, 2, N, F, I), dtype=ctype, device=dev),
             "S": torch.empty((M, 2, F, I, I), dtype=torch.complex128, device=dev),
@@ -239,6 +243,28 @@ def main():
                           chunk_frames=cf, kernel_timing=timing, out=bufs)
 
     bufs["workspace"] = step().workspace
+    nstreams = args.streams if M > 1 else 1
+    if nstreams > 1:  # independent mixtures on concurrent streams (hides K1 and wave tails)
+        from paper_1805_06572_b200._engine import run_device_streams
+
+        sstreams = [torch.cuda.Stream() for _ in range(nstreams)]
+        first = run_device_streams(args.engine, y_d, v_d, S_d, fl_d, L, nstreams=nstreams,
+                                   out=bufs, likelihood=False, history=False, images=True,
+                                   dtype=args.dtype, timing=False, check=False,
+                                   chunk_frames=cf, streams=sstreams)
+        torch.cuda.synchronize()
+        wss = [r.workspace for r in first.parts]
+        for r in first.parts:
+            status_of(r, N, F)
+        plain_step = step
+
+        def step(timing=False):  # noqa: F811
+            if timing:
+                return plain_step(timing=True)
+            return run_device_streams(args.engine, y_d, v_d, S_d, fl_d, L, nstreams=nstreams,
+                                      out=bufs, workspaces=wss, likelihood=False, history=False,
+                                      images=True, dtype=args.dtype, timing=False, check=False,
+                                      chunk_frames=cf, streams=sstreams)
 
     for _ in range(args.warmup):
         step()
@@ -257,7 +283,8 @@ def main():
     ms = start.elapsed_time(end)
     from paper_1805_06572_b200._engine import status_of
 
-    status_of(last, N, F)
+    for r in (last.parts if hasattr(last, "parts") else [last]):
+        status_of(r, N, F)
     del last
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
@@ -380,7 +407,8 @@ def main():
         cpu = {"value": v_cpu, "unit": "TF-bin*it/s", "cores": cores, "kind": kind,
                "sample": desc}
 
-    launches_per_step = 2 + 2 * L  # status init + initial pencil + L x (fused pass + pencil)
+    # status init + initial pencil + L x (fused pass + pencil), per concurrent part
+    launches_per_step = (2 + 2 * L) * nstreams
     if rank == 0:
         line = {
             "metric": f"EM TF-bin*iterations/s ({'FastFCA' if args.engine == 'fast' else 'FCA'}, config {cfg.index})",
@@ -391,6 +419,7 @@ def main():
             "config": {"workload": cfg.description, "engine": args.engine, "iterations": L,
                        "M": cfg.M, "F": cfg.F, "N": cfg.N, "I": cfg.I,
                        "parallelism": f"{sh[0]}-sharded x{world}",
+                       "streams_per_gpu": nstreams,
                        "l2": "inputs larger than L2 (y = %.2f GB)" % (Y.nbytes / 1e9 * world)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             ("fca" if other == "fca" else "fastfca"): other_line,

@@ -285,3 +285,53 @@ def run_host_pipelined(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=
     return {"images": out_img.numpy(), "v": out_v.numpy(), "S": out_S.numpy(),
             "floor": fh.numpy(), "loglik": out_ll.numpy() if likelihood else None,
             "iteration_ms": runs[0][0].iteration_ms, "chunks": len(bounds)}
+
+
+class MultiStreamRun:
+    """A batched device run split over several CUDA streams (see run_device_streams)."""
+
+    def __init__(self, parts, streams, events):
+        self.parts = parts
+        self.streams = streams
+        self.events = events
+
+    def wait(self):
+        cur = D.torch.cuda.current_stream()
+        for e in self.events:
+            cur.wait_event(e)
+
+
+def run_device_streams(algorithm, y, v0, S0, v_floor, iterations, *, nstreams=2, out=None,
+                       workspaces=None, **kw):
+    """Independent mixtures of a batch run as ``nstreams`` concurrent device
+    runs (one stream each): while one part is in its per-bin pencil update or
+    its last partial wave, the other part's streaming pass fills the SMs.
+    Outputs are written into ``out`` (images, S, v: full-batch tensors);
+    per-part workspaces are reused when given. Same results as one run with
+    the same ``chunk_frames``."""
+    torch = D.torch
+    M = int(y.shape[0])
+    k = max(1, min(int(nstreams), M))
+    bounds = [(M * i // k, M * (i + 1) // k) for i in range(k)]
+    cur = torch.cuda.current_stream()
+    streams = kw.pop("streams", None) or [torch.cuda.Stream() for _ in range(k)]
+    parts, events = [], []
+    for i, (a, b) in enumerate(bounds):
+        s = streams[i]
+        s.wait_stream(cur)
+        with torch.cuda.stream(s):
+            o = None
+            if out is not None:
+                o = {key: (t[a:b] if key in ("images", "S", "v") and t is not None else t)
+                     for key, t in out.items() if key != "workspace"}
+                if workspaces is not None and workspaces[i] is not None:
+                    o["workspace"] = workspaces[i]
+            r = run_device(algorithm, y[a:b], v0[a:b], S0[a:b], v_floor[a:b], iterations,
+                           out=o, **kw)
+            ev = torch.cuda.Event()
+            ev.record(s)
+        parts.append(r)
+        events.append(ev)
+    for e in events:
+        cur.wait_event(e)
+    return MultiStreamRun(parts, streams, events)

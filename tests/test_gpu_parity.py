@@ -145,6 +145,31 @@ def test_pipelined_host_path_equals_device_path():
     assert np.array_equal(res["loglik"], ref.loglik.cpu().numpy())
 
 
+def test_multistream_run_equals_single_stream_run():
+    import torch
+
+    from paper_1805_06572_b200._engine import plan_chunks, run_device, run_device_streams
+
+    P = _pkg()
+    gen = np.random.default_rng(22)
+    Y = torch.from_numpy(random_complex(gen, (6, 90, 13, 3))).cuda()
+    inits = [P.init_random(Y[m], 50 + m) for m in range(6)]
+    V = torch.stack([i.v for i in inits])
+    S = torch.stack([i.S for i in inits])
+    FL = torch.stack([i.v_floor for i in inits])
+    cf, _ = plan_chunks(6 * 13, 90, 3)
+    ref = run_device("fast", Y, V, S, FL, 5, likelihood=False, chunk_frames=cf)
+    out = {"images": torch.empty_like(ref.images), "S": torch.empty_like(ref.S),
+           "v": torch.empty_like(ref.v)}
+    ms = run_device_streams("fast", Y, V, S, FL, 5, nstreams=3, out=out, likelihood=False,
+                            chunk_frames=cf, check=False)
+    torch.cuda.synchronize()
+    assert torch.equal(out["images"], ref.images)
+    assert torch.equal(out["v"], ref.v)
+    assert torch.equal(out["S"], ref.S)
+    assert len(ms.parts) == 3
+
+
 def test_bin_shards_are_bitwise_identical_to_the_full_run():
     """Frequency bins are independent; with equal frame chunking the per-bin
     reduction order is the same, so 1-GPU and k-GPU runs agree bit for bit."""
