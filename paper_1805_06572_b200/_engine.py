@@ -71,6 +71,16 @@ def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, hi
     if L < 0:
         raise ConfigurationError("iterations must be >= 0")
     res = out or {}
+    # preallocated outputs must match exactly: the kernels trust dtype/shape
+    want = {"v": (rtype, (M, 2, N, F)), "images": (ctype, (M, 2, N, F, I)),
+            "S": (torch.complex128, (M, 2, F, I, I)), "loglik": (torch.float64, (M, L + 1))}
+    for key, (dt, shp) in want.items():
+        t = res.get(key)
+        if t is not None and (t.dtype != dt or tuple(t.shape) != shp or not t.is_cuda or
+                              not t.is_contiguous()):
+            raise ConfigurationError(
+                f"out[{key!r}] must be a contiguous CUDA {dt} tensor of shape {shp}, got "
+                f"{t.dtype} {tuple(t.shape)}")
     v = D.to_device(v0, rtype)
     if res.get("v") is not None:
         res["v"].copy_(v)  # preallocated work buffer: the run updates v in place

@@ -5,6 +5,8 @@
 // ffca_fca_run mirrors fca_run (conventional.py:104-164): same iteration
 // structure, same likelihood / history / image semantics, but every step is
 // a kernel on one stream and nothing returns to the host inside the loop.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "ffca_internal.cuh"
@@ -122,10 +124,25 @@ int check_args(const ffca_run_args* a) {
 }
 
 inline int cu(cudaError_t e) { return e == cudaSuccess ? FFCA_OK : FFCA_ERR_CUDA; }
-#define FFCA_TRY(expr)                 \
-  do {                                 \
-    int _rc = cu(expr);                \
-    if (_rc != FFCA_OK) return _rc;    \
+// FFCA_DEBUG_SYNC=1: synchronise after every launch and name the failing step
+inline bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FFCA_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+inline cudaError_t checked(cudaError_t e, const char* what, int line) {
+  if (e == cudaSuccess && debug_sync()) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess && debug_sync())
+    fprintf(stderr, "ffca: %s (capi line %d) failed: %s\n", what, line, cudaGetErrorString(e));
+  return e;
+}
+#define FFCA_TRY(expr)                                   \
+  do {                                                   \
+    int _rc = cu(checked((expr), #expr, __LINE__));      \
+    if (_rc != FFCA_OK) return _rc;                      \
   } while (0)
 
 inline size_t real_size(int dtype) { return dtype == FFCA_C64 ? 4 : 8; }

@@ -12,6 +12,13 @@
 #include "ffca_fast2.cuh"
 #include "ffca_pencil_par.cuh"
 
+#ifdef FFCA_DEBUG_BOUNDS
+#include <cassert>
+#define FFCA_CHECK(cond) assert(cond)
+#else
+#define FFCA_CHECK(cond) ((void)0)
+#endif
+
 namespace ffca {
 
 namespace {
@@ -66,6 +73,15 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32) fast_par_kernel(
   const int64_t NF = p.N * p.F;
   const C* __restrict__ yb = (const C*)p.y + (m * p.N * p.F + f) * I;
   R* __restrict__ vb = (R*)p.v + m * 2 * NF + f;
+  FFCA_CHECK(g >= 0 && g < G && m < p.M && n0 >= 0 && n1 <= p.N);
+#ifdef FFCA_DEBUG_BOUNDS
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+    printf("fast_par I=%d R=%d U%d L%d M%d: M=%ld N=%ld F=%ld G=%ld cf=%ld nc=%d y=%p v=%p P=%p W=%p lam=%p fl=%p Sp=%p ll=%p mu=%p st=%p\n",
+           I, (int)sizeof(R), (int)UPDATE, (int)LL, (int)MU, (long)p.M, (long)p.N, (long)p.F,
+           (long)p.G, (long)p.chunk_frames, p.nchunk, p.y, p.v, (const void*)p.P,
+           (const void*)p.W, (const void*)p.lam, (const void*)p.floor, (void*)p.Spart,
+           (void*)p.llbin, p.mu_out, (void*)p.st);
+#endif
 
   double acc1[I], acc2[I];  // row rr: [c] = Re (c == rr) or (re, im) packed as below
   double acc1i[I], acc2i[I];
@@ -83,6 +99,7 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32) fast_par_kernel(
     yq[k] = cmk(0.0, 0.0);
     v1q[k] = v2q[k] = 1.0;
     if (n < n1) {
+      FFCA_CHECK((m * p.N * p.F + f) * I + n * p.F * I + rr < p.M * p.N * p.F * I);
       yq[k] = to_c128(yb[n * p.F * I + rr]);
       v1q[k] = (double)vb[n * p.F];
       v2q[k] = (double)vb[NF + n * p.F];
@@ -94,6 +111,7 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32) fast_par_kernel(
     const double2 ycur = yq[slot];
     const double v1 = v1q[slot], v2 = v2q[slot];
     if (n + 2 < n1) {
+      FFCA_CHECK((m * p.N * p.F + f) * I + (n + 2) * p.F * I + rr < p.M * p.N * p.F * I);
       yq[slot] = to_c128(yb[(n + 2) * p.F * I + rr]);
       v1q[slot] = (double)vb[(n + 2) * p.F];
       v2q[slot] = (double)vb[NF + (n + 2) * p.F];
@@ -195,6 +213,7 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32) fast_par_kernel(
   const int64_t ch = blockIdx.y;
   if (UPDATE && own) {
     double* sp = p.Spart + (size_t)ch * 2 * NP * G + g;
+    FFCA_CHECK(ch < p.nchunk);
     sp[(size_t)r * G] = acc1[r];
     sp[(size_t)(NP + r) * G] = acc2[r];
 #pragma unroll

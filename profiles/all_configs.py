@@ -1,0 +1,87 @@
+#!/usr/bin/env python3
+"""Throughput of both engines on all five BASELINE configs (1 GPU, inputs
+resident in HBM, outputs preallocated), plus the CPU oracle port on a bounded
+sample of each config. One JSON line per (config, engine, dtype).
+
+    python profiles/all_configs.py [--cpu] [--steps 3]
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+from bench import make_inputs, shard  # noqa: E402
+from paper_1805_06572_b200._engine import plan_chunks, run_device, status_of, torch_types  # noqa: E402
+from paper_1805_06572_b200.synth import CONFIGS  # noqa: E402
+
+
+def measure(cfg, engine, dtype, steps, Y, V, S, FL):
+    ctype, rtype = torch_types(dtype)
+    y = torch.from_numpy(Y).cuda().to(ctype)
+    v = torch.from_numpy(V).cuda().to(rtype)
+    s = torch.from_numpy(S).cuda()
+    fl = torch.from_numpy(FL).cuda()
+    M, N, F, I = Y.shape
+    cf, nc = plan_chunks(M * F, N, I, dtype, engine)
+    bufs = {"images": torch.empty((M, 2, N, F, I), dtype=ctype, device="cuda"),
+            "S": torch.empty((M, 2, F, I, I), dtype=torch.complex128, device="cuda"),
+            "v": torch.empty_like(v)}
+    r = run_device(engine, y, v, s, fl, cfg.L, likelihood=False, check=False, out=bufs,
+                   chunk_frames=cf, dtype=dtype)
+    status_of(r)
+    bufs["workspace"] = r.workspace
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        r = run_device(engine, y, v, s, fl, cfg.L, likelihood=False, check=False, out=bufs,
+                       chunk_frames=cf, dtype=dtype)
+    e1.record()
+    torch.cuda.synchronize()
+    status_of(r)
+    ms = e0.elapsed_time(e1) / steps
+    kr = run_device(engine, y, v, s, fl, cfg.L, likelihood=False, check=True, out=bufs,
+                    chunk_frames=cf, kernel_timing=True, dtype=dtype)
+    hot = kr.kernel_ms[:-1] if len(kr.kernel_ms) > 1 else kr.kernel_ms
+    k_ms = sum(hot) / len(hot) if hot else float("nan")
+    r_bytes = 8 if dtype == "c128" else 4
+    gbs = (2 * I + 4) * r_bytes * M * F * N / (k_ms / 1e3) / 1e9
+    return {"config": cfg.index, "engine": engine, "dtype": dtype,
+            "tf_bin_it_per_s": M * F * N * cfg.L / (ms / 1e3), "ms_per_run": ms,
+            "pass_ms": k_ms, "pass_GBps": gbs, "chunk_frames": cf, "nchunk": nc}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--cpu", action="store_true")
+    ap.add_argument("--configs", default="0,1,2,3,4")
+    a = ap.parse_args()
+    for idx in [int(x) for x in a.configs.split(",")]:
+        cfg = CONFIGS[idx]
+        Y, V, S, FL = make_inputs(cfg, shard(cfg, 0, 1))
+        for engine in ("fast", "fca"):
+            for dtype in cfg.dtypes:
+                rec = measure(cfg, engine, dtype, a.steps, Y, V, S, FL)
+                if a.cpu and dtype == "c128":
+                    from oracle import cpu_port
+
+                    t0 = time.time()
+                    val, desc, kind, cores = cpu_port.measure(cfg, engine, 0,
+                                                              len(os.sched_getaffinity(0)))
+                    rec["cpu_port"] = {"tf_bin_it_per_s": val, "sample": desc, "cores": cores,
+                                       "wall_s": round(time.time() - t0, 1)}
+                print(json.dumps(rec), flush=True)
+        del Y, V, S, FL
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

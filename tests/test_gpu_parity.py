@@ -170,6 +170,21 @@ def test_multistream_run_equals_single_stream_run():
     assert len(ms.parts) == 3
 
 
+def test_mismatched_output_buffers_are_rejected():
+    import torch
+
+    from paper_1805_06572_b200._engine import run_device
+    from paper_1805_06572_b200.errors import ConfigurationError
+
+    P = _pkg()
+    gen = np.random.default_rng(23)
+    y = random_complex(gen, (20, 5, 2))
+    init = P.init_random(y, 1)
+    bad = {"v": torch.empty((1, 2, 20, 5), dtype=torch.float32, device="cuda")}
+    with pytest.raises(ConfigurationError):
+        run_device("fast", y[None], init.v[None], init.S[None], init.v_floor[None], 2, out=bad)
+
+
 def test_bin_shards_are_bitwise_identical_to_the_full_run():
     """Frequency bins are independent; with equal frame chunking the per-bin
     reduction order is the same, so 1-GPU and k-GPU runs agree bit for bit."""
