@@ -31,7 +31,8 @@ struct FastParLayout {
   static constexpr int RAW = 6 * I;
   static constexpr int U16 = (RAW + 1) / 2;
   static constexpr int GROUP_DOUBLES = 2 * ((U16 % 2) ? U16 : U16 + 1);
-  static constexpr size_t SMEM = (size_t)BPB * GROUP_DOUBLES * sizeof(double);
+  static constexpr size_t RINGB = (size_t)8 * WARPS * 32 * 48;  // 8 stages x 64 lanes x 48 B
+  static constexpr size_t SMEM = (size_t)BPB * GROUP_DOUBLES * sizeof(double) + RINGB;
 };
 }  // namespace
 
@@ -83,39 +84,56 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32) fast_par_kernel(
            (void*)p.llbin, p.mu_out, (void*)p.st);
 #endif
 
-  double acc1[I], acc2[I];  // row rr: [c] = Re (c == rr) or (re, im) packed as below
-  double acc1i[I], acc2i[I];
+  // row rr of both accumulators: diagonal (real) and the entries c > rr;
+  // arrays are only ever indexed by compile-time c (runtime indexing would
+  // demote them to local memory)
+  double accd1 = 0.0, accd2 = 0.0;
+  double acc1[I], acc2[I], acc1i[I], acc2i[I];
 #pragma unroll
   for (int c = 0; c < I; ++c) acc1[c] = acc2[c] = acc1i[c] = acc2i[c] = 0.0;
   double llacc = 0.0;
   int64_t bad_n = 0;
 
-  // two frames of register prefetch
-  double2 yq[2];
-  double v1q[2], v2q[2];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  // per-lane cp.async ring (kStages frames in flight, no registers held):
+  // slot = y_r | v1 | v2, padded to an odd number of 16-B units
+  constexpr int kStages = 8;
+  constexpr int YB = (int)sizeof(C), VB = (int)sizeof(R);
+  constexpr int SLOT = 16 * ((((YB + 2 * VB + 15) / 16) % 2) ? (YB + 2 * VB + 15) / 16
+                                                                : (YB + 2 * VB + 15) / 16 + 1);
+  unsigned char* ring = (unsigned char*)(sm + (size_t)Lay::BPB * Lay::GROUP_DOUBLES) +
+                        (size_t)threadIdx.x * SLOT;
+  constexpr size_t kStageStride = (size_t)Lay::WARPS * 32 * SLOT;
+  const int K = (int)(n1 - n0 > 0 ? n1 - n0 : 0);
+  auto issue = [&](int k) {
     const int64_t n = n0 + k;
-    yq[k] = cmk(0.0, 0.0);
-    v1q[k] = v2q[k] = 1.0;
-    if (n < n1) {
-      FFCA_CHECK((m * p.N * p.F + f) * I + n * p.F * I + rr < p.M * p.N * p.F * I);
-      yq[k] = to_c128(yb[n * p.F * I + rr]);
-      v1q[k] = (double)vb[n * p.F];
-      v2q[k] = (double)vb[NF + n * p.F];
+    unsigned char* slot = ring + (size_t)(k % kStages) * kStageStride;
+    if constexpr (YB == 16)
+      cp_async16(slot, yb + n * p.F * I + rr);
+    else
+      cp_async8(slot, yb + n * p.F * I + rr);
+    if constexpr (VB == 8) {
+      cp_async8(slot + YB, vb + n * p.F);
+      cp_async8(slot + YB + 8, vb + NF + n * p.F);
+    } else {
+      cp_async4(slot + YB, vb + n * p.F);
+      cp_async4(slot + YB + 4, vb + NF + n * p.F);
     }
+  };
+#pragma unroll
+  for (int k = 0; k < kStages - 1; ++k) {
+    if (k < K) issue(k);
+    cp_async_commit();
   }
 #pragma unroll 1
   for (int64_t n = n0; n < n1; ++n) {
-    const int slot = (int)((n - n0) & 1);
-    const double2 ycur = yq[slot];
-    const double v1 = v1q[slot], v2 = v2q[slot];
-    if (n + 2 < n1) {
-      FFCA_CHECK((m * p.N * p.F + f) * I + (n + 2) * p.F * I + rr < p.M * p.N * p.F * I);
-      yq[slot] = to_c128(yb[(n + 2) * p.F * I + rr]);
-      v1q[slot] = (double)vb[(n + 2) * p.F];
-      v2q[slot] = (double)vb[NF + (n + 2) * p.F];
-    }
+    const int k = (int)(n - n0);
+    if (k + kStages - 1 < K) issue(k + kStages - 1);
+    cp_async_commit();
+    cp_async_wait<kStages - 1>();
+    const unsigned char* slot = ring + (size_t)(k % kStages) * kStageStride;
+    const double2 ycur = to_c128(*(const C*)slot);
+    const double v1 = (double)*(const R*)(slot + YB);
+    const double v2 = (double)*(const R*)(slot + YB + VB);
     if (own) sy[r] = ycur;
     __syncwarp();
     // channel r
@@ -162,8 +180,8 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32) fast_par_kernel(
     if (UPDATE && own) {
       const double iw1 = rcp_nr(w1), iw2 = rcp_nr(w2);
       const double h1 = g1 * iw1, h2 = g2 * iw2;
-      acc1[r] = fma(t1, iw1, acc1[r]);
-      acc2[r] = fma(t2, iw2, acc2[r]);
+      accd1 = fma(t1, iw1, accd1);
+      accd2 = fma(t2, iw2, accd2);
 #pragma unroll
       for (int cc = 0; cc < I; ++cc) {
         if (cc <= r) continue;
@@ -205,6 +223,7 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32) fast_par_kernel(
     }
     __syncwarp();  // sy / sz are rewritten by the next frame
   }
+  cp_async_wait_all();
   if (bad_n && active && p.st)
     report_error(p.st, p.iter, FFCA_ERR_SINGULAR_MATRIX,
                  (unsigned long long)((m * p.N + (bad_n - 1)) * p.F + f));
@@ -214,8 +233,8 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32) fast_par_kernel(
   if (UPDATE && own) {
     double* sp = p.Spart + (size_t)ch * 2 * NP * G + g;
     FFCA_CHECK(ch < p.nchunk);
-    sp[(size_t)r * G] = acc1[r];
-    sp[(size_t)(NP + r) * G] = acc2[r];
+    sp[(size_t)r * G] = accd1;
+    sp[(size_t)(NP + r) * G] = accd2;
 #pragma unroll
     for (int cc = 0; cc < I; ++cc) {
       if (cc <= r) continue;

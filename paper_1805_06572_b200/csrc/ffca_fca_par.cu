@@ -222,8 +222,8 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
 #pragma unroll
           for (int k = 0; k < I; ++k) s = cadd(s, cmul(packed_get<I>(S1, r, k), at(Tm, k, c)));
           cr[c] = cscale(s, vv);
+          if (c == r) cr[c].y = 0.0;  // compile-time index only: cr stays in registers
         }
-        cr[r].y = 0.0;
         const double2 m1r = vm1[r], m2r = vm2[r];
 #pragma unroll
         for (int b = 0; b < I; ++b) {
