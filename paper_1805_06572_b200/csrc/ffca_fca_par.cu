@@ -119,12 +119,16 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
       }
     }
     __syncwarp();
-    // Cholesky in place (lower), column-sequential
+    // Cholesky in place (lower), column-sequential. Every loop below is
+    // unrolled over compile-time indices with the triangular bounds as
+    // predicates: independent products interleave (ILP) instead of forming
+    // one dependent chain of shared-memory loads per loop.
     bool okc = true;
-#pragma unroll 1
+#pragma unroll
     for (int j = 0; j < I; ++j) {
       if (own && r == j) {
         double d = at(Lm, j, j).x;
+#pragma unroll
         for (int k = 0; k < j; ++k) d -= cabs2(at(Lm, j, k));
         misc[0] = d;
         at(Lm, j, j) = cmk(sqrt(fmax(d, 0.0)), 0.0);
@@ -133,34 +137,37 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
       okc = okc && misc[0] > 0.0;
       if (own && r > j) {
         double2 s = at(Lm, r, j);
+#pragma unroll
         for (int k = 0; k < j; ++k) s = csub(s, cmulc(at(Lm, r, k), at(Lm, j, k)));
         at(Lm, r, j) = cscale(s, 1.0 / at(Lm, j, j).x);
       }
       __syncwarp();
     }
     if (!okc && bad_n == 0) bad_n = n + 1;
-    // L^-1, column-parallel
+    // L^-1, column-parallel: lane c keeps its column in registers
     if (own) {
-      const int c = r;
-#pragma unroll 1
+      double2 col[I];
+#pragma unroll
       for (int rr = 0; rr < I; ++rr) {
-        if (rr < c) {
-          at(Li, rr, c) = cmk(0.0, 0.0);
-          continue;
-        }
-        double2 s = cmk(rr == c ? 1.0 : 0.0, 0.0);
-        for (int k = c; k < rr; ++k) s = csub(s, cmul(at(Lm, rr, k), at(Li, k, c)));
-        at(Li, rr, c) = cscale(s, 1.0 / at(Lm, rr, rr).x);
+        double2 sacc = cmk(rr == r ? 1.0 : 0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < rr; ++k)
+          if (k >= r) sacc = csub(sacc, cmul(at(Lm, rr, k), col[k]));
+        col[rr] = (rr >= r) ? cscale(sacc, 1.0 / at(Lm, rr, rr).x) : cmk(0.0, 0.0);
       }
+#pragma unroll
+      for (int rr = 0; rr < I; ++rr) at(Li, rr, r) = col[rr];
     }
     __syncwarp();
     // u = L^-1 y (row r), likelihood terms
     double lquad = 0.0, llog = 0.0;
     if (own) {
-      double2 s = cmk(0.0, 0.0);
-      for (int k = 0; k <= r; ++k) s = cadd(s, cmul(at(Li, r, k), vy[k]));
-      vu[r] = s;
-      lquad = cabs2(s);
+      double2 sacc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < I; ++k)
+        if (k <= r) sacc = cadd(sacc, cmul(at(Li, r, k), vy[k]));
+      vu[r] = sacc;
+      lquad = cabs2(sacc);
       llog = log(at(Lm, r, r).x);
     }
     __syncwarp();
@@ -171,13 +178,20 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
     // x = L^-H u = R^-1 y; Y2 = L^-1 S2 into Lm (L no longer needed)
     double2 y2row[I];
     if (own) {
-      double2 s = cmk(0.0, 0.0);
-      for (int k = r; k < I; ++k) s = cadd(s, cconjmul(at(Li, k, r), vu[k]));
-      vx[r] = s;
+      double2 sacc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < I; ++k)
+        if (k >= r) sacc = cadd(sacc, cconjmul(at(Li, k, r), vu[k]));
+      vx[r] = sacc;
+      double2 lrow[I];
+#pragma unroll
+      for (int k = 0; k < I; ++k) lrow[k] = at(Li, r, k);
 #pragma unroll
       for (int c = 0; c < I; ++c) {
         double2 t = cmk(0.0, 0.0);
-        for (int k = 0; k <= r; ++k) t = cadd(t, cmul(at(Li, r, k), packed_get<I>(S2, k, c)));
+#pragma unroll
+        for (int k = 0; k < I; ++k)
+          if (k <= r) t = cadd(t, cmul(lrow[k], packed_get<I>(S2, k, c)));
         y2row[c] = t;
       }
     }
@@ -197,10 +211,15 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
       }
       vm1[r] = cscale(s1, v1);
       vm2[r] = cscale(s2, v2);
+      double2 lcol[I];  // column r of Li: conj -> row r of Li^H
+#pragma unroll
+      for (int k = 0; k < I; ++k) lcol[k] = at(Li, k, r);
 #pragma unroll
       for (int c = 0; c < I; ++c) {
         double2 t = cmk(0.0, 0.0);
-        for (int k = r; k < I; ++k) t = cadd(t, cconjmul(at(Li, k, r), at(Lm, k, c)));
+#pragma unroll
+        for (int k = 0; k < I; ++k)
+          if (k >= r) t = cadd(t, cconjmul(lcol[k], at(Lm, k, c)));
         at(Tm, r, c) = t;
       }
     }
