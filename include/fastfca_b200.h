@@ -190,6 +190,21 @@ int ffca_logdet2(const double* P, double* out, int64_t batch, int D, void* strea
 int ffca_init_powers(const void* y, void* v, double* v_floor, int64_t M, int64_t N, int64_t F,
                      int I, int dtype, void* stream);
 
+/* ---- STFT front / back end (reference stft.py:9-107) ----------------------
+ * Square-root periodic Hann window, frame_shift = frame_length / 2, half a
+ * frame of leading zeros; frame_length a power of two in [2, 8192].
+ * frames = max((length - 1) / shift + 2, 2)   (stft.py:30-32, num_frames) */
+int64_t ffca_stft_frames(int64_t length, int frame_shift);
+/* stft_analyze (stft.py:35-70): x (batch, channels, length) f64 ->
+ * spec (batch, frames, frame_length/2 + 1, channels) c128 */
+int ffca_stft_analyze(const double* x, double* spec, int64_t batch, int channels, int64_t length,
+                      int frame_length, void* stream);
+/* stft_synthesize (stft.py:73-107): spec (batch, frames, frame_length/2 + 1,
+ * channels) c128 -> out (batch, channels, length) f64, DC / Nyquist taken as
+ * real, overlap-add trimmed to [shift, shift + length); length <= frames * shift */
+int ffca_stft_synthesize(const double* spec, double* out, int64_t batch, int channels,
+                         int64_t frames, int frame_length, int64_t length, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,29 +6,37 @@ Two-source multichannel separation with full-rank spatial covariances:
 run entirely on the GPU through hand-written sm_100a CUDA kernels in
 ``lib/libfastfca_b200.so`` (C ABI: ``include/fastfca_b200.h``). Names,
 signatures, layouts, return types and exceptions follow the reference
-(``pkg/src/fastfca/__init__.py:10-77``) for everything on the EM path; the
-STFT front end, simulator, metrics and CLI are out of scope.
+(``pkg/src/fastfca/__init__.py:10-77``) for everything on the EM path and
+the STFT front / back end (``stft_analyze`` / ``stft_synthesize``, also on
+the GPU); ``separate`` chains analysis -> init -> EM -> synthesis in HBM.
+The simulator, metrics, WAV I/O and CLI are out of scope.
 """
 
 from .conventional import e_step, fca_run, log_likelihood, m_step
 from .errors import (BackendUnavailableError, ConfigurationError, DefinitenessError,
-                     FastFcaError, NonHermitianError, SingularMatrixError,
+                     FastFcaError, NonHermitianError, PipelineError, SingularMatrixError,
                      SingularMixtureError)
 from .fast import (fast_e_step, fast_m_step_S, fast_m_step_v, fastfca_run, propagate_pencil,
                    transform_observations)
 from .initializers import init_random
 from .pencil import PencilDecomposition, gevd_hpd, hermitian_eig, solve_hermitian_system
-from .types import OpCounts, PosteriorMoments, SeparationResult, SpatialModel, SpectrogramTensor
+from .pipeline import separate, separate_device
+from .stft import (sqrt_hann, stft_analyze, stft_analyze_device, stft_synthesize,
+                   stft_synthesize_device)
+from .types import (AudioBuffer, OpCounts, PosteriorMoments, SeparationResult, SpatialModel,
+                    SpectrogramTensor)
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "AudioBuffer",
     "BackendUnavailableError",
     "ConfigurationError",
     "DefinitenessError",
     "FastFcaError",
     "NonHermitianError",
     "OpCounts",
+    "PipelineError",
     "PencilDecomposition",
     "PosteriorMoments",
     "SeparationResult",
@@ -48,6 +56,13 @@ __all__ = [
     "log_likelihood",
     "m_step",
     "propagate_pencil",
+    "separate",
+    "separate_device",
     "solve_hermitian_system",
+    "sqrt_hann",
+    "stft_analyze",
+    "stft_analyze_device",
+    "stft_synthesize",
+    "stft_synthesize_device",
     "transform_observations",
 ]
