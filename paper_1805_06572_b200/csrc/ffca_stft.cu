@@ -2,6 +2,8 @@
 // square-root periodic Hann window, 50% overlap, half a frame of leading zero
 // padding, rfft / irfft per frame and overlap-add.
 //
+// Frame lengths up to 4096 run the team-FFT kernels below (register radix-16
+// Stockham passes); 8192 runs the simpler radix-2 shared-memory kernels.
 // Both directions are persistent kernels (grid = resident CTAs, each CTA a
 // contiguous run of frames / output hops) so the per-CTA tables (twiddles
 // e^{-2 pi i k / L} and the window) are built once per CTA, not per frame.
@@ -272,6 +274,393 @@ int stft_grid(K kern, size_t smem, int64_t work) {
   return (int)(work < cap ? work : cap);
 }
 
+// ---------------------------------------------------------------------------
+// Team FFT kernels (frame lengths 2 .. 4096): a transform of H = L/2 complex
+// points is owned by a team of T = H/E lanes, each holding E = min(H, 16)
+// points in registers. Stockham autosort passes of radix 16 (the last one
+// radix 2..16): a lane's radix-R butterflies run in registers, and one
+// shared-memory exchange (padded 1-in-16 against bank conflicts) separates
+// consecutive passes — 1-3 exchanges per transform instead of log2(H)
+// synchronised radix-2 stages. A CTA runs 256/T transforms per round: groups
+// of whole frames (all channels, when they fit), so the analysis writes a
+// round's output as one contiguous run of the (frame, bin, channel) tensor.
+// ---------------------------------------------------------------------------
+template <int LOGH>
+struct TeamFft {
+  static constexpr int H = 1 << LOGH;
+  static constexpr int L = 2 * H;
+  static constexpr int LOGE = LOGH < 4 ? LOGH : 4;
+  static constexpr int E = 1 << LOGE;
+  static constexpr int T = H / E;  // lanes per transform
+  static constexpr int TEAMS = kStftThreads / T;
+  static constexpr int NPASS = LOGH == 0 ? 1 : (LOGH + LOGE - 1) / LOGE;
+  static constexpr int PADH = H + (H >> 4);
+  static constexpr int rlog(int p) { return p < NPASS - 1 ? LOGE : LOGH - (NPASS - 1) * LOGE; }
+  static constexpr int ns(int p) {
+    int v = 1;
+    for (int i = 0; i < p; ++i) v <<= rlog(i);
+    return v;
+  }
+  static constexpr int tw_off(int p) {  // pass p >= 1 twiddle table offset
+    int o = 0;
+    for (int i = 1; i < p; ++i) o += ns(i) << rlog(i);
+    return o;
+  }
+  static constexpr int TW = tw_off(NPASS);
+  // shared memory (bytes): win[L] f64 | tws[H] c128 | twp[TW] c128 |
+  // data[TEAMS][PADH] c128 | carry[TEAMS][H] f64 (synthesis)
+  static constexpr size_t OFF_TWS = (size_t)L * 8;
+  static constexpr size_t OFF_TWP = OFF_TWS + (size_t)H * 16;
+  static constexpr size_t OFF_DATA = OFF_TWP + (size_t)TW * 16;
+  static constexpr size_t OFF_CARRY = OFF_DATA + (size_t)TEAMS * PADH * 16;
+  static constexpr size_t SMEM_A = OFF_CARRY;
+  static constexpr size_t SMEM_S = OFF_CARRY + (size_t)TEAMS * H * 8;
+};
+
+FFCA_DEV int pad16(int i) { return i + (i >> 4); }
+
+// x * e^{-2 pi i k / 16} for a compile-time k in [0, 8)
+FFCA_DEV double2 mul_w16(double2 x, int k) {
+  constexpr double c1 = 0.92387953251128674, s1 = 0.38268343236508978, h = 0.70710678118654752;
+  switch (k) {
+    case 0: return x;
+    case 1: return make_double2(c1 * x.x + s1 * x.y, c1 * x.y - s1 * x.x);
+    case 2: return make_double2(h * (x.x + x.y), h * (x.y - x.x));
+    case 3: return make_double2(s1 * x.x + c1 * x.y, s1 * x.y - c1 * x.x);
+    case 4: return make_double2(x.y, -x.x);
+    case 5: return make_double2(-s1 * x.x + c1 * x.y, -s1 * x.y - c1 * x.x);
+    case 6: return make_double2(h * (x.y - x.x), -h * (x.x + x.y));
+    default: return make_double2(-c1 * x.x + s1 * x.y, -c1 * x.y - s1 * x.x);
+  }
+}
+
+constexpr int brev_c(int v, int bits) {
+  int r = 0;
+  for (int i = 0; i < bits; ++i) r |= ((v >> i) & 1) << (bits - 1 - i);
+  return r;
+}
+
+// in-register DFT of R = 2^LR points v[OFF .. OFF+R), natural order in and out
+template <int LR, int OFF, int N>
+FFCA_DEV void dft_reg(double2 (&v)[N]) {
+  constexpr int R = 1 << LR;
+  if constexpr (R > 1) {
+    double2 a[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) a[i] = v[OFF + brev_c(i, LR)];
+#pragma unroll
+    for (int m = 1; m < R; m <<= 1)
+#pragma unroll
+      for (int blk = 0; blk < R; blk += 2 * m)
+#pragma unroll
+        for (int j = 0; j < m; ++j) {
+          const double2 b = mul_w16(a[blk + j + m], j * (8 / m));
+          const double2 x = a[blk + j];
+          a[blk + j] = cadd(x, b);
+          a[blk + j + m] = csub(x, b);
+        }
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[OFF + i] = a[i];
+  }
+}
+
+// Stockham pass P on a lane's registers: v[m*R + r] = in[j_m + r*H/R],
+// j_m = t + m*T; outputs to the team buffer (natural order after the last pass)
+template <int LOGH, int P, int M = 0>
+FFCA_DEV void team_pass_m(double2 (&v)[TeamFft<LOGH>::E], int t, double2* buf,
+                          const double2* twp) {
+  using F = TeamFft<LOGH>;
+  constexpr int LR = F::rlog(P), R = 1 << LR, NS = F::ns(P), MB = F::E / R;
+  if constexpr (M < MB) {
+    const int j = t + M * F::T;
+    const int sidx = j & (NS - 1);
+    if constexpr (P > 0) {
+#pragma unroll
+      for (int r = 1; r < R; ++r)
+        v[M * R + r] = cmul(v[M * R + r], twp[F::tw_off(P) + r * NS + sidx]);
+    }
+    dft_reg<LR, M * R>(v);
+    const int base = (j / NS) * NS * R + sidx;
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[pad16(base + r * NS)] = v[M * R + r];
+    team_pass_m<LOGH, P, M + 1>(v, t, buf, twp);
+  }
+}
+
+template <int LOGH, int P>
+FFCA_DEV void team_load_pass(double2 (&v)[TeamFft<LOGH>::E], int t, const double2* buf) {
+  using F = TeamFft<LOGH>;
+  constexpr int R = 1 << F::rlog(P), MB = F::E / R;
+#pragma unroll
+  for (int m = 0; m < MB; ++m)
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[m * R + r] = buf[pad16(t + m * F::T + r * (F::H / R))];
+}
+
+// passes 1 .. NPASS-1 (pass 0 is issued by the caller from its own loads);
+// every team of the CTA runs in lockstep, so CTA barriers separate passes
+template <int LOGH, int P = 1>
+FFCA_DEV void team_rest(double2 (&v)[TeamFft<LOGH>::E], int t, double2* buf, const double2* twp) {
+  if constexpr (P < TeamFft<LOGH>::NPASS) {
+    __syncthreads();
+    team_load_pass<LOGH, P>(v, t, buf);
+    __syncthreads();
+    team_pass_m<LOGH, P>(v, t, buf, twp);
+    team_rest<LOGH, P + 1>(v, t, buf, twp);
+  }
+}
+
+template <int LOGH>
+FFCA_DEV void team_tables(double* win, double2* tws, double2* twp) {
+  using F = TeamFft<LOGH>;
+  for (int k = threadIdx.x; k < F::H; k += blockDim.x) {
+    double sn, cs;
+    sincospi(-2.0 * (double)k / (double)F::L, &sn, &cs);
+    tws[k] = make_double2(cs, sn);
+  }
+  for (int i = threadIdx.x; i < F::L; i += blockDim.x)
+    win[i] = sqrt(0.5 * (1.0 - cos(2.0 * kPi * (double)i / (double)F::L)));  // stft.py:16-19
+#pragma unroll 1
+  for (int p = 1; p < F::NPASS; ++p) {
+    const int ns = F::ns(p), R = 1 << F::rlog(p);
+    for (int i = threadIdx.x; i < ns * R; i += blockDim.x) {
+      const int r = i / ns, sidx = i - r * ns;
+      double sn, cs;
+      sincospi(-2.0 * (double)(sidx * r) / (double)(ns * R), &sn, &cs);
+      twp[F::tw_off(p) + i] = make_double2(cs, sn);
+    }
+  }
+}
+
+// rounds: channel groups of ncl = min(C, TEAMS) channels (outer), groups of
+// nfr = TEAMS / ncl consecutive frames (inner); team tm -> (frame, channel)
+template <int LOGH>
+__global__ void __launch_bounds__(kStftThreads, 2)
+    stft_team_analyze(const double* __restrict__ x, double2* __restrict__ out, int64_t B, int C,
+                      int64_t len, int64_t N) {
+  using F = TeamFft<LOGH>;
+  extern __shared__ __align__(16) unsigned char sm[];
+  double* win = (double*)sm;
+  double2* tws = (double2*)(sm + F::OFF_TWS);
+  double2* twp = (double2*)(sm + F::OFF_TWP);
+  double2* data = (double2*)(sm + F::OFF_DATA);
+  team_tables<LOGH>(win, tws, twp);
+  __syncthreads();
+  constexpr int H = F::H, NB = H + 1;
+  const int ncl = C < F::TEAMS ? C : F::TEAMS;
+  const int nfr = F::TEAMS / ncl;
+  const int ngroups = (C + ncl - 1) / ncl;
+  const int64_t BN = B * N;
+  const int64_t rpg = (BN + nfr - 1) / nfr;  // rounds per channel group
+  const int64_t total = rpg * ngroups;
+  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(total, r0 + per);
+  const int tm = threadIdx.x / F::T, t = threadIdx.x - tm * F::T;
+  const int fr = tm / ncl, cl = tm - fr * ncl;
+  double2* buf = data + (size_t)tm * F::PADH;
+  for (int64_t rr = r0; rr < r1; ++rr) {
+    const int g = (int)(rr / rpg);
+    const int64_t f0 = (rr - (int64_t)g * rpg) * nfr;
+    const int nf = (int)min((int64_t)nfr, BN - f0);
+    const int c0 = g * ncl;
+    const int nc = min(ncl, C - c0);
+    const bool act = fr < nf && cl < nc;
+    // pass-0 inputs straight from HBM: z_n = w x_2n + i w x_2n+1, n = t + r T
+    double2 v[F::E];
+    {
+      const int64_t fl = f0 + fr;
+      const int64_t b = act ? fl / N : 0, k = act ? fl - b * N : 0;
+      const double* xc = x + ((size_t)b * C + c0 + cl) * len;
+      const int64_t base = (k - 1) * H;
+#pragma unroll
+      for (int r = 0; r < F::E; ++r) {
+        const int n = t + r * F::T;
+        const int64_t i0 = base + 2 * n;
+        double a0 = 0.0, a1 = 0.0;
+        if (act) {
+          if (i0 >= 0 && i0 < len) a0 = xc[i0];
+          if (i0 + 1 >= 0 && i0 + 1 < len) a1 = xc[i0 + 1];
+        }
+        v[r] = make_double2(a0 * win[2 * n], a1 * win[2 * n + 1]);
+      }
+    }
+    team_pass_m<LOGH, 0>(v, t, buf, twp);
+    team_rest<LOGH>(v, t, buf, twp);
+    __syncthreads();
+    // split + store: X_f = E_f + e^{-2 pi i f / L} O_f, contiguous (frame, bin, channel)
+    double2* o = out + (size_t)f0 * NB * C + c0;
+    const int cnt = nf * NB * nc;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const int q = i / (NB * nc);
+      const int rem = i - q * NB * nc;
+      const int f = rem / nc, c = rem - f * nc;
+      const double2* z = data + (size_t)(q * ncl + c) * F::PADH;
+      const double2 zk = z[pad16(f & (H - 1))];
+      const double2 zm = cconj(z[pad16((H - f) & (H - 1))]);
+      const double2 e = cscale(cadd(zk, zm), 0.5);
+      const double2 d = cscale(csub(zk, zm), 0.5);
+      const double2 od = make_double2(d.y, -d.x);
+      const double2 w = f < H ? tws[f] : make_double2(-1.0, 0.0);
+      o[((size_t)q * NB + f) * C + c] = cadd(e, cmul(w, od));
+    }
+    __syncthreads();
+  }
+}
+
+// windowed time sample s of the frame held (as FFT(conj Z)) in team buffer z
+FFCA_DEV double synth_sample(const double2* z, int s, double invH, const double* win) {
+  const double2 y = z[pad16(s >> 1)];
+  return ((s & 1) ? -y.y : y.x) * invH * win[s];
+}
+
+// rounds: channel group (outer), mixture b, hop group [q0, q0 + nh) with
+// nh <= nfr; a round transforms frames q0+1 .. q0+nh and takes frame q0's
+// second half from `carry` (the previous round of this CTA, or a one-frame
+// prologue at the start of a run)
+template <int LOGH>
+__global__ void __launch_bounds__(kStftThreads, 2)
+    stft_team_synth(const double2* __restrict__ spec, double* __restrict__ out, int64_t B, int C,
+                    int64_t N, int64_t len) {
+  using F = TeamFft<LOGH>;
+  extern __shared__ __align__(16) unsigned char sm[];
+  double* win = (double*)sm;
+  double2* tws = (double2*)(sm + F::OFF_TWS);
+  double2* twp = (double2*)(sm + F::OFF_TWP);
+  double2* data = (double2*)(sm + F::OFF_DATA);
+  double* carry = (double*)(sm + F::OFF_CARRY);
+  team_tables<LOGH>(win, tws, twp);
+  __syncthreads();
+  constexpr int H = F::H, NB = H + 1;
+  const double invH = 1.0 / (double)H;
+  const int ncl = C < F::TEAMS ? C : F::TEAMS;
+  const int nfr = F::TEAMS / ncl;
+  const int ngroups = (C + ncl - 1) / ncl;
+  const int64_t Q = (len + H - 1) / H;
+  const int64_t rq = (Q + nfr - 1) / nfr;  // rounds per (group, mixture)
+  const int64_t total = rq * B * ngroups;
+  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(total, r0 + per);
+  const int tm = threadIdx.x / F::T, t = threadIdx.x - tm * F::T;
+  const int fr = tm / ncl, cl = tm - fr * ncl;
+  double2* buf = data + (size_t)tm * F::PADH;
+  int64_t ckey = -1;  // carry holds frame (key % N) second half of (group, b) = key / N
+
+  // inverse transform of frame k (mixture b, channels c0 + cl) into each
+  // active team's buffer; `act` per team
+  auto transform = [&](int64_t b, int64_t k, int c0, bool act) {
+    double2 v[F::E];
+    const double2* s = spec + ((size_t)b * N + k) * NB * C + c0 + cl;
+#pragma unroll
+    for (int r = 0; r < F::E; ++r) {
+      const int n = t + r * F::T;
+      double2 z = make_double2(0.0, 0.0);
+      if (act) {
+        double2 xa = s[(size_t)n * C];
+        double2 xb = s[(size_t)(H - n) * C];
+        if (n == 0) {  // DC and Nyquist real-valued (stft.py:91-92)
+          xa.y = 0.0;
+          xb.y = 0.0;
+        }
+        const double2 xm = cconj(xb);
+        const double2 e = cscale(cadd(xa, xm), 0.5);
+        const double2 d = cscale(csub(xa, xm), 0.5);
+        const double2 od = cmul(d, cconj(tws[n]));
+        z = make_double2(e.x - od.y, -(e.y + od.x));  // conj(Z_n): inverse via forward FFT
+      }
+      v[r] = z;
+    }
+    team_pass_m<LOGH, 0>(v, t, buf, twp);
+    team_rest<LOGH>(v, t, buf, twp);
+    __syncthreads();
+  };
+
+  for (int64_t rr = r0; rr < r1; ++rr) {
+    const int64_t gb = rr / rq;
+    const int g = (int)(gb / B);
+    const int64_t b = gb - (int64_t)g * B;
+    const int64_t q0 = (rr - gb * rq) * nfr;
+    const int nh = (int)min((int64_t)nfr, Q - q0);
+    const int c0 = g * ncl;
+    const int nc = min(ncl, C - c0);
+    const int64_t key = gb * N + q0;
+    if (ckey != key) {  // prologue: frame q0 -> carry
+      transform(b, q0, c0, fr == 0 && cl < nc);
+      for (int i = threadIdx.x; i < nc * H; i += blockDim.x) {
+        const int c = i / H, sx = i - c * H;
+        carry[(size_t)c * H + sx] = synth_sample(data + (size_t)c * F::PADH, H + sx, invH, win);
+      }
+      __syncthreads();
+    }
+    const int nnext = (int)min((int64_t)nh, N - 1 - q0);  // frames q0+1 .. q0+nnext exist
+    transform(b, q0 + 1 + fr, c0, fr < nnext && cl < nc);
+    // hop q0 + i: frame (q0+i) second half + frame (q0+i+1) first half (stft.py:95-99)
+    const int cnt = nc * nh * H;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const int c = i / (nh * H);
+      const int rem = i - c * nh * H;
+      const int h = rem / H, sx = rem - h * H;
+      const int64_t tt = (q0 + h) * H + sx;
+      if (tt >= len) continue;
+      const double a = h == 0 ? carry[(size_t)c * H + sx]
+                              : synth_sample(data + (size_t)((h - 1) * ncl + c) * F::PADH, H + sx,
+                                             invH, win);
+      const double val =
+          h < nnext ? a + synth_sample(data + (size_t)(h * ncl + c) * F::PADH, sx, invH, win) : a;
+      out[((size_t)b * C + c0 + c) * len + tt] = val;
+    }
+    __syncthreads();
+    if (nnext == nh) {  // frame q0 + nh exists: its second half seeds the next round
+      for (int i = threadIdx.x; i < nc * H; i += blockDim.x) {
+        const int c = i / H, sx = i - c * H;
+        carry[(size_t)c * H + sx] =
+            synth_sample(data + (size_t)((nh - 1) * ncl + c) * F::PADH, H + sx, invH, win);
+      }
+      ckey = key + nh;
+    } else {
+      ckey = -1;
+    }
+    __syncthreads();
+  }
+}
+
+template <int LOGH>
+cudaError_t launch_team(const double* x, double2* spec, const double2* spec_in, double* out,
+                        int64_t B, int C, int64_t len, int64_t N, bool synth, cudaStream_t s) {
+  using F = TeamFft<LOGH>;
+  const size_t smem = synth ? F::SMEM_S : F::SMEM_A;
+  const int ncl = C < F::TEAMS ? C : F::TEAMS;
+  const int nfr = F::TEAMS / ncl;
+  const int ngroups = (C + ncl - 1) / ncl;
+  if (synth) {
+    const int64_t Q = (len + F::H - 1) / F::H;
+    const int64_t work = ((Q + nfr - 1) / nfr) * B * ngroups;
+    const int grid = stft_grid(stft_team_synth<LOGH>, smem, work);
+    if (grid < 1) return cudaErrorInvalidValue;
+    stft_team_synth<LOGH><<<grid, kStftThreads, smem, s>>>(spec_in, out, B, C, N, len);
+  } else {
+    const int64_t work = ((B * N + nfr - 1) / nfr) * ngroups;
+    const int grid = stft_grid(stft_team_analyze<LOGH>, smem, work);
+    if (grid < 1) return cudaErrorInvalidValue;
+    stft_team_analyze<LOGH><<<grid, kStftThreads, smem, s>>>(x, spec, B, C, len, N);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t dispatch_team(int logH, const double* x, double2* spec, const double2* spec_in,
+                          double* out, int64_t B, int C, int64_t len, int64_t N, bool synth,
+                          cudaStream_t s) {
+  switch (logH) {
+#define FFCA_TEAM(K) \
+  case K:            \
+    return launch_team<K>(x, spec, spec_in, out, B, C, len, N, synth, s);
+    FFCA_TEAM(0) FFCA_TEAM(1) FFCA_TEAM(2) FFCA_TEAM(3) FFCA_TEAM(4) FFCA_TEAM(5)
+    FFCA_TEAM(6) FFCA_TEAM(7) FFCA_TEAM(8) FFCA_TEAM(9) FFCA_TEAM(10) FFCA_TEAM(11)
+#undef FFCA_TEAM
+    default: return cudaErrorInvalidValue;
+  }
+}
+constexpr int kTeamMaxLogH = 11;
+
 }  // namespace
 
 int64_t stft_frames(int64_t length, int frame_shift) {
@@ -284,6 +673,8 @@ cudaError_t launch_stft_analyze(const double* x, double2* spec, int64_t B, int C
   const int logL = log2_exact(L);
   if (logL < 0 || B < 1 || C < 1 || len < 1) return cudaErrorInvalidValue;
   const int64_t N = stft_frames(len, L / 2);
+  if (logL - 1 <= kTeamMaxLogH)
+    return dispatch_team(logL - 1, x, spec, nullptr, nullptr, B, C, len, N, false, s);
   size_t smem = 0;
   const int cg = stft_group(L, C, false, &smem);
   const int grid = stft_grid(stft_analyze_kernel, smem, B * N);
@@ -297,6 +688,8 @@ cudaError_t launch_stft_synthesize(const double2* spec, double* out, int64_t B, 
   const int logL = log2_exact(L);
   if (logL < 0 || B < 1 || C < 1 || N < 1 || len < 1 || len > N * (L / 2))
     return cudaErrorInvalidValue;
+  if (logL - 1 <= kTeamMaxLogH)
+    return dispatch_team(logL - 1, nullptr, nullptr, spec, out, B, C, len, N, true, s);
   size_t smem = 0;
   const int cg = stft_group(L, C, true, &smem);
   const int64_t Q = (len + L / 2 - 1) / (L / 2);
