@@ -25,6 +25,10 @@ namespace {
 
 constexpr int kStftThreads = 256;
 constexpr int kStftMaxLength = 8192;
+#ifndef FFCA_TEAM_THREADS
+#define FFCA_TEAM_THREADS 128
+#endif
+constexpr int kTeamThreads = FFCA_TEAM_THREADS;  // team kernels: small CTAs, several per SM
 constexpr double kPi = 3.141592653589793;  // np.pi
 
 struct StftSmem {
@@ -257,7 +261,7 @@ int stft_group(int L, int C, bool synth, size_t* bytes) {
 }
 
 template <typename K>
-int stft_grid(K kern, size_t smem, int64_t work) {
+int stft_grid(K kern, size_t smem, int64_t work, int threads = kStftThreads) {
   static int dev_max = -1;
   if (dev_max < 0) {
     int dev = 0, v = 0;
@@ -268,7 +272,7 @@ int stft_grid(K kern, size_t smem, int64_t work) {
   if ((int)smem > dev_max) return -1;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStftThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t cap = (int64_t)sm_count() * per_sm;
   return (int)(work < cap ? work : cap);
@@ -292,7 +296,9 @@ struct TeamFft {
   static constexpr int LOGE = LOGH < 4 ? LOGH : 4;
   static constexpr int E = 1 << LOGE;
   static constexpr int T = H / E;  // lanes per transform
-  static constexpr int TEAMS = kStftThreads / T;
+  static constexpr int THREADS = 2 * T > kTeamThreads ? 2 * T : kTeamThreads;
+  static constexpr int TEAMS = THREADS / T;
+  static constexpr int MINB = 512 / THREADS;
   static constexpr int NPASS = LOGH == 0 ? 1 : (LOGH + LOGE - 1) / LOGE;
   static constexpr int PADH = H + (H >> 4);
   static constexpr int rlog(int p) { return p < NPASS - 1 ? LOGE : LOGH - (NPASS - 1) * LOGE; }
@@ -308,12 +314,15 @@ struct TeamFft {
   }
   static constexpr int TW = tw_off(NPASS);
   // shared memory (bytes): win[L] f64 | tws[H] c128 | twp[TW] c128 |
-  // data[TEAMS][PADH] c128 | carry[TEAMS][H] f64 (synthesis)
+  // data[TEAMS][PADH] c128 | analysis: stage[E][THREADS] c128 (next round's
+  // samples, lane-private) | synthesis: carry[TEAMS][H] f64
   static constexpr size_t OFF_TWS = (size_t)L * 8;
   static constexpr size_t OFF_TWP = OFF_TWS + (size_t)H * 16;
   static constexpr size_t OFF_DATA = OFF_TWP + (size_t)TW * 16;
   static constexpr size_t OFF_CARRY = OFF_DATA + (size_t)TEAMS * PADH * 16;
-  static constexpr size_t SMEM_A = OFF_CARRY;
+  static constexpr size_t STAGE_B = (size_t)E * THREADS * 16;
+  static constexpr bool STAGED = OFF_CARRY + STAGE_B <= 200 * 1024;  // else direct loads
+  static constexpr size_t SMEM_A = OFF_CARRY + (STAGED ? STAGE_B : 0);
   static constexpr size_t SMEM_S = OFF_CARRY + (size_t)TEAMS * H * 8;
 };
 
@@ -435,7 +444,7 @@ FFCA_DEV void team_tables(double* win, double2* tws, double2* twp) {
 // rounds: channel groups of ncl = min(C, TEAMS) channels (outer), groups of
 // nfr = TEAMS / ncl consecutive frames (inner); team tm -> (frame, channel)
 template <int LOGH>
-__global__ void __launch_bounds__(kStftThreads, 2)
+__global__ void __launch_bounds__(TeamFft<LOGH>::THREADS, TeamFft<LOGH>::MINB)
     stft_team_analyze(const double* __restrict__ x, double2* __restrict__ out, int64_t B, int C,
                       int64_t len, int64_t N) {
   using F = TeamFft<LOGH>;
@@ -458,42 +467,101 @@ __global__ void __launch_bounds__(kStftThreads, 2)
   const int tm = threadIdx.x / F::T, t = threadIdx.x - tm * F::T;
   const int fr = tm / ncl, cl = tm - fr * ncl;
   double2* buf = data + (size_t)tm * F::PADH;
+  double2* stage = (double2*)(sm + F::OFF_CARRY);  // [E][THREADS], lane-private slots
+  const bool vec = (len & 1) == 0;  // rows 16-B aligned: pairs never straddle an edge
+
+  // cp.async the samples of round rr for this lane (pairs n = t + r T), zero
+  // fill outside [0, len) (the half-frame / tail padding, stft.py:56-59)
+  auto issue = [&](int64_t rr) {
+    if constexpr (!F::STAGED) return;
+    const int g = (int)(rr / rpg);
+    const int64_t f0 = (rr - (int64_t)g * rpg) * nfr;
+    const int nf = (int)min((int64_t)nfr, BN - f0);
+    const int c0 = g * ncl;
+    const bool act = fr < nf && cl < min(ncl, C - c0);
+    const int64_t fl = f0 + fr;
+    const int64_t b = act ? fl / N : 0, k = act ? fl - b * N : 0;
+    const double* xc = x + ((size_t)b * C + (act ? c0 + cl : 0)) * len;
+    const int64_t base = (k - 1) * H;
+#pragma unroll
+    for (int r = 0; r < F::E; ++r) {
+      const int64_t i0 = base + 2 * (t + r * F::T);
+      double2* dst = stage + r * F::THREADS + threadIdx.x;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+      if (vec) {
+        const bool ok = act && i0 >= 0 && i0 < len;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa),
+                     "l"(ok ? xc + i0 : x), "r"(ok ? 16 : 0));
+      } else {
+        const bool ok0 = act && i0 >= 0 && i0 < len;
+        const bool ok1 = act && i0 + 1 >= 0 && i0 + 1 < len;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa),
+                     "l"(ok0 ? xc + i0 : x), "r"(ok0 ? 8 : 0));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa + 8),
+                     "l"(ok1 ? xc + i0 + 1 : x), "r"(ok1 ? 8 : 0));
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+
+  if (r0 < r1) issue(r0);
   for (int64_t rr = r0; rr < r1; ++rr) {
     const int g = (int)(rr / rpg);
     const int64_t f0 = (rr - (int64_t)g * rpg) * nfr;
     const int nf = (int)min((int64_t)nfr, BN - f0);
     const int c0 = g * ncl;
     const int nc = min(ncl, C - c0);
-    const bool act = fr < nf && cl < nc;
-    // pass-0 inputs straight from HBM: z_n = w x_2n + i w x_2n+1, n = t + r T
     double2 v[F::E];
-    {
+    if constexpr (F::STAGED) {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+#pragma unroll
+      for (int r = 0; r < F::E; ++r) {
+        const int n = t + r * F::T;
+        const double2 a = stage[r * F::THREADS + threadIdx.x];
+        v[r] = make_double2(a.x * win[2 * n], a.y * win[2 * n + 1]);
+      }
+    } else {
+      const bool act = fr < nf && cl < nc;
       const int64_t fl = f0 + fr;
       const int64_t b = act ? fl / N : 0, k = act ? fl - b * N : 0;
-      const double* xc = x + ((size_t)b * C + c0 + cl) * len;
+      const double* xc = x + ((size_t)b * C + (act ? c0 + cl : 0)) * len;
       const int64_t base = (k - 1) * H;
+      const bool inner = act && base >= 0 && base + F::L <= len;
 #pragma unroll
       for (int r = 0; r < F::E; ++r) {
         const int n = t + r * F::T;
         const int64_t i0 = base + 2 * n;
         double a0 = 0.0, a1 = 0.0;
-        if (act) {
+        if (inner) {
+          a0 = xc[i0];
+          a1 = xc[i0 + 1];
+        } else if (act) {
           if (i0 >= 0 && i0 < len) a0 = xc[i0];
           if (i0 + 1 >= 0 && i0 + 1 < len) a1 = xc[i0 + 1];
         }
         v[r] = make_double2(a0 * win[2 * n], a1 * win[2 * n + 1]);
       }
     }
+    if (rr + 1 < r1) issue(rr + 1);  // overlaps this round's passes and stores
     team_pass_m<LOGH, 0>(v, t, buf, twp);
     team_rest<LOGH>(v, t, buf, twp);
     __syncthreads();
     // split + store: X_f = E_f + e^{-2 pi i f / L} O_f, contiguous (frame, bin, channel)
     double2* o = out + (size_t)f0 * NB * C + c0;
     const int cnt = nf * NB * nc;
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-      const int q = i / (NB * nc);
-      const int rem = i - q * NB * nc;
-      const int f = rem / nc, c = rem - f * nc;
+    // (q, f, c) walk of the round's output with carries instead of divisions
+    int q = 0, f = 0, c = threadIdx.x;
+    {
+      const int per = NB * nc;
+      q = c / per;
+      c -= q * per;
+      f = c / nc;
+      c -= f * nc;
+    }
+    const int sq = F::THREADS / (NB * nc);
+    int sr = F::THREADS - sq * NB * nc;
+    const int sf = sr / nc, sc = sr - (sr / nc) * nc;
+    for (int i = threadIdx.x; i < cnt; i += F::THREADS) {
       const double2* z = data + (size_t)(q * ncl + c) * F::PADH;
       const double2 zk = z[pad16(f & (H - 1))];
       const double2 zm = cconj(z[pad16((H - f) & (H - 1))]);
@@ -502,9 +570,21 @@ __global__ void __launch_bounds__(kStftThreads, 2)
       const double2 od = make_double2(d.y, -d.x);
       const double2 w = f < H ? tws[f] : make_double2(-1.0, 0.0);
       o[((size_t)q * NB + f) * C + c] = cadd(e, cmul(w, od));
+      c += sc;
+      f += sf;
+      q += sq;
+      if (c >= nc) {
+        c -= nc;
+        ++f;
+      }
+      if (f >= NB) {
+        f -= NB;
+        ++q;
+      }
     }
     __syncthreads();
   }
+  asm volatile("cp.async.wait_all;\n" ::);
 }
 
 // windowed time sample s of the frame held (as FFT(conj Z)) in team buffer z
@@ -518,7 +598,7 @@ FFCA_DEV double synth_sample(const double2* z, int s, double invH, const double*
 // second half from `carry` (the previous round of this CTA, or a one-frame
 // prologue at the start of a run)
 template <int LOGH>
-__global__ void __launch_bounds__(kStftThreads, 2)
+__global__ void __launch_bounds__(TeamFft<LOGH>::THREADS, TeamFft<LOGH>::MINB)
     stft_team_synth(const double2* __restrict__ spec, double* __restrict__ out, int64_t B, int C,
                     int64_t N, int64_t len) {
   using F = TeamFft<LOGH>;
@@ -634,14 +714,14 @@ cudaError_t launch_team(const double* x, double2* spec, const double2* spec_in, 
   if (synth) {
     const int64_t Q = (len + F::H - 1) / F::H;
     const int64_t work = ((Q + nfr - 1) / nfr) * B * ngroups;
-    const int grid = stft_grid(stft_team_synth<LOGH>, smem, work);
+    const int grid = stft_grid(stft_team_synth<LOGH>, smem, work, F::THREADS);
     if (grid < 1) return cudaErrorInvalidValue;
-    stft_team_synth<LOGH><<<grid, kStftThreads, smem, s>>>(spec_in, out, B, C, N, len);
+    stft_team_synth<LOGH><<<grid, F::THREADS, smem, s>>>(spec_in, out, B, C, N, len);
   } else {
     const int64_t work = ((B * N + nfr - 1) / nfr) * ngroups;
-    const int grid = stft_grid(stft_team_analyze<LOGH>, smem, work);
+    const int grid = stft_grid(stft_team_analyze<LOGH>, smem, work, F::THREADS);
     if (grid < 1) return cudaErrorInvalidValue;
-    stft_team_analyze<LOGH><<<grid, kStftThreads, smem, s>>>(x, spec, B, C, len, N);
+    stft_team_analyze<LOGH><<<grid, F::THREADS, smem, s>>>(x, spec, B, C, len, N);
   }
   return cudaGetLastError();
 }
