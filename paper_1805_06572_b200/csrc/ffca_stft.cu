@@ -300,7 +300,9 @@ struct TeamFft {
   static constexpr int TEAMS = THREADS / T;
   static constexpr int MINB = 512 / THREADS;
   static constexpr int NPASS = LOGH == 0 ? 1 : (LOGH + LOGE - 1) / LOGE;
-  static constexpr int PADH = H + (H >> 4);
+  // team buffer stride: padded length rounded to an odd number of 16-B
+  // units, so equal offsets in different teams fall in different banks
+  static constexpr int PADH = (H + (H >> 4)) | 1;
   static constexpr int rlog(int p) { return p < NPASS - 1 ? LOGE : LOGH - (NPASS - 1) * LOGE; }
   static constexpr int ns(int p) {
     int v = 1;
@@ -323,7 +325,10 @@ struct TeamFft {
   static constexpr size_t STAGE_B = (size_t)E * THREADS * 16;
   static constexpr bool STAGED = OFF_CARRY + STAGE_B <= 200 * 1024;  // else direct loads
   static constexpr size_t SMEM_A = OFF_CARRY + (STAGED ? STAGE_B : 0);
-  static constexpr size_t SMEM_S = OFF_CARRY + (size_t)TEAMS * H * 8;
+  static constexpr int NBP = (H + 1) | 1;  // staged spectrum row (odd # of 16-B units)
+  static constexpr size_t OFF_SSTAGE = OFF_CARRY + (size_t)TEAMS * H * 8;
+  static constexpr bool SSTAGED = OFF_SSTAGE + (size_t)TEAMS * NBP * 16 <= 200 * 1024;
+  static constexpr size_t SMEM_S = OFF_SSTAGE + (SSTAGED ? (size_t)TEAMS * NBP * 16 : 0);
 };
 
 FFCA_DEV int pad16(int i) { return i + (i >> 4); }
@@ -596,7 +601,9 @@ FFCA_DEV double synth_sample(const double2* z, int s, double invH, const double*
 // rounds: channel group (outer), mixture b, hop group [q0, q0 + nh) with
 // nh <= nfr; a round transforms frames q0+1 .. q0+nh and takes frame q0's
 // second half from `carry` (the previous round of this CTA, or a one-frame
-// prologue at the start of a run)
+// prologue at the start of a run). The spectra of the next round's frames are
+// cp.async-copied (coalesced, one 16-B bin per copy) into a transposed
+// [team][bin] stage while the current round computes.
 template <int LOGH>
 __global__ void __launch_bounds__(TeamFft<LOGH>::THREADS, TeamFft<LOGH>::MINB)
     stft_team_synth(const double2* __restrict__ spec, double* __restrict__ out, int64_t B, int C,
@@ -608,6 +615,7 @@ __global__ void __launch_bounds__(TeamFft<LOGH>::THREADS, TeamFft<LOGH>::MINB)
   double2* twp = (double2*)(sm + F::OFF_TWP);
   double2* data = (double2*)(sm + F::OFF_DATA);
   double* carry = (double*)(sm + F::OFF_CARRY);
+  double2* stage = (double2*)(sm + F::OFF_SSTAGE);
   team_tables<LOGH>(win, tws, twp);
   __syncthreads();
   constexpr int H = F::H, NB = H + 1;
@@ -625,82 +633,162 @@ __global__ void __launch_bounds__(TeamFft<LOGH>::THREADS, TeamFft<LOGH>::MINB)
   double2* buf = data + (size_t)tm * F::PADH;
   int64_t ckey = -1;  // carry holds frame (key % N) second half of (group, b) = key / N
 
-  // inverse transform of frame k (mixture b, channels c0 + cl) into each
-  // active team's buffer; `act` per team
-  auto transform = [&](int64_t b, int64_t k, int c0, bool act) {
+  struct Round {
+    int64_t b, q0;
+    int g, c0, nc, nh, nnext;
+  };
+  auto round_of = [&](int64_t rr) {
+    Round R;
+    const int64_t gb = rr / rq;
+    R.g = (int)(gb / B);
+    R.b = gb - (int64_t)R.g * B;
+    R.q0 = (rr - gb * rq) * nfr;
+    R.nh = (int)min((int64_t)nfr, Q - R.q0);
+    R.c0 = R.g * ncl;
+    R.nc = min(ncl, C - R.c0);
+    R.nnext = (int)min((int64_t)R.nh, N - 1 - R.q0);  // frames q0+1 .. q0+nnext exist
+    return R;
+  };
+  // stage the spectra of frames q0+1 .. q0+nnext (channels c0 .. c0+nc)
+  auto issue = [&](const Round& R) {
+    if constexpr (F::SSTAGED) {
+      const int per_f = NB * R.nc;
+      const int cnt = R.nnext * per_f;
+      const double2* src = spec + ((size_t)R.b * N + R.q0 + 1) * NB * C + R.c0;
+      for (int i = threadIdx.x; i < cnt; i += F::THREADS) {
+        const int q = i / per_f;
+        const int rem = i - q * per_f;
+        const int f = rem / R.nc, c = rem - f * R.nc;
+        const unsigned sa =
+            (unsigned)__cvta_generic_to_shared(stage + (size_t)(q * ncl + c) * F::NBP + f);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                     "l"(src + ((size_t)q * NB + f) * C + c));
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+
+  // conj(Z_n) from X_n, X_{H-n} (DC / Nyquist real-valued, stft.py:91-92);
+  // the inverse FFT is the forward FFT of conj(Z)
+  auto zconj = [&](double2 xa, double2 xb, int n) {
+    if (n == 0) {
+      xa.y = 0.0;
+      xb.y = 0.0;
+    }
+    const double2 xm = cconj(xb);
+    const double2 e = cscale(cadd(xa, xm), 0.5);
+    const double2 d = cscale(csub(xa, xm), 0.5);
+    const double2 od = cmul(d, cconj(tws[n]));
+    return make_double2(e.x - od.y, -(e.y + od.x));
+  };
+
+  // prologue transform of frame k straight from HBM (team fr == 0 only)
+  auto transform_direct = [&](int64_t b, int64_t k, int c0, bool act) {
     double2 v[F::E];
-    const double2* s = spec + ((size_t)b * N + k) * NB * C + c0 + cl;
+    const double2* sp = spec + ((size_t)b * N + k) * NB * C + c0 + cl;
 #pragma unroll
     for (int r = 0; r < F::E; ++r) {
       const int n = t + r * F::T;
-      double2 z = make_double2(0.0, 0.0);
-      if (act) {
-        double2 xa = s[(size_t)n * C];
-        double2 xb = s[(size_t)(H - n) * C];
-        if (n == 0) {  // DC and Nyquist real-valued (stft.py:91-92)
-          xa.y = 0.0;
-          xb.y = 0.0;
-        }
-        const double2 xm = cconj(xb);
-        const double2 e = cscale(cadd(xa, xm), 0.5);
-        const double2 d = cscale(csub(xa, xm), 0.5);
-        const double2 od = cmul(d, cconj(tws[n]));
-        z = make_double2(e.x - od.y, -(e.y + od.x));  // conj(Z_n): inverse via forward FFT
-      }
-      v[r] = z;
+      v[r] = act ? zconj(sp[(size_t)n * C], sp[(size_t)(H - n) * C], n) : make_double2(0.0, 0.0);
     }
     team_pass_m<LOGH, 0>(v, t, buf, twp);
     team_rest<LOGH>(v, t, buf, twp);
     __syncthreads();
   };
 
+  if (r0 < r1) {
+    const Round R = round_of(r0);
+    issue(R);
+  }
   for (int64_t rr = r0; rr < r1; ++rr) {
-    const int64_t gb = rr / rq;
-    const int g = (int)(gb / B);
-    const int64_t b = gb - (int64_t)g * B;
-    const int64_t q0 = (rr - gb * rq) * nfr;
-    const int nh = (int)min((int64_t)nfr, Q - q0);
-    const int c0 = g * ncl;
-    const int nc = min(ncl, C - c0);
-    const int64_t key = gb * N + q0;
+    const Round R = round_of(rr);
+    const int64_t key = (rr / rq) * N + R.q0;
     if (ckey != key) {  // prologue: frame q0 -> carry
-      transform(b, q0, c0, fr == 0 && cl < nc);
-      for (int i = threadIdx.x; i < nc * H; i += blockDim.x) {
+      transform_direct(R.b, R.q0, R.c0, fr == 0 && cl < R.nc);
+      for (int i = threadIdx.x; i < R.nc * H; i += F::THREADS) {
         const int c = i / H, sx = i - c * H;
         carry[(size_t)c * H + sx] = synth_sample(data + (size_t)c * F::PADH, H + sx, invH, win);
       }
       __syncthreads();
     }
-    const int nnext = (int)min((int64_t)nh, N - 1 - q0);  // frames q0+1 .. q0+nnext exist
-    transform(b, q0 + 1 + fr, c0, fr < nnext && cl < nc);
-    // hop q0 + i: frame (q0+i) second half + frame (q0+i+1) first half (stft.py:95-99)
-    const int cnt = nc * nh * H;
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-      const int c = i / (nh * H);
-      const int rem = i - c * nh * H;
-      const int h = rem / H, sx = rem - h * H;
-      const int64_t tt = (q0 + h) * H + sx;
-      if (tt >= len) continue;
-      const double a = h == 0 ? carry[(size_t)c * H + sx]
-                              : synth_sample(data + (size_t)((h - 1) * ncl + c) * F::PADH, H + sx,
-                                             invH, win);
-      const double val =
-          h < nnext ? a + synth_sample(data + (size_t)(h * ncl + c) * F::PADH, sx, invH, win) : a;
-      out[((size_t)b * C + c0 + c) * len + tt] = val;
+    // frames q0+1 .. q0+nnext
+    {
+      const bool act = fr < R.nnext && cl < R.nc;
+      double2 v[F::E];
+      if constexpr (F::SSTAGED) {
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncthreads();  // every lane's copies landed
+        const double2* st = stage + (size_t)tm * F::NBP;
+#pragma unroll
+        for (int r = 0; r < F::E; ++r) {
+          const int n = t + r * F::T;
+          v[r] = act ? zconj(st[n], st[H - n], n) : make_double2(0.0, 0.0);
+        }
+      } else {
+        const double2* sp = spec + ((size_t)R.b * N + R.q0 + 1 + fr) * NB * C + R.c0 + cl;
+#pragma unroll
+        for (int r = 0; r < F::E; ++r) {
+          const int n = t + r * F::T;
+          v[r] = act ? zconj(sp[(size_t)n * C], sp[(size_t)(H - n) * C], n)
+                     : make_double2(0.0, 0.0);
+        }
+      }
+      team_pass_m<LOGH, 0>(v, t, buf, twp);
+      __syncthreads();  // stage fully consumed: prefetch the next round
+      if (rr + 1 < r1) issue(round_of(rr + 1));
+      team_rest<LOGH>(v, t, buf, twp);
+      __syncthreads();
+    }
+    // hop q0 + h: frame (q0+h) second half + frame (q0+h+1) first half
+    // (stft.py:95-99 order); walk (c, h, sx) with carries, no divisions
+    {
+      const int nhH = R.nh * H;
+      const int cnt = R.nc * nhH;
+      int c = threadIdx.x / nhH;
+      int rem = threadIdx.x - c * nhH;
+      int h = rem >> LOGH, sx = rem & (H - 1);
+      const int sc = F::THREADS / nhH;
+      const int srem = F::THREADS - sc * nhH;
+      const int sh = srem >> LOGH, ss = srem & (H - 1);
+      for (int i = threadIdx.x; i < cnt; i += F::THREADS) {
+        const int64_t tt = (R.q0 + h) * H + sx;
+        if (tt < len) {
+          const double a = h == 0 ? carry[(size_t)c * H + sx]
+                                  : synth_sample(data + (size_t)((h - 1) * ncl + c) * F::PADH,
+                                                 H + sx, invH, win);
+          const double val =
+              h < R.nnext
+                  ? a + synth_sample(data + (size_t)(h * ncl + c) * F::PADH, sx, invH, win)
+                  : a;
+          out[((size_t)R.b * C + R.c0 + c) * len + tt] = val;
+        }
+        sx += ss;
+        h += sh;
+        c += sc;
+        if (sx >= H) {
+          sx -= H;
+          ++h;
+        }
+        if (h >= R.nh) {
+          h -= R.nh;
+          ++c;
+        }
+      }
     }
     __syncthreads();
-    if (nnext == nh) {  // frame q0 + nh exists: its second half seeds the next round
-      for (int i = threadIdx.x; i < nc * H; i += blockDim.x) {
-        const int c = i / H, sx = i - c * H;
+    if (R.nnext == R.nh) {  // frame q0 + nh exists: its second half seeds the next round
+      for (int i = threadIdx.x; i < R.nc * H; i += F::THREADS) {
+        const int c = i >> LOGH, sx = i & (H - 1);
         carry[(size_t)c * H + sx] =
-            synth_sample(data + (size_t)((nh - 1) * ncl + c) * F::PADH, H + sx, invH, win);
+            synth_sample(data + (size_t)((R.nh - 1) * ncl + c) * F::PADH, H + sx, invH, win);
       }
-      ckey = key + nh;
+      ckey = key + R.nh;
     } else {
       ckey = -1;
     }
     __syncthreads();
   }
+  asm volatile("cp.async.wait_all;\n" ::);
 }
 
 template <int LOGH>

@@ -22,16 +22,20 @@ import torch  # noqa: E402
 from paper_1805_06572_b200.stft import num_frames, stft_analyze_device, stft_synthesize_device  # noqa: E402
 
 
-def timed(fn, reps):
-    fn()
+def timed(fn, reps, windows=3):
+    """Best of `windows` CUDA-event windows of `reps` calls each (after warm-up)."""
+    out = fn()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        out = fn()
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps, out
+    best = float("inf")
+    for _ in range(windows):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            out = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) / reps)
+    return best, out
 
 
 def main():
