@@ -655,14 +655,29 @@ __global__ void __launch_bounds__(TeamFft<LOGH>::THREADS, TeamFft<LOGH>::MINB)
       const int per_f = NB * R.nc;
       const int cnt = R.nnext * per_f;
       const double2* src = spec + ((size_t)R.b * N + R.q0 + 1) * NB * C + R.c0;
+      // (q, f, c) walk with carries: source reads stay contiguous per frame
+      int q = threadIdx.x / per_f;
+      int rem = threadIdx.x - q * per_f;
+      int f = rem / R.nc, c = rem - f * R.nc;
+      const int sq = F::THREADS / per_f;
+      const int sr = F::THREADS - sq * per_f;
+      const int sf = sr / R.nc, sc = sr - sf * R.nc;
       for (int i = threadIdx.x; i < cnt; i += F::THREADS) {
-        const int q = i / per_f;
-        const int rem = i - q * per_f;
-        const int f = rem / R.nc, c = rem - f * R.nc;
         const unsigned sa =
             (unsigned)__cvta_generic_to_shared(stage + (size_t)(q * ncl + c) * F::NBP + f);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
                      "l"(src + ((size_t)q * NB + f) * C + c));
+        c += sc;
+        f += sf;
+        q += sq;
+        if (c >= R.nc) {
+          c -= R.nc;
+          ++f;
+        }
+        if (f >= NB) {
+          f -= NB;
+          ++q;
+        }
       }
     }
     asm volatile("cp.async.commit_group;\n" ::);
@@ -740,33 +755,59 @@ __global__ void __launch_bounds__(TeamFft<LOGH>::THREADS, TeamFft<LOGH>::MINB)
       __syncthreads();
     }
     // hop q0 + h: frame (q0+h) second half + frame (q0+h+1) first half
-    // (stft.py:95-99 order); walk (c, h, sx) with carries, no divisions
+    // (stft.py:95-99 order). Each thread emits a pair of samples (one 16-B
+    // shared load per frame); walk (c, h, pair) with carries, no divisions.
     {
-      const int nhH = R.nh * H;
-      const int cnt = R.nc * nhH;
-      int c = threadIdx.x / nhH;
-      int rem = threadIdx.x - c * nhH;
-      int h = rem >> LOGH, sx = rem & (H - 1);
-      const int sc = F::THREADS / nhH;
-      const int srem = F::THREADS - sc * nhH;
-      const int sh = srem >> LOGH, ss = srem & (H - 1);
+      constexpr int HP = H / 2 > 0 ? H / 2 : 1;  // sample pairs per hop (H = 1: one single)
+      const int nhP = R.nh * HP;
+      const int cnt = R.nc * nhP;
+      int c = threadIdx.x / nhP;
+      int rem = threadIdx.x - c * nhP;
+      int h = rem / HP, px = rem - h * HP;
+      const int sc = F::THREADS / nhP;
+      const int srem = F::THREADS - sc * nhP;
+      const int sh = srem / HP, sp = srem - sh * HP;
+      const bool vec2 = (H >= 2) && ((len & 1) == 0);
       for (int i = threadIdx.x; i < cnt; i += F::THREADS) {
+        const int sx = 2 * px;
         const int64_t tt = (R.q0 + h) * H + sx;
-        if (tt < len) {
-          const double a = h == 0 ? carry[(size_t)c * H + sx]
-                                  : synth_sample(data + (size_t)((h - 1) * ncl + c) * F::PADH,
-                                                 H + sx, invH, win);
-          const double val =
-              h < R.nnext
-                  ? a + synth_sample(data + (size_t)(h * ncl + c) * F::PADH, sx, invH, win)
-                  : a;
-          out[((size_t)R.b * C + R.c0 + c) * len + tt] = val;
+        double* dst = out + ((size_t)R.b * C + R.c0 + c) * len + tt;
+        if (H == 1) {
+          if (tt < len) {
+            const double a = h == 0 ? carry[c]
+                                    : synth_sample(data + (size_t)((h - 1) * ncl + c) * F::PADH,
+                                                   1, invH, win);
+            *dst = h < R.nnext
+                       ? a + synth_sample(data + (size_t)(h * ncl + c) * F::PADH, 0, invH, win)
+                       : a;
+          }
+        } else if (tt < len) {
+          double a0, a1;
+          if (h == 0) {
+            a0 = carry[(size_t)c * H + sx];
+            a1 = carry[(size_t)c * H + sx + 1];
+          } else {  // second half of frame q0+h: pair index (H + sx) / 2
+            const double2 y = data[(size_t)((h - 1) * ncl + c) * F::PADH + pad16((H + sx) >> 1)];
+            a0 = y.x * invH * win[H + sx];
+            a1 = -y.y * invH * win[H + sx + 1];
+          }
+          if (h < R.nnext) {
+            const double2 y = data[(size_t)(h * ncl + c) * F::PADH + pad16(sx >> 1)];
+            a0 = a0 + y.x * invH * win[sx];
+            a1 = a1 + -y.y * invH * win[sx + 1];
+          }
+          if (vec2 && tt + 1 < len) {
+            *(double2*)dst = make_double2(a0, a1);
+          } else {
+            dst[0] = a0;
+            if (tt + 1 < len) dst[1] = a1;
+          }
         }
-        sx += ss;
+        px += sp;
         h += sh;
         c += sc;
-        if (sx >= H) {
-          sx -= H;
+        if (px >= HP) {
+          px -= HP;
           ++h;
         }
         if (h >= R.nh) {
