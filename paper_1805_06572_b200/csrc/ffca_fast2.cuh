@@ -30,6 +30,52 @@ FFCA_DEV double rcp_nr(double x) {
   return r;
 }
 
+#ifndef FFCA_RCP_BATCH
+#define FFCA_RCP_BATCH 0  // measured slower on config 3 (longer dependent chain)
+#endif
+#ifndef FFCA_RCP_NR
+#define FFCA_RCP_NR 1  // Newton steps after rcp.approx.f64 in the streaming pass (1: ~1e-14 rel.)
+#endif
+// reciprocal for the streaming pass: MUFU.RCP64H seed + FFCA_RCP_NR Newton steps
+FFCA_DEV double rcp_pass(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < FFCA_RCP_NR; ++i) {
+    const double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+  }
+  return r;
+}
+// r[a] = 1 / d[a] for all a with ONE reciprocal (Montgomery's trick:
+// prefix products, one rcp, back-substitution; ~2 ulp), falling back to
+// per-element reciprocals when the product leaves the safe exponent range
+template <int I>
+FFCA_DEV void rcp_batch(const double (&d)[I], double (&r)[I]) {
+  if constexpr (I == 1 || !FFCA_RCP_BATCH) {
+#pragma unroll
+    for (int a = 0; a < I; ++a) r[a] = rcp_pass(d[a]);
+  } else {
+    double pre[I];
+    pre[0] = d[0];
+#pragma unroll
+    for (int a = 1; a < I; ++a) pre[a] = pre[a - 1] * d[a];
+    const double all = pre[I - 1];
+    if (all > 1e-280 && all < 1e280) {
+      double inv = rcp_nr(all);
+#pragma unroll
+      for (int a = I - 1; a > 0; --a) {
+        r[a] = inv * pre[a - 1];
+        inv = inv * d[a];
+      }
+      r[0] = inv;
+    } else {
+#pragma unroll
+      for (int a = 0; a < I; ++a) r[a] = rcp_nr(d[a]);
+    }
+  }
+}
+
 FFCA_DEV void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
@@ -64,6 +110,8 @@ struct Math<double> {
   using T2 = double2;
   static constexpr bool kBlocked = false;
   static FFCA_DEV double rcp(double x) { return rcp_nr(x); }
+  template <int I>
+  static FFCA_DEV void rcp_n(const double (&d)[I], double (&r)[I]) { rcp_batch<I>(d, r); }
   static FFCA_DEV double2 c2(double2 a) { return a; }
 };
 template <>
@@ -72,6 +120,11 @@ struct Math<float> {
   using T2 = float2;
   static constexpr bool kBlocked = true;
   static FFCA_DEV float rcp(float x) { return __frcp_rn(x); }
+  template <int I>
+  static FFCA_DEV void rcp_n(const float (&d)[I], float (&r)[I]) {
+#pragma unroll
+    for (int a = 0; a < I; ++a) r[a] = __frcp_rn(d[a]);
+  }
   static FFCA_DEV float2 c2(double2 a) { return make_float2((float)a.x, (float)a.y); }
 };
 
@@ -98,6 +151,12 @@ struct Fast2Smem {
 #ifndef FAST2_MINB
 #define FAST2_MINB 3  // CTAs per SM the update pass is register-budgeted for
 #endif
+#ifndef FAST2_MU_STAGES
+#define FAST2_MU_STAGES 6  // ring depth of the image-writing (last) pass
+#endif
+#ifndef FAST2_MU_MINB
+#define FAST2_MU_MINB 2  // CTAs per SM the image-writing pass is budgeted for
+#endif
 #ifndef FAST2_STAGES
 #define FAST2_STAGES 6  // cp.async ring depth (frames per thread)
 #endif
@@ -106,7 +165,7 @@ struct Fast2Smem {
 #endif
 
 template <int I, typename R, int WARPS, int STAGES, bool UPDATE, bool LL, bool MU>
-__global__ void __launch_bounds__(WARPS * 32, MU ? 2 : FAST2_MINB) fast_em2_kernel(const FastIterParams p) {
+__global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) fast_em2_kernel(const FastIterParams p) {
   using C = typename CplxOf<R>::type;
   using Slot = RingSlot<I, R>;
   using T = typename Math<R>::T;    // per-point compute type
@@ -242,23 +301,27 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : FAST2_MINB) fast_em2_kern
     T tr1 = 0, tr2 = 0;  // already divided by I (folded into ilI / invI)
     double lprod = 1.0, quad = 0.0;
     bool bad = false;
+    T v1l[I], den[I], rden[I];
 #pragma unroll
     for (int a = 0; a < I; ++a) {
-      const T v1l = v1 * lam[a];
-      const T den = v1l + v2;
-      const T rden = Math<R>::rcp(den);
-      g1[a] = v1l * rden;
-      g2[a] = v2 * rden;
+      v1l[a] = v1 * lam[a];
+      den[a] = v1l[a] + v2;
+    }
+    Math<R>::template rcp_n<I>(den, rden);
+#pragma unroll
+    for (int a = 0; a < I; ++a) {
+      g1[a] = v1l[a] * rden[a];
+      g2[a] = v2 * rden[a];
       const T pz = fma(z[a].x, z[a].x, z[a].y * z[a].y);
       // t_j = g_j^2 |z|^2 + c with c = v2 g1 = v1 lam g2 (reference
       // _kernels_numba.py:359-363), factored to save one multiply each
       t1[a] = g1[a] * fma(g1[a], pz, v2);
-      t2[a] = g2[a] * fma(g2[a], pz, v1l);
+      t2[a] = g2[a] * fma(g2[a], pz, v1l[a]);
       tr1 = fma(t1[a], il[a], tr1);
       tr2 = fma(t2[a], invI, tr2);
       if (LL) {
-        lprod *= (double)den;
-        quad = fma((double)pz, (double)rden, quad);
+        lprod *= (double)den[a];
+        quad = fma((double)pz, (double)rden[a], quad);
       }
       // den == 0 needs no test: rcp(0) poisons w below (inf * 0 / NaN)
     }
@@ -277,7 +340,9 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : FAST2_MINB) fast_em2_kern
         bad |= (((b1 >> 52) & 0x7ff) == 0x7ff) | (((b2 >> 52) & 0x7ff) == 0x7ff) | (b1 <= 0) |
                (b2 <= 0);
       }
-      const T iw1 = Math<R>::rcp(w1), iw2 = Math<R>::rcp(w2);
+      T wv[2] = {w1, w2}, iw[2];
+      Math<R>::template rcp_n<2>(wv, iw);
+      const T iw1 = iw[0], iw2 = iw[1];
       T h1[I], h2[I];
 #pragma unroll
       for (int a = 0; a < I; ++a) {
@@ -393,7 +458,7 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? 2 : FAST2_MINB) fast_em2_kern
 template <int I, typename R, bool UPDATE, bool LL, bool MU>
 cudaError_t launch_fast2_variant(const FastIterParams& p, cudaStream_t s) {
   constexpr int WARPS = kWarps;
-  constexpr int STAGES = FAST2_STAGES;
+  constexpr int STAGES = MU ? FAST2_MU_STAGES : FAST2_STAGES;
   using Sm = Fast2Smem<I, R, WARPS, STAGES, MU>;
   auto kern = fast_em2_kernel<I, R, WARPS, STAGES, UPDATE, LL, MU>;
   static bool configured = false;
