@@ -23,6 +23,22 @@ constexpr double kHermRtol = 1e-10;            // reference pencil.py:22
 
 // ---- complex arithmetic --------------------------------------------------
 FFCA_DEV double2 cmk(double re, double im) { return make_double2(re, im); }
+// sum_{c < n} src[c * stride] in the fixed order ((s_0 + s_1) + s_2) + ...
+// (bitwise equal to the plain loop), with the loads issued in batches of 8 so
+// their latencies overlap instead of forming one load -> add chain
+FFCA_DEV double ordered_sum(const double* __restrict__ src, int n, size_t stride) {
+  double s = 0.0;
+  for (int c = 0; c < n; c += 8) {
+    double t[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t[k] = (c + k < n) ? src[(size_t)(c + k) * stride] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (c + k < n) s += t[k];
+  }
+  return s;
+}
+
 FFCA_DEV double2 cadd(double2 a, double2 b) { return cmk(a.x + b.x, a.y + b.y); }
 FFCA_DEV double2 csub(double2 a, double2 b) { return cmk(a.x - b.x, a.y - b.y); }
 FFCA_DEV double2 cconj(double2 a) { return cmk(a.x, -a.y); }

@@ -90,8 +90,7 @@ __global__ void ll_collect_kernel(const double* __restrict__ llbin, int nchunk,
                                   double* __restrict__ llg) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= G) return;
-  double s = 0.0;
-  for (int c = 0; c < nchunk; ++c) s += llbin[(size_t)c * G + g];
+  const double s = ordered_sum(llbin + g, nchunk, (size_t)G);
   const double ld = logdet2 ? (double)N * logdet2[g] : 0.0;
   llg[g] = ld - s;
 }

@@ -404,9 +404,7 @@ __global__ void __launch_bounds__(64)
   if (g >= G) return;
   const int64_t m = g / F, f = g - m * F;
   if (llg) {
-    double s = 0.0;
-    for (int c = 0; c < nchunk; ++c) s += llbin[(size_t)c * G + g];
-    llg[g] = -s;
+    llg[g] = -ordered_sum(llbin + g, nchunk, (size_t)G);
   }
   double2 S[2][I][I];
   const double invN = 1.0 / (double)N;

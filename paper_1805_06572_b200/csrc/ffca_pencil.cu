@@ -50,8 +50,7 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
   }
   // likelihood of the model this pass used (P_e, logdet2(P_e))
   if (p.llg) {
-    double s = 0.0;
-    for (int c = 0; c < p.nchunk; ++c) s += p.llbin[(size_t)c * G + g];
+    const double s = ordered_sum(p.llbin + g, p.nchunk, (size_t)G);
     p.llg[g] = (double)p.N * p.logdet2[g] - s;
   }
 

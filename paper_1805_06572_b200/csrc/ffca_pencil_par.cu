@@ -46,8 +46,7 @@ __global__ void __launch_bounds__(ParLayout<I>::WARPS * 32) pencil_par_kernel(co
   // 1. chunk partials -> S~1, S~2 (full Hermitian); entries split over lanes
   bool fin = true;
   for (int e = r; e < 2 * NP; e += Lay::LB) {
-    double sacc = 0.0;
-    for (int c = 0; c < p.nchunk; ++c) sacc += p.Spart[((size_t)c * 2 * NP + e) * G + g];
+    double sacc = ordered_sum(p.Spart + (size_t)e * G + g, p.nchunk, (size_t)2 * NP * G);
     sacc *= 1.0 / (double)p.N;
     fin = fin && isfinite(sacc);
     const int j = e < NP ? 0 : 1;
@@ -67,8 +66,7 @@ __global__ void __launch_bounds__(ParLayout<I>::WARPS * 32) pencil_par_kernel(co
   if (!fin && active && p.st)
     report_error(p.st, p.iter, FFCA_ERR_SINGULAR_MATRIX, (unsigned long long)g);
   if (p.llg && active && r == 0) {
-    double sacc = 0.0;
-    for (int c = 0; c < p.nchunk; ++c) sacc += p.llbin[(size_t)c * G + g];
+    const double sacc = ordered_sum(p.llbin + g, p.nchunk, (size_t)G);
     p.llg[g] = (double)p.N * p.logdet2[g] - sacc;
   }
   // 2. P_e -> kP, W_e -> kX (row r)
