@@ -262,41 +262,15 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
     }
   };
 
+  constexpr int kAhead = STAGES - 1;  // frames issued ahead
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
+  for (int s = 0; s < kAhead; ++s) {
     if (s < K) issue(s);
     cp_async_commit();
   }
 
-  constexpr int kUnroll = FAST2_UNROLL;
-#pragma unroll kUnroll
-  for (int k = 0; k < K; ++k) {
-    if (k + STAGES - 1 < K) issue(k + STAGES - 1);
-    cp_async_commit();
-    cp_async_wait<STAGES - 1>();
-    const int64_t n = nfirst + (int64_t)k * WARPS;
-    const unsigned char* slot = myslots + (size_t)(k % STAGES) * kStageStride;
-    T2 yv[I];
-#pragma unroll
-    for (int a = 0; a < I; ++a) yv[a] = ((const T2*)slot)[a];
-    const T v1 = *(const R*)(slot + Slot::YB);
-    const T v2 = *(const R*)(slot + Slot::YB + sizeof(R));
-
-    T2 z[I];
-#pragma unroll
-    for (int a = 0; a < I; ++a) {
-      const T2 p0 = sP[(0 * I + a) * 32 + lane];
-      T zr = p0.x * yv[0].x + p0.y * yv[0].y;
-      T zi = p0.x * yv[0].y - p0.y * yv[0].x;
-#pragma unroll
-      for (int b = 1; b < I; ++b) {
-        const T2 pb = sP[(b * I + a) * 32 + lane];
-        zr = fma(pb.x, yv[b].x, fma(pb.y, yv[b].y, zr));
-        zi = fma(pb.x, yv[b].y, fma(-pb.y, yv[b].x, zi));
-      }
-      z[a].x = zr;
-      z[a].y = zi;
-    }
+  // per-frame E+M body once z = P^H y is known
+  auto frame = [&](int k, int64_t n, const T2 (&yv)[I], T v1, T v2, const T2 (&z)[I]) {
     T g1[I], g2[I], t1[I], t2[I];
     T tr1 = 0, tr2 = 0;  // already divided by I (folded into ilI / invI)
     double lprod = 1.0, quad = 0.0;
@@ -408,6 +382,42 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
       }
     }
     if (bad && bad_n == 0) bad_n = n + 1;
+  };
+  auto load_frame = [&](int k, T2 (&yv)[I], T& v1, T& v2) {
+    const unsigned char* slot = myslots + (size_t)(k % STAGES) * kStageStride;
+#pragma unroll
+    for (int a = 0; a < I; ++a) yv[a] = ((const T2*)slot)[a];
+    v1 = *(const R*)(slot + Slot::YB);
+    v2 = *(const R*)(slot + Slot::YB + sizeof(R));
+  };
+
+  {
+    constexpr int kUnroll = FAST2_UNROLL;
+#pragma unroll kUnroll
+    for (int k = 0; k < K; ++k) {
+      if (k + STAGES - 1 < K) issue(k + STAGES - 1);
+      cp_async_commit();
+      cp_async_wait<STAGES - 1>();
+      T2 yv[I];
+      T v1, v2;
+      load_frame(k, yv, v1, v2);
+      T2 z[I];
+#pragma unroll
+      for (int a = 0; a < I; ++a) {
+        const T2 p0 = sP[(0 * I + a) * 32 + lane];
+        T zr = p0.x * yv[0].x + p0.y * yv[0].y;
+        T zi = p0.x * yv[0].y - p0.y * yv[0].x;
+#pragma unroll
+        for (int b = 1; b < I; ++b) {
+          const T2 pb = sP[(b * I + a) * 32 + lane];
+          zr = fma(pb.x, yv[b].x, fma(pb.y, yv[b].y, zr));
+          zi = fma(pb.x, yv[b].y, fma(-pb.y, yv[b].x, zi));
+        }
+        z[a].x = zr;
+        z[a].y = zi;
+      }
+      frame(k, nfirst + (int64_t)k * WARPS, yv, v1, v2, z);
+    }
   }
   flush();
   cp_async_wait_all();
