@@ -190,6 +190,16 @@ int ffca_logdet2(const double* P, double* out, int64_t batch, int D, void* strea
 int ffca_init_powers(const void* y, void* v, double* v_floor, int64_t M, int64_t N, int64_t F,
                      int I, int dtype, void* stream);
 
+/* ---- mask-clustering initial model (reference initializers.py:42-143) -----
+ * y (M,N,F,I) complex128 -> v (M,2,N,F) f64, S (M,2,F,I,I) c128, v_floor (M,F):
+ * per-bin deterministic 2-means of the phase-aligned unit observations, unit-
+ * trace group covariances + 1e-2 ridge, cross-bin label alignment, masked
+ * floored powers. Needs N >= 2 I (the reference falls back to init_random(y, 0)
+ * below that; the caller does too). */
+size_t ffca_init_masks_workspace_size(int64_t M, int64_t N, int64_t F, int I);
+int ffca_init_masks(const double* y, double* v, double* S, double* v_floor, int64_t M, int64_t N,
+                    int64_t F, int I, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- STFT front / back end (reference stft.py:9-107) ----------------------
  * Square-root periodic Hann window, frame_shift = frame_length / 2, half a
  * frame of leading zeros; frame_length a power of two in [2, 8192].

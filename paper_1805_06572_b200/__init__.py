@@ -9,7 +9,9 @@ signatures, layouts, return types and exceptions follow the reference
 (``pkg/src/fastfca/__init__.py:10-77``) for everything on the EM path and
 the STFT front / back end (``stft_analyze`` / ``stft_synthesize``, also on
 the GPU); ``separate`` chains analysis -> init -> EM -> synthesis in HBM.
-The simulator, metrics, WAV I/O and CLI are out of scope.
+``init_from_masks`` (the direction-clustering initial model) runs on the
+GPU as well. The simulator, metrics, WAV I/O and CLI are out of scope (see
+DESIGN.md).
 """
 
 from .conventional import e_step, fca_run, log_likelihood, m_step
@@ -18,7 +20,7 @@ from .errors import (BackendUnavailableError, ConfigurationError, DefinitenessEr
                      SingularMixtureError)
 from .fast import (fast_e_step, fast_m_step_S, fast_m_step_v, fastfca_run, propagate_pencil,
                    transform_observations)
-from .initializers import init_random
+from .initializers import init_from_masks, init_from_masks_batch, init_random, init_random_batch
 from .pencil import PencilDecomposition, gevd_hpd, hermitian_eig, solve_hermitian_system
 from .pipeline import separate, separate_device
 from .stft import (sqrt_hann, stft_analyze, stft_analyze_device, stft_synthesize,
@@ -52,7 +54,10 @@ __all__ = [
     "fca_run",
     "gevd_hpd",
     "hermitian_eig",
+    "init_from_masks",
+    "init_from_masks_batch",
     "init_random",
+    "init_random_batch",
     "log_likelihood",
     "m_step",
     "propagate_pencil",

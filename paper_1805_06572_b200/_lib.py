@@ -97,6 +97,9 @@ SIGNATURES = [
      [c_vp, c_vp, c_vp, c_i64, c_i64, c_int, c_vp, c_vp]),
     ("ffca_logdet2", c_int, [c_vp, c_vp, c_i64, c_int, c_vp]),
     ("ffca_init_powers", c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_int, c_int, c_vp]),
+    ("ffca_init_masks_workspace_size", c_sz, [c_i64, c_i64, c_i64, c_int]),
+    ("ffca_init_masks", c_int,
+     [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_sz, c_vp]),
     ("ffca_stft_frames", c_i64, [c_i64, c_int]),
     ("ffca_stft_analyze", c_int, [c_vp, c_vp, c_i64, c_int, c_i64, c_int, c_vp]),
     ("ffca_stft_synthesize", c_int, [c_vp, c_vp, c_i64, c_int, c_i64, c_int, c_i64, c_vp]),

@@ -1,0 +1,528 @@
+// Mask-clustering initial model on the device (reference initializers.py:42-143,
+// SURVEY.md §8(f) row 3).
+//
+//  K7a masks_bin_kernel   one CTA per (mixture, bin): channel energies and
+//                         frame powers, unit-normalised phase-aligned
+//                         observations z (stored bin-major in the
+//                         workspace), deterministic 2-means over the frames
+//                         (_two_means, :42-68), unit-trace group
+//                         covariances + 1e-2 ridge (:108-115);
+//  K7b masks_align_kernel one CTA per mixture: cross-bin label alignment —
+//                         greedy pass in decreasing bin-power order, then up
+//                         to five refinement sweeps (:117-137) — on the exact
+//                         integer centred masks N * mask - count (a flip is
+//                         the sign of the exact rational correlation);
+//  K7c masks_apply_kernel masked, floored powers (:139-143) and the S swap of
+//                         flipped bins.
+// Frames are spread over the CTA's threads with a fixed thread->frame map and
+// fixed-order block reductions, so the result is deterministic.
+#include "ffca_internal.cuh"
+
+namespace ffca {
+namespace {
+
+constexpr int kMT = 256;  // threads per bin CTA
+constexpr int kMW = kMT / 32;
+constexpr int kAT = 1024;  // threads of the alignment CTA
+constexpr int kAW = kAT / 32;
+constexpr int kKmeansIters = 50;
+constexpr double kMaskRidge = 1e-2;
+
+// sum of NV values over the CTA (warp shuffles, then warps in index order);
+// every thread receives the totals
+template <int NV, int W>
+FFCA_DEV void block_sum(double (&v)[NV], double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) red[warp * NV + k] = x;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double s = 0.0;
+    for (int w = 0; w < W; ++w) s += red[w * NV + k];
+    v[k] = s;
+  }
+  __syncthreads();
+}
+
+template <int W>
+FFCA_DEV long long block_sum_i64(long long x, long long* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if (lane == 0) red[warp] = x;
+  __syncthreads();
+  long long s = 0;
+  for (int w = 0; w < W; ++w) s += red[w];
+  __syncthreads();
+  return s;
+}
+
+// (value, index, payload) with numpy argmax semantics: largest value, first
+// index among equals
+struct ArgMax {
+  double v;
+  int i;
+  int pay;
+};
+FFCA_DEV bool better(const ArgMax& a, const ArgMax& b) {
+  return a.v > b.v || (a.v == b.v && a.i < b.i);
+}
+template <int W>
+FFCA_DEV ArgMax block_argmax(ArgMax a, double* rv, int* ri) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMax b;
+    b.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+    b.i = __shfl_xor_sync(0xffffffffu, a.i, o);
+    b.pay = __shfl_xor_sync(0xffffffffu, a.pay, o);
+    if (better(b, a)) a = b;
+  }
+  if (lane == 0) {
+    rv[warp] = a.v;
+    ri[2 * warp] = a.i;
+    ri[2 * warp + 1] = a.pay;
+  }
+  __syncthreads();
+  ArgMax r{rv[0], ri[0], ri[1]};
+  for (int w = 1; w < W; ++w) {
+    ArgMax b{rv[w], ri[2 * w], ri[2 * w + 1]};
+    if (better(b, r)) r = b;
+  }
+  __syncthreads();
+  return r;
+}
+
+template <int I>
+FFCA_DEV double dist2(const double2* z, const double2 (&c)[I]) {
+  double d = 0.0;
+#pragma unroll
+  for (int a = 0; a < I; ++a) {
+    const double2 e = make_double2(z[a].x - c[a].x, z[a].y - c[a].y);
+    d += e.x * e.x + e.y * e.y;
+  }
+  return d;
+}
+
+template <int I>
+__global__ void __launch_bounds__(kMT)
+    masks_bin_kernel(const double2* __restrict__ y, int64_t N, int64_t F,
+                     double2* __restrict__ zs, uint8_t* __restrict__ lab,
+                     double* __restrict__ fpow, double* __restrict__ bpow, int* __restrict__ cnt,
+                     double2* __restrict__ S) {
+  constexpr int NE = I * (I + 1) / 2;  // upper-triangle entries of a covariance
+  constexpr int NR = 4 * I > 2 * NE ? 4 * I : 2 * NE;
+  __shared__ double red[kMW * (NR > 16 ? NR : 16)];
+  __shared__ double rv[kMW];
+  __shared__ int ri[2 * kMW];
+  const int tid = threadIdx.x;
+  const int64_t g = blockIdx.x;
+  const int64_t m = g / F, f = g - m * F;
+  const double2* yb = y + (m * N * F + f) * I;
+  const int64_t FI = F * I;
+  double2* zb = zs + g * N * I;
+  uint8_t* lb = lab + g * N;
+  double* pb = fpow + g * N;
+
+  // 1. channel energies (reference channel) and frame powers
+  double E[I];
+#pragma unroll
+  for (int a = 0; a < I; ++a) E[a] = 0.0;
+  for (int64_t n = tid; n < N; n += kMT) {
+    double p = 0.0;
+#pragma unroll
+    for (int a = 0; a < I; ++a) {
+      const double2 x = yb[n * FI + a];
+      const double e = x.x * x.x + x.y * x.y;
+      E[a] += e;
+      p += e;
+    }
+    pb[n] = p;
+  }
+  block_sum<I, kMW>(E, red);
+  int ref = 0;
+  double tot = E[0];
+#pragma unroll
+  for (int a = 1; a < I; ++a) {
+    if (E[a] > E[ref]) ref = a;
+    tot += E[a];
+  }
+  if (tid == 0) bpow[g] = tot;
+
+  // 2. z = w / max(|w|, 1e-300) * conj(phase of the reference channel)
+  //    (initializers.py:100-106); highest-power frame seeds cluster 0
+  ArgMax best{-1.0, 0x7fffffff, 0};
+  for (int64_t n = tid; n < N; n += kMT) {
+    const double p = pb[n];
+    const double nrm = fmax(sqrt(p), 1e-300);
+    double2 z[I];
+#pragma unroll
+    for (int a = 0; a < I; ++a) {
+      const double2 x = yb[n * FI + a];
+      z[a] = make_double2(x.x / nrm, x.y / nrm);
+    }
+    const double2 rvv = z[ref];
+    const double mag = hypot(rvv.x, rvv.y);
+    double2 ph = make_double2(1.0, 0.0);
+    if (mag > 0.0) {
+      const double d = fmax(mag, 1e-300);
+      ph = make_double2(rvv.x / d, rvv.y / d);
+    }
+#pragma unroll
+    for (int a = 0; a < I; ++a) {
+      const double2 t = z[a];
+      zb[n * I + a] = make_double2(t.x * ph.x + t.y * ph.y, t.y * ph.x - t.x * ph.y);
+    }
+    ArgMax c{p, (int)n, 0};
+    if (better(c, best)) best = c;
+  }
+  best = block_argmax<kMW>(best, rv, ri);
+  __syncthreads();  // z visible to the CTA
+  double2 c0[I], c1[I];
+#pragma unroll
+  for (int a = 0; a < I; ++a) c0[a] = zb[(int64_t)best.i * I + a];
+  // farthest frame from c0 seeds cluster 1
+  ArgMax far{-1.0, 0x7fffffff, 0};
+  for (int64_t n = tid; n < N; n += kMT) {
+    ArgMax c{dist2<I>(zb + n * I, c0), (int)n, 0};
+    if (better(c, far)) far = c;
+    lb[n] = 0;
+  }
+  far = block_argmax<kMW>(far, rv, ri);
+#pragma unroll
+  for (int a = 0; a < I; ++a) c1[a] = zb[(int64_t)far.i * I + a];
+
+  // 3. 2-means (_two_means, initializers.py:42-68); label 1 = cluster 0
+  long long count0 = 0;
+#pragma unroll 1
+  for (int it = 0; it < kKmeansIters; ++it) {
+    double acc[2];  // count of label 1, number of changed labels
+    acc[0] = acc[1] = 0.0;
+    ArgMax worst{-1.0, 0x7fffffff, 0};
+    for (int64_t n = tid; n < N; n += kMT) {
+      const double d0 = dist2<I>(zb + n * I, c0);
+      const double d1 = dist2<I>(zb + n * I, c1);
+      const int nw = d0 <= d1 ? 1 : 0;
+      const int old = lb[n];
+      acc[0] += nw;
+      acc[1] += (nw != old);
+      lb[n] = (uint8_t)nw;
+      ArgMax c{nw ? d0 : d1, (int)n, nw | (old << 1)};
+      if (better(c, worst)) worst = c;
+    }
+    block_sum<2, kMW>(acc, red);
+    worst = block_argmax<kMW>(worst, rv, ri);
+    count0 = (long long)acc[0];
+    long long changed = (long long)acc[1];
+    if (count0 == 0 || count0 == N) {  // re-seed the empty cluster with the worst fit
+      const int nw = worst.pay & 1, old = (worst.pay >> 1) & 1;
+      if (tid == 0) lb[worst.i] = (uint8_t)(1 - nw);
+      count0 += nw ? -1 : 1;
+      changed += (nw == old) ? 1 : -1;
+    }
+    __syncthreads();
+    if (changed == 0) break;
+    // centroids of the new groups
+    double s[4 * I];
+#pragma unroll
+    for (int k = 0; k < 4 * I; ++k) s[k] = 0.0;
+    for (int64_t n = tid; n < N; n += kMT) {
+      const int l = lb[n];
+#pragma unroll
+      for (int a = 0; a < I; ++a) {
+        const double2 z = zb[n * I + a];
+        if (l) {
+          s[2 * a] += z.x;
+          s[2 * a + 1] += z.y;
+        } else {
+          s[2 * I + 2 * a] += z.x;
+          s[2 * I + 2 * a + 1] += z.y;
+        }
+      }
+    }
+    block_sum<4 * I, kMW>(s, red);
+    const double n0 = (double)count0, n1 = (double)(N - count0);
+#pragma unroll
+    for (int a = 0; a < I; ++a) {
+      c0[a] = make_double2(s[2 * a] / n0, s[2 * a + 1] / n0);
+      c1[a] = make_double2(s[2 * I + 2 * a] / n1, s[2 * I + 2 * a + 1] / n1);
+    }
+  }
+  if (tid == 0) cnt[g] = (int)count0;
+
+  // 4. group covariances sum w w^H / |group|, unit trace, + ridge (:108-115)
+#pragma unroll 1
+  for (int j = 0; j < 2; ++j) {
+    const int want = j == 0 ? 1 : 0;
+    const long long ng = j == 0 ? count0 : N - count0;
+    double s[2 * NE];
+#pragma unroll
+    for (int k = 0; k < 2 * NE; ++k) s[k] = 0.0;
+    for (int64_t n = tid; n < N; n += kMT) {
+      if (lb[n] != want) continue;
+      double2 w[I];
+#pragma unroll
+      for (int a = 0; a < I; ++a) w[a] = yb[n * FI + a];
+      int e = 0;
+#pragma unroll
+      for (int a = 0; a < I; ++a)
+#pragma unroll
+        for (int b = a; b < I; ++b, ++e) {  // w_a conj(w_b)
+          s[2 * e] += w[a].x * w[b].x + w[a].y * w[b].y;
+          s[2 * e + 1] += w[a].y * w[b].x - w[a].x * w[b].y;
+        }
+    }
+    block_sum<2 * NE, kMW>(s, red);
+    double2* Sd = S + ((m * 2 + j) * F + f) * I * I;
+    if (tid == 0) {
+      double tr = 0.0;
+      double2 cov[I][I];
+      int e = 0;
+#pragma unroll
+      for (int a = 0; a < I; ++a)
+#pragma unroll
+        for (int b = a; b < I; ++b, ++e) {
+          double2 v = ng > 0 ? make_double2(s[2 * e] / (double)ng, s[2 * e + 1] / (double)ng)
+                             : make_double2(a == b ? 1.0 : 0.0, 0.0);
+          cov[a][b] = v;
+          cov[b][a] = make_double2(v.x, -v.y);
+        }
+#pragma unroll
+      for (int a = 0; a < I; ++a) tr += cov[a][a].x;
+#pragma unroll
+      for (int a = 0; a < I; ++a)
+#pragma unroll
+        for (int b = 0; b < I; ++b) {
+          double2 v = tr > 0.0 ? make_double2(cov[a][b].x / tr, cov[a][b].y / tr)
+                               : make_double2(a == b ? 1.0 / I : 0.0, 0.0);
+          if (a == b) v.x += kMaskRidge;
+          Sd[a * I + b] = v;
+        }
+    }
+  }
+}
+
+// cross-bin alignment of one mixture; D_f[n] = N lab_f[n] - cnt_f (exact)
+__global__ void __launch_bounds__(kAT)
+    masks_align_kernel(const uint8_t* __restrict__ lab, const int* __restrict__ cnt,
+                       const double* __restrict__ bpow, int64_t N, int64_t F,
+                       long long* __restrict__ gbuf, int* __restrict__ order,
+                       uint8_t* __restrict__ flip) {
+  __shared__ long long red[kAW];
+  __shared__ int sflip;
+  const int tid = threadIdx.x;
+  const int64_t m = blockIdx.x;
+  const uint8_t* L = lab + m * F * N;
+  const int* K = cnt + m * F;
+  const double* P = bpow + m * F;
+  long long* gv = gbuf + m * N;
+  int* ord = order + m * F;
+  uint8_t* fl = flip + m * F;
+  // decreasing bin power, ties by index (stable)
+  for (int64_t f = tid; f < F; f += kAT) {
+    int64_t r = 0;
+    const double pf = P[f];
+    for (int64_t h = 0; h < F; ++h) r += (P[h] > pf) || (P[h] == pf && h < f);
+    ord[r] = (int)f;
+    fl[f] = 0;
+  }
+  __syncthreads();
+  const long long NN = (long long)N;
+  auto D = [&](int64_t f, int64_t n) -> long long { return NN * L[f * N + n] - K[f]; };
+  {
+    const int64_t f0 = ord[0];
+    for (int64_t n = tid; n < N; n += kAT) gv[n] = D(f0, n);
+  }
+  __syncthreads();
+  // greedy pass (initializers.py:125-129)
+#pragma unroll 1
+  for (int64_t i = 1; i < F; ++i) {
+    const int64_t f = ord[i];
+    long long part = 0;
+    for (int64_t n = tid; n < N; n += kAT) part += D(f, n) * gv[n];
+    const long long dot = block_sum_i64<kAW>(part, red);
+    const bool neg = dot < 0;
+    if (tid == 0 && neg) fl[f] = 1;
+    for (int64_t n = tid; n < N; n += kAT) gv[n] += neg ? -D(f, n) : D(f, n);
+    __syncthreads();
+  }
+  // refinement sweeps (initializers.py:130-137)
+#pragma unroll 1
+  for (int sweep = 0; sweep < 5; ++sweep) {
+    for (int64_t n = tid; n < N; n += kAT) {
+      long long s = 0;
+      for (int64_t f = 0; f < F; ++f) s += fl[f] ? -D(f, n) : D(f, n);
+      gv[n] = s;
+    }
+    if (tid == 0) sflip = 0;
+    __syncthreads();
+#pragma unroll 1
+    for (int64_t i = 0; i < F; ++i) {
+      const int64_t f = ord[i];
+      const bool fi = fl[f] != 0;
+      long long part = 0;
+      for (int64_t n = tid; n < N; n += kAT) {
+        const long long d = fi ? -D(f, n) : D(f, n);
+        part += d * (gv[n] - d);
+      }
+      const long long dot = block_sum_i64<kAW>(part, red);
+      if (dot < 0) {
+        for (int64_t n = tid; n < N; n += kAT) {
+          const long long d = fi ? -D(f, n) : D(f, n);
+          gv[n] -= 2 * d;
+        }
+        if (tid == 0) {
+          fl[f] = fi ? 0 : 1;
+          sflip = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!sflip) break;
+    __syncthreads();
+  }
+}
+
+// v = max(mask * |y|^2 / I, floor) per source (:139-143); swap S of flipped bins
+template <int I>
+__global__ void masks_apply_kernel(const uint8_t* __restrict__ lab, const uint8_t* __restrict__ flip,
+                                   const double* __restrict__ fpow, const double* __restrict__ floor,
+                                   double* __restrict__ v, double2* __restrict__ S, int64_t M,
+                                   int64_t N, int64_t F) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < M * F && flip[t]) {  // swap the two sources' covariances of this bin
+    const int64_t m = t / F, f = t - m * F;
+    double2* a = S + ((m * 2 + 0) * F + f) * I * I;
+    double2* b = S + ((m * 2 + 1) * F + f) * I * I;
+    for (int e = 0; e < I * I; ++e) {
+      const double2 x = a[e];
+      a[e] = b[e];
+      b[e] = x;
+    }
+  }
+  if (t >= M * N * F) return;
+  const int64_t m = t / (N * F);
+  const int64_t r = t - m * N * F;
+  const int64_t n = r / F, f = r - n * F;
+  const int64_t g = m * F + f;
+  const int l = lab[g * N + n] ^ flip[g];
+  const double pp = fpow[g * N + n] / I;
+  const double fl = floor[g];
+  const double a = l ? pp : 0.0, b = l ? 0.0 : pp;
+  v[(m * 2 + 0) * N * F + n * F + f] = a < fl ? fl : a;
+  v[(m * 2 + 1) * N * F + n * F + f] = b < fl ? fl : b;
+}
+
+struct MaskWs {
+  double2* zs;
+  double* fpow;
+  double* bpow;
+  long long* gbuf;
+  int* cnt;
+  int* order;
+  uint8_t* lab;
+  uint8_t* flip;
+  size_t bytes;
+};
+
+MaskWs carve_masks(void* base, int64_t M, int64_t N, int64_t F, int I) {
+  MaskWs w{};
+  size_t off = 0;
+  auto take = [&](size_t nbytes) {
+    const size_t o = off;
+    off += (nbytes + 255) / 256 * 256;
+    return base ? (char*)base + o : nullptr;
+  };
+  const int64_t G = M * F;
+  w.zs = (double2*)take((size_t)G * N * I * sizeof(double2));
+  w.fpow = (double*)take((size_t)G * N * sizeof(double));
+  w.bpow = (double*)take((size_t)G * sizeof(double));
+  w.gbuf = (long long*)take((size_t)M * N * sizeof(long long));
+  w.cnt = (int*)take((size_t)G * sizeof(int));
+  w.order = (int*)take((size_t)G * sizeof(int));
+  w.lab = (uint8_t*)take((size_t)G * N);
+  w.flip = (uint8_t*)take((size_t)G);
+  w.bytes = off;
+  return w;
+}
+
+}  // namespace
+
+cudaError_t launch_init_powers(const void* y, void* v, double* floor, int64_t M, int64_t N,
+                               int64_t F, int I, int dtype, cudaStream_t s);
+
+}  // namespace ffca
+
+using namespace ffca;
+
+extern "C" {
+
+size_t ffca_init_masks_workspace_size(int64_t M, int64_t N, int64_t F, int I) {
+  if (M < 1 || N < 1 || F < 1 || I < 1 || I > kMaxOrder) return 0;
+  return carve_masks(nullptr, M, N, F, I).bytes;
+}
+
+int ffca_init_masks(const double* y, double* v, double* S, double* v_floor, int64_t M, int64_t N,
+                    int64_t F, int I, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!y || !v || !S || !v_floor || !workspace || M < 1 || F < 1 || I < 1 || I > kMaxOrder ||
+      N < 2 * I || N > 0x7fffffff)
+    return FFCA_ERR_INVALID;
+  const MaskWs w = carve_masks(workspace, M, N, F, I);
+  if (w.bytes > workspace_bytes) return FFCA_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_init_powers(y, v, v_floor, M, N, F, I, FFCA_C128, s);  // floor
+  if (e != cudaSuccess) return FFCA_ERR_CUDA;
+  const double2* y2 = (const double2*)y;
+  double2* S2 = (double2*)S;
+  switch (I) {
+#define FFCA_MASK_CASE(II)                                                                  \
+  case II:                                                                                  \
+    masks_bin_kernel<II><<<(unsigned)(M * F), kMT, 0, s>>>(y2, N, F, w.zs, w.lab, w.fpow,   \
+                                                           w.bpow, w.cnt, S2);              \
+    break;
+    FFCA_MASK_CASE(1)
+    FFCA_MASK_CASE(2)
+    FFCA_MASK_CASE(3)
+    FFCA_MASK_CASE(4)
+    FFCA_MASK_CASE(5)
+    FFCA_MASK_CASE(6)
+    FFCA_MASK_CASE(7)
+    FFCA_MASK_CASE(8)
+#undef FFCA_MASK_CASE
+    default:
+      return FFCA_ERR_INVALID;
+  }
+  if (cudaGetLastError() != cudaSuccess) return FFCA_ERR_CUDA;
+  masks_align_kernel<<<(unsigned)M, kAT, 0, s>>>(w.lab, w.cnt, w.bpow, N, F, w.gbuf, w.order,
+                                                 w.flip);
+  if (cudaGetLastError() != cudaSuccess) return FFCA_ERR_CUDA;
+  const int64_t total = M * N * F;
+  const unsigned nb = (unsigned)((total + 255) / 256);
+  switch (I) {
+#define FFCA_APPLY_CASE(II)                                                               \
+  case II:                                                                                \
+    masks_apply_kernel<II><<<nb, 256, 0, s>>>(w.lab, w.flip, w.fpow, v_floor, v, S2, M,  \
+                                              N, F);                                      \
+    break;
+    FFCA_APPLY_CASE(1)
+    FFCA_APPLY_CASE(2)
+    FFCA_APPLY_CASE(3)
+    FFCA_APPLY_CASE(4)
+    FFCA_APPLY_CASE(5)
+    FFCA_APPLY_CASE(6)
+    FFCA_APPLY_CASE(7)
+    FFCA_APPLY_CASE(8)
+#undef FFCA_APPLY_CASE
+    default:
+      return FFCA_ERR_INVALID;
+  }
+  return cudaGetLastError() == cudaSuccess ? FFCA_OK : FFCA_ERR_CUDA;
+}
+
+}  // extern "C"
