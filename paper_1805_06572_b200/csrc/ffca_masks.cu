@@ -7,24 +7,34 @@
 //                         workspace), deterministic 2-means over the frames
 //                         (_two_means, :42-68), unit-trace group
 //                         covariances + 1e-2 ridge (:108-115);
-//  K7b masks_align_kernel one CTA per mixture: cross-bin label alignment —
+//  K7b masks_pack / masks_gram / masks_align: cross-bin label alignment —
 //                         greedy pass in decreasing bin-power order, then up
 //                         to five refinement sweeps (:117-137) — on the exact
 //                         integer centred masks N * mask - count (a flip is
-//                         the sign of the exact rational correlation);
+//                         the sign of the exact rational correlation),
+//                         evaluated through their Gram matrix (bit-packed
+//                         popcounts) so each sequential step is O(F);
 //  K7c masks_apply_kernel masked, floored powers (:139-143) and the S swap of
 //                         flipped bins.
 // Frames are spread over the CTA's threads with a fixed thread->frame map and
 // fixed-order block reductions, so the result is deterministic.
+#include <cstdio>
+#include <cstdlib>
+
 #include "ffca_internal.cuh"
 
 namespace ffca {
 namespace {
 
-constexpr int kMT = 256;  // threads per bin CTA
-constexpr int kMW = kMT / 32;
-constexpr int kAT = 1024;  // threads of the alignment CTA
-constexpr int kAW = kAT / 32;
+// threads per bin CTA (measured: 256 beats 32/64/128 even for 1250 frames)
+constexpr int kMTLarge = 256;
+// a bin whose phase-aligned observations fit keeps them (and its labels) in
+// shared memory for all 2-means iterations instead of re-reading HBM
+constexpr size_t kMaskSmemBytes = 100 * 1024;
+inline size_t mask_smem(int64_t N, int I) {
+  const size_t b = (size_t)N * I * 16 + (size_t)N;
+  return b <= kMaskSmemBytes ? b : 0;
+}
 constexpr int kKmeansIters = 50;
 constexpr double kMaskRidge = 1e-2;
 
@@ -48,19 +58,6 @@ FFCA_DEV void block_sum(double (&v)[NV], double* red) {
     v[k] = s;
   }
   __syncthreads();
-}
-
-template <int W>
-FFCA_DEV long long block_sum_i64(long long x, long long* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  if (lane == 0) red[warp] = x;
-  __syncthreads();
-  long long s = 0;
-  for (int w = 0; w < W; ++w) s += red[w];
-  __syncthreads();
-  return s;
 }
 
 // (value, index, payload) with numpy argmax semantics: largest value, first
@@ -99,6 +96,10 @@ FFCA_DEV ArgMax block_argmax(ArgMax a, double* rv, int* ri) {
   return r;
 }
 
+FFCA_DEV bool mask_smem_dev(int64_t N, int I) {
+  return (size_t)N * I * 16 + (size_t)N <= kMaskSmemBytes;
+}
+
 template <int I>
 FFCA_DEV double dist2(const double2* z, const double2 (&c)[I]) {
   double d = 0.0;
@@ -110,12 +111,13 @@ FFCA_DEV double dist2(const double2* z, const double2 (&c)[I]) {
   return d;
 }
 
-template <int I>
+template <int I, int kMT>
 __global__ void __launch_bounds__(kMT)
     masks_bin_kernel(const double2* __restrict__ y, int64_t N, int64_t F,
                      double2* __restrict__ zs, uint8_t* __restrict__ lab,
                      double* __restrict__ fpow, double* __restrict__ bpow, int* __restrict__ cnt,
                      double2* __restrict__ S) {
+  constexpr int kMW = kMT / 32;
   constexpr int NE = I * (I + 1) / 2;  // upper-triangle entries of a covariance
   constexpr int NR = 4 * I > 2 * NE ? 4 * I : 2 * NE;
   __shared__ double red[kMW * (NR > 16 ? NR : 16)];
@@ -126,15 +128,19 @@ __global__ void __launch_bounds__(kMT)
   const int64_t m = g / F, f = g - m * F;
   const double2* yb = y + (m * N * F + f) * I;
   const int64_t FI = F * I;
-  double2* zb = zs + g * N * I;
-  uint8_t* lb = lab + g * N;
+  extern __shared__ __align__(16) unsigned char zsm[];
+  const bool in_smem = mask_smem_dev(N, I);
+  double2* zb = in_smem ? (double2*)zsm : zs + g * N * I;
+  uint8_t* lb_out = lab + g * N;
+  uint8_t* lb = in_smem ? zsm + (size_t)N * I * 16 : lb_out;
   double* pb = fpow + g * N;
+  const int Ni = (int)N;  // N < 2^31 (checked by the caller)
 
   // 1. channel energies (reference channel) and frame powers
   double E[I];
 #pragma unroll
   for (int a = 0; a < I; ++a) E[a] = 0.0;
-  for (int64_t n = tid; n < N; n += kMT) {
+  for (int n = tid; n < Ni; n += kMT) {
     double p = 0.0;
 #pragma unroll
     for (int a = 0; a < I; ++a) {
@@ -158,7 +164,7 @@ __global__ void __launch_bounds__(kMT)
   // 2. z = w / max(|w|, 1e-300) * conj(phase of the reference channel)
   //    (initializers.py:100-106); highest-power frame seeds cluster 0
   ArgMax best{-1.0, 0x7fffffff, 0};
-  for (int64_t n = tid; n < N; n += kMT) {
+  for (int n = tid; n < Ni; n += kMT) {
     const double p = pb[n];
     const double nrm = fmax(sqrt(p), 1e-300);
     double2 z[I];
@@ -177,7 +183,7 @@ __global__ void __launch_bounds__(kMT)
 #pragma unroll
     for (int a = 0; a < I; ++a) {
       const double2 t = z[a];
-      zb[n * I + a] = make_double2(t.x * ph.x + t.y * ph.y, t.y * ph.x - t.x * ph.y);
+      zb[(size_t)n * I + a] = make_double2(t.x * ph.x + t.y * ph.y, t.y * ph.x - t.x * ph.y);
     }
     ArgMax c{p, (int)n, 0};
     if (better(c, best)) best = c;
@@ -189,8 +195,8 @@ __global__ void __launch_bounds__(kMT)
   for (int a = 0; a < I; ++a) c0[a] = zb[(int64_t)best.i * I + a];
   // farthest frame from c0 seeds cluster 1
   ArgMax far{-1.0, 0x7fffffff, 0};
-  for (int64_t n = tid; n < N; n += kMT) {
-    ArgMax c{dist2<I>(zb + n * I, c0), (int)n, 0};
+  for (int n = tid; n < Ni; n += kMT) {
+    ArgMax c{dist2<I>(zb + (size_t)n * I, c0), (int)n, 0};
     if (better(c, far)) far = c;
     lb[n] = 0;
   }
@@ -205,9 +211,10 @@ __global__ void __launch_bounds__(kMT)
     double acc[2];  // count of label 1, number of changed labels
     acc[0] = acc[1] = 0.0;
     ArgMax worst{-1.0, 0x7fffffff, 0};
-    for (int64_t n = tid; n < N; n += kMT) {
-      const double d0 = dist2<I>(zb + n * I, c0);
-      const double d1 = dist2<I>(zb + n * I, c1);
+#pragma unroll 4
+    for (int n = tid; n < Ni; n += kMT) {
+      const double d0 = dist2<I>(zb + (size_t)n * I, c0);
+      const double d1 = dist2<I>(zb + (size_t)n * I, c1);
       const int nw = d0 <= d1 ? 1 : 0;
       const int old = lb[n];
       acc[0] += nw;
@@ -232,11 +239,12 @@ __global__ void __launch_bounds__(kMT)
     double s[4 * I];
 #pragma unroll
     for (int k = 0; k < 4 * I; ++k) s[k] = 0.0;
-    for (int64_t n = tid; n < N; n += kMT) {
+#pragma unroll 4
+    for (int n = tid; n < Ni; n += kMT) {
       const int l = lb[n];
 #pragma unroll
       for (int a = 0; a < I; ++a) {
-        const double2 z = zb[n * I + a];
+        const double2 z = zb[(size_t)n * I + a];
         if (l) {
           s[2 * a] += z.x;
           s[2 * a + 1] += z.y;
@@ -255,6 +263,8 @@ __global__ void __launch_bounds__(kMT)
     }
   }
   if (tid == 0) cnt[g] = (int)count0;
+  if (in_smem)
+    for (int n = tid; n < Ni; n += kMT) lb_out[n] = lb[n];
 
   // 4. group covariances sum w w^H / |group|, unit trace, + ridge (:108-115)
 #pragma unroll 1
@@ -264,7 +274,7 @@ __global__ void __launch_bounds__(kMT)
     double s[2 * NE];
 #pragma unroll
     for (int k = 0; k < 2 * NE; ++k) s[k] = 0.0;
-    for (int64_t n = tid; n < N; n += kMT) {
+    for (int n = tid; n < Ni; n += kMT) {
       if (lb[n] != want) continue;
       double2 w[I];
 #pragma unroll
@@ -309,23 +319,77 @@ __global__ void __launch_bounds__(kMT)
 }
 
 // cross-bin alignment of one mixture; D_f[n] = N lab_f[n] - cnt_f (exact)
-__global__ void __launch_bounds__(kAT)
-    masks_align_kernel(const uint8_t* __restrict__ lab, const int* __restrict__ cnt,
-                       const double* __restrict__ bpow, int64_t N, int64_t F,
-                       long long* __restrict__ gbuf, int* __restrict__ order,
+// ---- K7b: cross-bin alignment through the Gram matrix of the centred masks.
+// With D_f = N b_f - k_f (b_f the bin's 0/1 labels, k_f their count), every
+// correlation the reference evaluates is a signed sum of
+//   Gram[f][h] = D_f . D_h = N^2 popc(b_f & b_h) - N k_f k_h   (exact, int64),
+// so the running profile g = sum_h s_h D_h is tracked through
+// hv[f] = D_f . g: a greedy step or a refinement flip of bin f updates hv
+// with one Gram row (O(F) parallel work), and each decision is the sign of
+// an exact integer — the same decisions as evaluating the dot products
+// directly.
+
+// labels (G, N) bytes -> bits (G, NW) words
+__global__ void masks_pack_kernel(const uint8_t* __restrict__ lab, unsigned long long* __restrict__ bits,
+                                  int64_t G, int64_t N, int64_t NW) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= G * NW) return;
+  const int64_t g = t / NW, w = t - g * NW;
+  const uint8_t* l = lab + g * N + w * 64;
+  const int64_t nb = min((int64_t)64, N - w * 64);
+  unsigned long long x = 0;
+  for (int64_t i = 0; i < nb; ++i) x |= (unsigned long long)(l[i] & 1) << i;
+  bits[t] = x;
+}
+
+// Gram[m][f][h] for one 32 x 32 tile of (f, h) per CTA (bit rows staged in
+// shared memory in chunks of words)
+constexpr int kGramWords = 32;
+__global__ void __launch_bounds__(1024)
+    masks_gram_kernel(const unsigned long long* __restrict__ bits, const int* __restrict__ cnt,
+                      int64_t F, int64_t N, int64_t NW, long long* __restrict__ gram) {
+  __shared__ unsigned long long ra[32][kGramWords + 1], rb[32][kGramWords + 1];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t tiles = (F + 31) / 32;
+  const int64_t m = blockIdx.z;
+  const int64_t f = blockIdx.y * 32 + ty, h = blockIdx.x * 32 + tx;
+  const unsigned long long* B = bits + m * F * NW;
+  long long c = 0;
+  for (int64_t w0 = 0; w0 < NW; w0 += kGramWords) {
+    // stage rows f0..f0+31 and h0..h0+31, words w0..w0+31
+    const int64_t fr = blockIdx.y * 32 + ty, hr = blockIdx.x * 32 + ty;
+    const int64_t w = w0 + tx;
+    ra[ty][tx] = (fr < F && w < NW) ? B[fr * NW + w] : 0ull;
+    rb[ty][tx] = (hr < F && w < NW) ? B[hr * NW + w] : 0ull;
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < kGramWords; ++k) c += __popcll(ra[ty][k] & rb[tx][k]);
+    __syncthreads();
+  }
+  (void)tiles;
+  if (f < F && h < F) {
+    const long long NN = (long long)N;
+    const int* K = cnt + m * F;
+    gram[(m * F + f) * F + h] = NN * NN * c - NN * (long long)K[f] * (long long)K[h];
+  }
+}
+
+// one CTA per mixture: order, greedy pass, refinement sweeps (:117-137)
+constexpr int kAlignT = 1024;
+__global__ void __launch_bounds__(kAlignT)
+    masks_align_kernel(const long long* __restrict__ gram, const double* __restrict__ bpow,
+                       int64_t F, int* __restrict__ order, long long* __restrict__ hbuf,
                        uint8_t* __restrict__ flip) {
-  __shared__ long long red[kAW];
   __shared__ int sflip;
   const int tid = threadIdx.x;
   const int64_t m = blockIdx.x;
-  const uint8_t* L = lab + m * F * N;
-  const int* K = cnt + m * F;
+  const long long* Gm = gram + m * F * F;
   const double* P = bpow + m * F;
-  long long* gv = gbuf + m * N;
   int* ord = order + m * F;
+  long long* hv = hbuf + m * F;
   uint8_t* fl = flip + m * F;
   // decreasing bin power, ties by index (stable)
-  for (int64_t f = tid; f < F; f += kAT) {
+  for (int64_t f = tid; f < F; f += kAlignT) {
     int64_t r = 0;
     const double pf = P[f];
     for (int64_t h = 0; h < F; ++h) r += (P[h] > pf) || (P[h] == pf && h < f);
@@ -333,52 +397,48 @@ __global__ void __launch_bounds__(kAT)
     fl[f] = 0;
   }
   __syncthreads();
-  const long long NN = (long long)N;
-  auto D = [&](int64_t f, int64_t n) -> long long { return NN * L[f * N + n] - K[f]; };
+  // greedy: g = D_{o0}; bin o_i flips when D . g < 0, then g += +-D
   {
     const int64_t f0 = ord[0];
-    for (int64_t n = tid; n < N; n += kAT) gv[n] = D(f0, n);
+    for (int64_t f = tid; f < F; f += kAlignT) hv[f] = Gm[f0 * F + f];  // Gram symmetric
   }
   __syncthreads();
-  // greedy pass (initializers.py:125-129)
 #pragma unroll 1
   for (int64_t i = 1; i < F; ++i) {
     const int64_t f = ord[i];
-    long long part = 0;
-    for (int64_t n = tid; n < N; n += kAT) part += D(f, n) * gv[n];
-    const long long dot = block_sum_i64<kAW>(part, red);
-    const bool neg = dot < 0;
-    if (tid == 0 && neg) fl[f] = 1;
-    for (int64_t n = tid; n < N; n += kAT) gv[n] += neg ? -D(f, n) : D(f, n);
+    const bool neg = hv[f] < 0;
+    __syncthreads();  // everyone read hv[f] before it changes
+    const long long* row = Gm + f * F;
+    if (neg) {
+      if (tid == 0) fl[f] = 1;
+      for (int64_t h = tid; h < F; h += kAlignT) hv[h] -= row[h];
+    } else {
+      for (int64_t h = tid; h < F; h += kAlignT) hv[h] += row[h];
+    }
     __syncthreads();
   }
-  // refinement sweeps (initializers.py:130-137)
+  // refinement: g = sum_h s_h D_h; flip f when s_f hv[f] - Gram[f][f] < 0
 #pragma unroll 1
   for (int sweep = 0; sweep < 5; ++sweep) {
-    for (int64_t n = tid; n < N; n += kAT) {
-      long long s = 0;
-      for (int64_t f = 0; f < F; ++f) s += fl[f] ? -D(f, n) : D(f, n);
-      gv[n] = s;
+    for (int64_t f = tid; f < F; f += kAlignT) {
+      long long acc = 0;
+      const long long* row = Gm + f * F;
+      for (int64_t h = 0; h < F; ++h) acc += fl[h] ? -row[h] : row[h];
+      hv[f] = acc;
     }
     if (tid == 0) sflip = 0;
     __syncthreads();
 #pragma unroll 1
     for (int64_t i = 0; i < F; ++i) {
       const int64_t f = ord[i];
-      const bool fi = fl[f] != 0;
-      long long part = 0;
-      for (int64_t n = tid; n < N; n += kAT) {
-        const long long d = fi ? -D(f, n) : D(f, n);
-        part += d * (gv[n] - d);
-      }
-      const long long dot = block_sum_i64<kAW>(part, red);
-      if (dot < 0) {
-        for (int64_t n = tid; n < N; n += kAT) {
-          const long long d = fi ? -D(f, n) : D(f, n);
-          gv[n] -= 2 * d;
-        }
+      const long long sgn = fl[f] ? -1 : 1;
+      const bool go = sgn * hv[f] - Gm[f * F + f] < 0;
+      __syncthreads();
+      if (go) {  // g -= 2 s D_f
+        const long long* row = Gm + f * F;
+        for (int64_t h = tid; h < F; h += kAlignT) hv[h] -= 2 * sgn * row[h];
         if (tid == 0) {
-          fl[f] = fi ? 0 : 1;
+          fl[f] = fl[f] ? 0 : 1;
           sflip = 1;
         }
       }
@@ -423,7 +483,9 @@ struct MaskWs {
   double2* zs;
   double* fpow;
   double* bpow;
-  long long* gbuf;
+  long long* gram;
+  long long* hbuf;
+  unsigned long long* bits;
   int* cnt;
   int* order;
   uint8_t* lab;
@@ -443,13 +505,23 @@ MaskWs carve_masks(void* base, int64_t M, int64_t N, int64_t F, int I) {
   w.zs = (double2*)take((size_t)G * N * I * sizeof(double2));
   w.fpow = (double*)take((size_t)G * N * sizeof(double));
   w.bpow = (double*)take((size_t)G * sizeof(double));
-  w.gbuf = (long long*)take((size_t)M * N * sizeof(long long));
+  const int64_t NW = (N + 63) / 64;
+  w.gram = (long long*)take((size_t)M * F * F * sizeof(long long));
+  w.hbuf = (long long*)take((size_t)G * sizeof(long long));
+  w.bits = (unsigned long long*)take((size_t)G * NW * sizeof(unsigned long long));
   w.cnt = (int*)take((size_t)G * sizeof(int));
   w.order = (int*)take((size_t)G * sizeof(int));
   w.lab = (uint8_t*)take((size_t)G * N);
   w.flip = (uint8_t*)take((size_t)G);
   w.bytes = off;
   return w;
+}
+
+// a failing step is named on stderr when FFCA_DEBUG_SYNC is set
+int masks_fail(const char* step, cudaError_t e) {
+  if (getenv("FFCA_DEBUG_SYNC"))
+    fprintf(stderr, "ffca_init_masks: %s: %s\n", step, cudaGetErrorString(e));
+  return FFCA_ERR_CUDA;
 }
 
 }  // namespace
@@ -477,14 +549,20 @@ int ffca_init_masks(const double* y, double* v, double* S, double* v_floor, int6
   if (w.bytes > workspace_bytes) return FFCA_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = launch_init_powers(y, v, v_floor, M, N, F, I, FFCA_C128, s);  // floor
-  if (e != cudaSuccess) return FFCA_ERR_CUDA;
+  if (e != cudaSuccess) return masks_fail("init_powers", e);
   const double2* y2 = (const double2*)y;
   double2* S2 = (double2*)S;
+  const size_t zsmem = mask_smem(N, I);
   switch (I) {
 #define FFCA_MASK_CASE(II)                                                                  \
   case II:                                                                                  \
-    masks_bin_kernel<II><<<(unsigned)(M * F), kMT, 0, s>>>(y2, N, F, w.zs, w.lab, w.fpow,   \
-                                                           w.bpow, w.cnt, S2);              \
+    if (zsmem > 0 &&                                                                        \
+        (e = cudaFuncSetAttribute(masks_bin_kernel<II, kMTLarge>,                           \
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,              \
+                                  (int)zsmem)) != cudaSuccess)                              \
+      return masks_fail("bin kernel smem attribute", e);                                    \
+    masks_bin_kernel<II, kMTLarge><<<(unsigned)(M * F), kMTLarge, zsmem, s>>>(              \
+        y2, N, F, w.zs, w.lab, w.fpow, w.bpow, w.cnt, S2);                                  \
     break;
     FFCA_MASK_CASE(1)
     FFCA_MASK_CASE(2)
@@ -498,10 +576,17 @@ int ffca_init_masks(const double* y, double* v, double* S, double* v_floor, int6
     default:
       return FFCA_ERR_INVALID;
   }
-  if (cudaGetLastError() != cudaSuccess) return FFCA_ERR_CUDA;
-  masks_align_kernel<<<(unsigned)M, kAT, 0, s>>>(w.lab, w.cnt, w.bpow, N, F, w.gbuf, w.order,
-                                                 w.flip);
-  if (cudaGetLastError() != cudaSuccess) return FFCA_ERR_CUDA;
+  if ((e = cudaGetLastError()) != cudaSuccess) return masks_fail("bin kernel", e);
+  {
+    const int64_t NW = (N + 63) / 64;
+    const int64_t G = M * F;
+    masks_pack_kernel<<<(unsigned)((G * NW + 255) / 256), 256, 0, s>>>(w.lab, w.bits, G, N, NW);
+    const unsigned t = (unsigned)((F + 31) / 32);
+    masks_gram_kernel<<<dim3(t, t, (unsigned)M), 1024, 0, s>>>(w.bits, w.cnt, F, N, NW, w.gram);
+    masks_align_kernel<<<(unsigned)M, kAlignT, 0, s>>>(w.gram, w.bpow, F, w.order, w.hbuf,
+                                                       w.flip);
+    if ((e = cudaGetLastError()) != cudaSuccess) return masks_fail("alignment", e);
+  }
   const int64_t total = M * N * F;
   const unsigned nb = (unsigned)((total + 255) / 256);
   switch (I) {

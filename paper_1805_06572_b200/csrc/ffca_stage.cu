@@ -13,36 +13,50 @@ inline unsigned nb(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 }  // namespace
 
 // ---- init_random powers (initializers.py:29-31, modelops.py:12-21) ---------
+// One CTA per tile of 32 bins: lane = bin (coalesced rows of y and v), the 32
+// warps take interleaved frame slices; per-bin frame sums are combined over
+// the warps in a fixed order (deterministic), floor = 1e-10 * mean_n ||y||^2 / I,
+// then v = max(||y||^2 / (2I), floor) for both sources.
+constexpr int kPowWarps = 32;
 template <int I, typename R>
-__global__ void init_powers_kernel(const void* y_, void* v_, double* floor, int64_t M, int64_t N,
-                                   int64_t F) {
+__global__ void __launch_bounds__(kPowWarps * 32)
+    init_powers_kernel(const void* y_, void* v_, double* floor, int64_t M, int64_t N, int64_t F) {
   using C = typename CplxOf<R>::type;
-  // one warp-slice per bin: floor = 1e-10 * mean_n ||y||^2 / I; then v
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= M * F) return;
-  const int64_t m = g / F, f = g - m * F;
-  const C* y = (const C*)y_ + (m * N * F + f) * I;
+  __shared__ double part[kPowWarps][32];
+  __shared__ double sfl[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t tiles = (F + 31) / 32;
+  const int64_t m = blockIdx.x / tiles;
+  const int64_t f = (blockIdx.x - m * tiles) * 32 + lane;
+  const bool act = f < F;
+  const C* y = (const C*)y_ + (m * N * F + (act ? f : 0)) * I;
   R* v = (R*)v_ + m * 2 * N * F + f;
+  auto power = [&](int64_t n) {
+    double p = 0.0;
+#pragma unroll
+    for (int a = 0; a < I; ++a) {
+      const double2 x = to_c128(y[n * F * I + a]);
+      p += x.x * x.x + x.y * x.y;
+    }
+    return p;
+  };
   double s = 0.0;
-  for (int64_t n = 0; n < N; ++n) {
-    double p = 0.0;
-#pragma unroll
-    for (int a = 0; a < I; ++a) {
-      const double2 x = to_c128(y[n * F * I + a]);
-      p += x.x * x.x + x.y * x.y;
-    }
-    s += p;
+  if (act)
+    for (int64_t n = warp; n < N; n += kPowWarps) s += power(n);
+  part[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kPowWarps; ++w) t += part[w][lane];
+    const double fl = 1e-10 * (t / (double)N) / I;
+    sfl[lane] = fl;
+    if (act) floor[m * F + f] = fl;
   }
-  const double fl = 1e-10 * (s / (double)N) / I;
-  floor[g] = fl;
-  for (int64_t n = 0; n < N; ++n) {
-    double p = 0.0;
-#pragma unroll
-    for (int a = 0; a < I; ++a) {
-      const double2 x = to_c128(y[n * F * I + a]);
-      p += x.x * x.x + x.y * x.y;
-    }
-    const double q = p / (2.0 * I);
+  __syncthreads();
+  if (!act) return;
+  const double fl = sfl[lane];
+  for (int64_t n = warp; n < N; n += kPowWarps) {
+    const double q = power(n) / (2.0 * I);
     const double w = q < fl ? fl : q;
     v[n * F] = (R)w;
     v[N * F + n * F] = (R)w;
@@ -51,12 +65,13 @@ __global__ void init_powers_kernel(const void* y_, void* v_, double* floor, int6
 
 cudaError_t launch_init_powers(const void* y, void* v, double* floor, int64_t M, int64_t N,
                                int64_t F, int I, int dtype, cudaStream_t s) {
+  const unsigned grid = (unsigned)(M * ((F + 31) / 32));
 #define FFCA_CASE(II)                                                                       \
   case II:                                                                                  \
     if (dtype == FFCA_C64)                                                                  \
-      init_powers_kernel<II, float><<<nb(M * F, 128), 128, 0, s>>>(y, v, floor, M, N, F);   \
+      init_powers_kernel<II, float><<<grid, kPowWarps * 32, 0, s>>>(y, v, floor, M, N, F);  \
     else                                                                                    \
-      init_powers_kernel<II, double><<<nb(M * F, 128), 128, 0, s>>>(y, v, floor, M, N, F);  \
+      init_powers_kernel<II, double><<<grid, kPowWarps * 32, 0, s>>>(y, v, floor, M, N, F); \
     break;
   switch (I) {
     FFCA_CASE(1)
