@@ -284,10 +284,11 @@ cudaError_t launch_initial_par(const double2* S0, double2* P, double2* W, double
                                double* logdet2, int64_t G, int64_t F, int I, ffca_status_dev* st,
                                cudaStream_t s);
 
-// Which per-bin kernel: the lane-parallel one (ffca_pencil_par.cu) wins when
-// bins are few (latency-bound) and for I >= 5 (no register spills); the
-// one-thread-per-bin kernel keeps more bins in flight for big batches.
-// FFCA_K1=par|thread overrides (experiments).
+// Which per-bin kernel: the lane-parallel one (ffca_pencil_par.cu) for
+// I >= 5 (no register spills) and for I = 4 with few bins (latency bound:
+// config 4, 46 vs 65 us); the one-thread-per-bin kernel for I <= 3 at any
+// size (configs 0/1: 0.28 vs 0.34 ms and 2.25 vs 2.66 ms per run) and for
+// big I = 4 batches. FFCA_K1=par|thread overrides (experiments).
 static bool use_par(int64_t G, int I) {
   static int mode = -1;
   if (mode < 0) {
@@ -296,7 +297,7 @@ static bool use_par(int64_t G, int I) {
   }
   if (mode == 1) return true;
   if (mode == 2) return I >= 5;
-  return I >= 5 || G < 16384;
+  return I >= 5 || (I == 4 && G < 16384);
 }
 
 cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s) {
