@@ -237,10 +237,10 @@ def main():
             "S": torch.empty((M, 2, F, I, I), dtype=torch.complex128, device=dev),
             "v": torch.empty_like(v_d)}
 
-    def step(timing=False):
+    def step(timing=False):  # untimed-event steps replay a cached CUDA graph of the run
         return run_device(args.engine, y_d, v_d, S_d, fl_d, L, likelihood=False, history=False,
                           images=True, dtype=args.dtype, timing=timing, check=False,
-                          chunk_frames=cf, kernel_timing=timing, out=bufs)
+                          chunk_frames=cf, kernel_timing=timing, out=bufs, graph=not timing)
 
     bufs["workspace"] = step().workspace
     nstreams = args.streams if M > 1 else 1
@@ -264,7 +264,7 @@ def main():
             return run_device_streams(args.engine, y_d, v_d, S_d, fl_d, L, nstreams=nstreams,
                                       out=bufs, workspaces=wss, likelihood=False, history=False,
                                       images=True, dtype=args.dtype, timing=False, check=False,
-                                      chunk_frames=cf, streams=sstreams)
+                                      chunk_frames=cf, streams=sstreams, graph=True)
 
     for _ in range(args.warmup):
         step()

@@ -47,14 +47,17 @@ class DeviceRun:
 
 def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, history=False,
                images=True, dtype="c128", timing=True, check=True, out=None, chunk_frames=0,
-               kernel_timing=False):
+               kernel_timing=False, graph=False):
     """Run ``iterations`` EM passes of FastFCA (``algorithm='fast'``) or
     conventional FCA (``'fca'``) entirely on the current CUDA stream.
 
     y (M,N,F,I) complex, v0 (M,2,N,F) real, S0 (M,2,F,I,I) complex128,
     v_floor (M,F) float64 — CUDA tensors (moved if not). ``v0`` is not
     modified. With ``check`` the stream is synchronised and numerical
-    failures are raised as the reference's exceptions.
+    failures are raised as the reference's exceptions. ``graph`` replays a
+    cached CUDA graph of the whole run when the arguments (buffers, sizes,
+    flags) repeat — for repeated runs on preallocated ``out`` buffers; it is
+    ignored when ``timing`` / ``kernel_timing`` events are requested.
     """
     lib = D.require()
     torch = D.torch
@@ -101,6 +104,8 @@ def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, hi
         flags |= _lib.FLAG_HISTORY
     if images:
         flags |= _lib.FLAG_IMAGES
+    if graph:
+        flags |= _lib.FLAG_GRAPH
     fast = algorithm == "fast"
     wsz = (lib.ffca_fastfca_workspace_size if fast else lib.ffca_fca_workspace_size)(
         M, N, F, I, L, flags, int(chunk_frames))

@@ -31,6 +31,7 @@ FFCA_C64 = 1
 FLAG_LIKELIHOOD = 1
 FLAG_HISTORY = 2
 FLAG_IMAGES = 4
+FLAG_GRAPH = 8
 
 c_i64 = ctypes.c_int64
 c_int = ctypes.c_int
@@ -69,6 +70,7 @@ SIGNATURES = [
     ("ffca_fastfca_run", c_int, [ctypes.POINTER(RunArgs), c_vp]),
     ("ffca_fca_workspace_size", c_sz, [c_i64, c_i64, c_i64, c_int, c_int, ctypes.c_uint, c_i64]),
     ("ffca_fca_run", c_int, [ctypes.POINTER(RunArgs), c_vp]),
+    ("ffca_graph_cache_clear", c_int, []),
     ("ffca_run_status", c_int, [c_vp, c_vp, ctypes.POINTER(Status)]),
     ("ffca_status_reset", c_int, [c_vp, c_vp]),
     ("ffca_status_read", c_int, [c_vp, c_vp, ctypes.POINTER(Status)]),

@@ -170,6 +170,39 @@ def test_multistream_run_equals_single_stream_run():
     assert len(ms.parts) == 3
 
 
+@pytest.mark.parametrize("algorithm", ["fast", "fca"])
+def test_graph_replay_equals_stream_launches(algorithm):
+    """FFCA_FLAG_GRAPH: the cached CUDA graph of a run replays bitwise the
+    same results, also with the likelihood trace, and picks up new inputs
+    written into the same buffers."""
+    import torch
+
+    from paper_1805_06572_b200._engine import run_device
+
+    P = _pkg()
+    gen = np.random.default_rng(23)
+    Y = torch.from_numpy(random_complex(gen, (2, 70, 11, 3))).cuda()
+    inits = [P.init_random(Y[m], 60 + m) for m in range(2)]
+    V = torch.stack([i.v for i in inits])
+    S = torch.stack([i.S for i in inits])
+    FL = torch.stack([i.v_floor for i in inits])
+    ref = run_device(algorithm, Y, V, S, FL, 4, likelihood=True, timing=False)
+    out = {"images": torch.empty_like(ref.images), "S": torch.empty_like(ref.S),
+           "v": torch.empty_like(ref.v), "loglik": torch.empty_like(ref.loglik)}
+    for _ in range(3):  # capture, then two replays
+        r = run_device(algorithm, Y, V, S, FL, 4, likelihood=True, timing=False, out=out,
+                       graph=True)
+        out["workspace"] = r.workspace
+        for k in ("images", "S", "v", "loglik"):
+            assert torch.equal(getattr(r, k), getattr(ref, k)), k
+    Y2 = Y.clone()
+    Y2 *= 1.5  # new data in a new buffer: a different graph; same buffer: replay sees it
+    ref2 = run_device(algorithm, Y2, V, S, FL, 4, likelihood=True, timing=False)
+    Y.copy_(Y2)
+    r = run_device(algorithm, Y, V, S, FL, 4, likelihood=True, timing=False, out=out, graph=True)
+    assert torch.equal(r.images, ref2.images) and torch.equal(r.loglik, ref2.loglik)
+
+
 def test_mismatched_output_buffers_are_rejected():
     import torch
 
