@@ -413,6 +413,9 @@ __global__ void __launch_bounds__(64)
     double s[NP];
 #pragma unroll
     for (int e = 0; e < NP; ++e) s[e] = 0.0;
+    // unrolled: the loads of several chunks are in flight together; the adds
+    // keep the chunk order (bitwise identical sums)
+#pragma unroll 4
     for (int c = 0; c < nchunk; ++c) {
       const double* sp = Spart + (size_t)c * 2 * NP * G + (size_t)j * NP * G + g;
 #pragma unroll

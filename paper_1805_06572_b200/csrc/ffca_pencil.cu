@@ -28,6 +28,9 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
     double s[2][NP];
 #pragma unroll
     for (int e = 0; e < NP; ++e) s[0][e] = s[1][e] = 0.0;
+    // unrolled: the loads of several chunks are in flight together; the adds
+    // keep the chunk order (bitwise identical sums)
+#pragma unroll 4
     for (int c = 0; c < p.nchunk; ++c) {
       const double* sp = p.Spart + (size_t)c * 2 * NP * G + g;
 #pragma unroll

@@ -406,6 +406,9 @@ __global__ void finalize_sraw_kernel(const double* Spart, int nchunk, int64_t N,
     double s[NP];
 #pragma unroll
     for (int e = 0; e < NP; ++e) s[e] = 0.0;
+    // unrolled: the loads of several chunks are in flight together; the adds
+    // keep the chunk order (bitwise identical sums)
+#pragma unroll 4
     for (int c = 0; c < nchunk; ++c)
 #pragma unroll
       for (int e = 0; e < NP; ++e) s[e] += Spart[((size_t)c * 2 * NP + j * NP + e) * F + g];
