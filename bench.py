@@ -308,18 +308,19 @@ def main():
     alg_bytes = bytes_per_tf * M * F * N
     achieved = alg_bytes / (k_avg / 1e3) / 1e9
     peak, peak_kind = peaks()
-    traffic = None
+    traffic, traffic_src = None, None
     try:  # dram read+write per launch from the committed ncu --set full capture
         tj = json.loads((REPO / "profiles" / "traffic.json").read_text())
         for k, rec in tj.items():
             if (args.engine == "fast" and args.dtype == "c128" and cfg.index == 3 and world == 1
                     and "config 3" in k and "c128" in k):
-                traffic = {"bytes_per_launch": rec["dram_bytes_per_launch"],
-                           "source": rec["source"]}
+                traffic = rec["dram_bytes_per_launch"]
+                traffic_src = rec["source"]
     except Exception:
-        traffic = None
+        traffic, traffic_src = None, None
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
+            "traffic_source": traffic_src, "algorithmic_bytes_per_launch": alg_bytes,
             "kernel": ("fast_em2_kernel (update pass)" if args.engine == "fast"
                        else "fca_em_kernel (update pass)"),
             "kernel_ms_avg": round(k_avg, 4), "launches_averaged": len(hot),
