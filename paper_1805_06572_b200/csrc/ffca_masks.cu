@@ -38,26 +38,84 @@ inline size_t mask_smem(int64_t N, int I) {
 constexpr int kKmeansIters = 50;
 constexpr double kMaskRidge = 1e-2;
 
-// sum of NV values over the CTA (warp shuffles, then warps in index order);
-// every thread receives the totals
-template <int NV, int W>
-FFCA_DEV void block_sum(double (&v)[NV], double* red) {
+constexpr int pow2ceil(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+constexpr int ilog2(int x) {
+  int l = 0;
+  while ((1 << l) < x) ++l;
+  return l;
+}
+struct NoFin {
+  FFCA_DEV double operator()(int, double s) const { return s; }
+};
+
+// Sum of NV <= 32 values over the CTA, every thread receiving fin(k, total_k).
+// Warp level: reduce-scatter (each butterfly step halves the values a lane
+// holds: P2-1 shuffles instead of 5 NV), then plain butterflies; CTA level:
+// thread k < NV adds the W warp partials in warp order and applies fin (e.g.
+// the centroid division, done once instead of by every thread); the totals
+// are broadcast through shared memory. Fixed order: deterministic.
+// red: >= W * 32 + 32 doubles.
+template <int NV, int W, typename Fin = NoFin>
+FFCA_DEV void block_sum(double (&v)[NV], double* red, Fin fin = Fin()) {
+  static_assert(NV >= 1 && NV <= 32, "block_sum handles up to 32 values per call");
+  constexpr int P2 = pow2ceil(NV), LP = ilog2(P2);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double h[P2];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    double x = v[k];
+  for (int k = 0; k < P2; ++k) h[k] = k < NV ? v[k] : 0.0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) red[warp * NV + k] = x;
+  for (int st = 0; st < LP; ++st) {
+    const int o = 16 >> st;
+    const int half = P2 >> (st + 1);
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < P2 / 2; ++k) {
+      if (k < half) {
+        const double send = upper ? h[k] : h[k + half];
+        const double keep = upper ? h[k + half] : h[k];
+        h[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16 >> LP; o > 0; o >>= 1) h[0] += __shfl_xor_sync(0xffffffffu, h[0], o);
+  const int j = LP ? (lane >> (5 - LP)) & (P2 - 1) : 0;
+  if ((lane & ((32 >> LP) - 1)) == 0 && j < NV) red[warp * P2 + j] = h[0];
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double t = 0.0;
+    for (int w = 0; w < W; ++w) t += red[w * P2 + threadIdx.x];
+    red[W * P2 + threadIdx.x] = fin((int)threadIdx.x, t);
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    double s = 0.0;
-    for (int w = 0; w < W; ++w) s += red[w * NV + k];
-    v[k] = s;
-  }
+  for (int k = 0; k < NV; ++k) v[k] = red[W * P2 + k];
   __syncthreads();
+}
+
+// more than 32 values: chunks of 32
+template <int NV, int W>
+FFCA_DEV void block_sum_wide(double (&v)[NV], double* red) {
+  if constexpr (NV <= 32) {
+    block_sum<NV, W>(v, red);
+  } else {
+    double a[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) a[k] = v[k];
+    block_sum<32, W>(a, red);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = a[k];
+    double b[NV - 32];
+#pragma unroll
+    for (int k = 0; k < NV - 32; ++k) b[k] = v[32 + k];
+    block_sum_wide<NV - 32, W>(b, red);
+#pragma unroll
+    for (int k = 0; k < NV - 32; ++k) v[32 + k] = b[k];
+  }
 }
 
 // (value, index, payload) with numpy argmax semantics: largest value, first
@@ -119,10 +177,10 @@ __global__ void __launch_bounds__(kMT)
                      double2* __restrict__ S) {
   constexpr int kMW = kMT / 32;
   constexpr int NE = I * (I + 1) / 2;  // upper-triangle entries of a covariance
-  constexpr int NR = 4 * I > 2 * NE ? 4 * I : 2 * NE;
-  __shared__ double red[kMW * (NR > 16 ? NR : 16)];
+  __shared__ double red[kMW * 32 + 32];
   __shared__ double rv[kMW];
   __shared__ int ri[2 * kMW];
+  __shared__ int ired[2 * kMW];
   const int tid = threadIdx.x;
   const int64_t g = blockIdx.x;
   const int64_t m = g / F, f = g - m * F;
@@ -208,26 +266,42 @@ __global__ void __launch_bounds__(kMT)
   long long count0 = 0;
 #pragma unroll 1
   for (int it = 0; it < kKmeansIters; ++it) {
-    double acc[2];  // count of label 1, number of changed labels
-    acc[0] = acc[1] = 0.0;
-    ArgMax worst{-1.0, 0x7fffffff, 0};
+    // labels with the current centroids; counts by warp REDUX + one smem stage
+    int cnt = 0, chg = 0;
 #pragma unroll 4
     for (int n = tid; n < Ni; n += kMT) {
       const double d0 = dist2<I>(zb + (size_t)n * I, c0);
       const double d1 = dist2<I>(zb + (size_t)n * I, c1);
       const int nw = d0 <= d1 ? 1 : 0;
-      const int old = lb[n];
-      acc[0] += nw;
-      acc[1] += (nw != old);
-      lb[n] = (uint8_t)nw;
-      ArgMax c{nw ? d0 : d1, (int)n, nw | (old << 1)};
-      if (better(c, worst)) worst = c;
+      const int old = lb[n] & 1;
+      cnt += nw;
+      chg += (nw != old);
+      lb[n] = (uint8_t)(nw | (old << 1));  // bit 0: label, bit 1: previous label
     }
-    block_sum<2, kMW>(acc, red);
-    worst = block_argmax<kMW>(worst, rv, ri);
-    count0 = (long long)acc[0];
-    long long changed = (long long)acc[1];
+    cnt = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
+    chg = (int)__reduce_add_sync(0xffffffffu, (unsigned)chg);
+    if ((tid & 31) == 0) {
+      ired[tid >> 5] = cnt;
+      ired[kMW + (tid >> 5)] = chg;
+    }
+    __syncthreads();
+    count0 = 0;
+    long long changed = 0;
+#pragma unroll
+    for (int w = 0; w < kMW; ++w) {
+      count0 += ired[w];
+      changed += ired[kMW + w];
+    }
     if (count0 == 0 || count0 == N) {  // re-seed the empty cluster with the worst fit
+      ArgMax worst{-1.0, 0x7fffffff, 0};
+      for (int n = tid; n < Ni; n += kMT) {  // rare: recompute the fits
+        const double d0 = dist2<I>(zb + (size_t)n * I, c0);
+        const double d1 = dist2<I>(zb + (size_t)n * I, c1);
+        const int nw = lb[n] & 1;
+        ArgMax c{nw ? d0 : d1, n, lb[n]};
+        if (better(c, worst)) worst = c;
+      }
+      worst = block_argmax<kMW>(worst, rv, ri);
       const int nw = worst.pay & 1, old = (worst.pay >> 1) & 1;
       if (tid == 0) lb[worst.i] = (uint8_t)(1 - nw);
       count0 += nw ? -1 : 1;
@@ -241,7 +315,7 @@ __global__ void __launch_bounds__(kMT)
     for (int k = 0; k < 4 * I; ++k) s[k] = 0.0;
 #pragma unroll 4
     for (int n = tid; n < Ni; n += kMT) {
-      const int l = lb[n];
+      const int l = lb[n] & 1;
 #pragma unroll
       for (int a = 0; a < I; ++a) {
         const double2 z = zb[(size_t)n * I + a];
@@ -254,17 +328,18 @@ __global__ void __launch_bounds__(kMT)
         }
       }
     }
-    block_sum<4 * I, kMW>(s, red);
     const double n0 = (double)count0, n1 = (double)(N - count0);
+    // centroids = group sums / group sizes (the division done once per value)
+    block_sum<4 * I, kMW>(s, red, [=](int k, double t) { return t / (k < 2 * I ? n0 : n1); });
 #pragma unroll
     for (int a = 0; a < I; ++a) {
-      c0[a] = make_double2(s[2 * a] / n0, s[2 * a + 1] / n0);
-      c1[a] = make_double2(s[2 * I + 2 * a] / n1, s[2 * I + 2 * a + 1] / n1);
+      c0[a] = make_double2(s[2 * a], s[2 * a + 1]);
+      c1[a] = make_double2(s[2 * I + 2 * a], s[2 * I + 2 * a + 1]);
     }
   }
   if (tid == 0) cnt[g] = (int)count0;
   if (in_smem)
-    for (int n = tid; n < Ni; n += kMT) lb_out[n] = lb[n];
+    for (int n = tid; n < Ni; n += kMT) lb_out[n] = lb[n] & 1;
 
   // 4. group covariances sum w w^H / |group|, unit trace, + ridge (:108-115)
 #pragma unroll 1
@@ -275,7 +350,7 @@ __global__ void __launch_bounds__(kMT)
 #pragma unroll
     for (int k = 0; k < 2 * NE; ++k) s[k] = 0.0;
     for (int n = tid; n < Ni; n += kMT) {
-      if (lb[n] != want) continue;
+      if ((lb[n] & 1) != want) continue;
       double2 w[I];
 #pragma unroll
       for (int a = 0; a < I; ++a) w[a] = yb[n * FI + a];
@@ -288,7 +363,7 @@ __global__ void __launch_bounds__(kMT)
           s[2 * e + 1] += w[a].y * w[b].x - w[a].x * w[b].y;
         }
     }
-    block_sum<2 * NE, kMW>(s, red);
+    block_sum_wide<2 * NE, kMW>(s, red);
     double2* Sd = S + ((m * 2 + j) * F + f) * I * I;
     if (tid == 0) {
       double tr = 0.0;
