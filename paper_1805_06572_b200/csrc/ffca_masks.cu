@@ -154,22 +154,7 @@ FFCA_DEV ArgMax block_argmax(ArgMax a, double* rv, int* ri) {
   return r;
 }
 
-FFCA_DEV bool mask_smem_dev(int64_t N, int I) {
-  return (size_t)N * I * 16 + (size_t)N <= kMaskSmemBytes;
-}
-
-template <int I>
-FFCA_DEV double dist2(const double2* z, const double2 (&c)[I]) {
-  double d = 0.0;
-#pragma unroll
-  for (int a = 0; a < I; ++a) {
-    const double2 e = make_double2(z[a].x - c[a].x, z[a].y - c[a].y);
-    d += e.x * e.x + e.y * e.y;
-  }
-  return d;
-}
-
-template <int I, int kMT>
+template <int I, int kMT, bool SM>
 __global__ void __launch_bounds__(kMT)
     masks_bin_kernel(const double2* __restrict__ y, int64_t N, int64_t F,
                      double2* __restrict__ zs, uint8_t* __restrict__ lab,
@@ -187,12 +172,33 @@ __global__ void __launch_bounds__(kMT)
   const double2* yb = y + (m * N * F + f) * I;
   const int64_t FI = F * I;
   extern __shared__ __align__(16) unsigned char zsm[];
-  const bool in_smem = mask_smem_dev(N, I);
-  double2* zb = in_smem ? (double2*)zsm : zs + g * N * I;
+  const int Ni = (int)N;  // N < 2^31 (checked by the caller)
+  // SM: z and the labels live in shared memory (compile-time, so the loads
+  // are LDS, not generic), channel-major ([a][n]: consecutive frames are
+  // consecutive 16-B words, bank-conflict free); otherwise z is frame-major
+  // in the workspace (one contiguous 16 I-byte row per frame)
+  constexpr bool in_smem = SM;
+  double2* zb = SM ? (double2*)zsm : zs + g * N * I;
+  // element (a, n) of z; shared-memory indices fit 32 bits
+  auto zat = [&](int a, int n) -> double2& {
+    if constexpr (SM)
+      return zb[a * Ni + n];
+    else
+      return zb[(size_t)n * I + a];
+  };
+  auto zdist = [&](int n, const double2(&c)[I]) {
+    double d = 0.0;
+#pragma unroll
+    for (int a = 0; a < I; ++a) {
+      const double2 za = zat(a, n);
+      const double2 e = make_double2(za.x - c[a].x, za.y - c[a].y);
+      d += e.x * e.x + e.y * e.y;
+    }
+    return d;
+  };
   uint8_t* lb_out = lab + g * N;
   uint8_t* lb = in_smem ? zsm + (size_t)N * I * 16 : lb_out;
   double* pb = fpow + g * N;
-  const int Ni = (int)N;  // N < 2^31 (checked by the caller)
 
   // 1. channel energies (reference channel) and frame powers
   double E[I];
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(kMT)
 #pragma unroll
     for (int a = 0; a < I; ++a) {
       const double2 t = z[a];
-      zb[(size_t)n * I + a] = make_double2(t.x * ph.x + t.y * ph.y, t.y * ph.x - t.x * ph.y);
+      zat(a, n) = make_double2(t.x * ph.x + t.y * ph.y, t.y * ph.x - t.x * ph.y);
     }
     ArgMax c{p, (int)n, 0};
     if (better(c, best)) best = c;
@@ -250,17 +256,17 @@ __global__ void __launch_bounds__(kMT)
   __syncthreads();  // z visible to the CTA
   double2 c0[I], c1[I];
 #pragma unroll
-  for (int a = 0; a < I; ++a) c0[a] = zb[(int64_t)best.i * I + a];
+  for (int a = 0; a < I; ++a) c0[a] = zat(a, best.i);
   // farthest frame from c0 seeds cluster 1
   ArgMax far{-1.0, 0x7fffffff, 0};
   for (int n = tid; n < Ni; n += kMT) {
-    ArgMax c{dist2<I>(zb + (size_t)n * I, c0), (int)n, 0};
+    ArgMax c{zdist(n, c0), (int)n, 0};
     if (better(c, far)) far = c;
     lb[n] = 0;
   }
   far = block_argmax<kMW>(far, rv, ri);
 #pragma unroll
-  for (int a = 0; a < I; ++a) c1[a] = zb[(int64_t)far.i * I + a];
+  for (int a = 0; a < I; ++a) c1[a] = zat(a, far.i);
 
   // 3. 2-means (_two_means, initializers.py:42-68); label 1 = cluster 0
   long long count0 = 0;
@@ -270,8 +276,8 @@ __global__ void __launch_bounds__(kMT)
     int cnt = 0, chg = 0;
 #pragma unroll 4
     for (int n = tid; n < Ni; n += kMT) {
-      const double d0 = dist2<I>(zb + (size_t)n * I, c0);
-      const double d1 = dist2<I>(zb + (size_t)n * I, c1);
+      const double d0 = zdist(n, c0);
+      const double d1 = zdist(n, c1);
       const int nw = d0 <= d1 ? 1 : 0;
       const int old = lb[n] & 1;
       cnt += nw;
@@ -295,8 +301,8 @@ __global__ void __launch_bounds__(kMT)
     if (count0 == 0 || count0 == N) {  // re-seed the empty cluster with the worst fit
       ArgMax worst{-1.0, 0x7fffffff, 0};
       for (int n = tid; n < Ni; n += kMT) {  // rare: recompute the fits
-        const double d0 = dist2<I>(zb + (size_t)n * I, c0);
-        const double d1 = dist2<I>(zb + (size_t)n * I, c1);
+        const double d0 = zdist(n, c0);
+        const double d1 = zdist(n, c1);
         const int nw = lb[n] & 1;
         ArgMax c{nw ? d0 : d1, n, lb[n]};
         if (better(c, worst)) worst = c;
@@ -318,7 +324,7 @@ __global__ void __launch_bounds__(kMT)
       const int l = lb[n] & 1;
 #pragma unroll
       for (int a = 0; a < I; ++a) {
-        const double2 z = zb[(size_t)n * I + a];
+        const double2 z = zat(a, n);
         if (l) {
           s[2 * a] += z.x;
           s[2 * a + 1] += z.y;
@@ -631,13 +637,17 @@ int ffca_init_masks(const double* y, double* v, double* S, double* v_floor, int6
   switch (I) {
 #define FFCA_MASK_CASE(II)                                                                  \
   case II:                                                                                  \
-    if (zsmem > 0 &&                                                                        \
-        (e = cudaFuncSetAttribute(masks_bin_kernel<II, kMTLarge>,                           \
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,              \
-                                  (int)zsmem)) != cudaSuccess)                              \
-      return masks_fail("bin kernel smem attribute", e);                                    \
-    masks_bin_kernel<II, kMTLarge><<<(unsigned)(M * F), kMTLarge, zsmem, s>>>(              \
-        y2, N, F, w.zs, w.lab, w.fpow, w.bpow, w.cnt, S2);                                  \
+    if (zsmem > 0) {                                                                        \
+      if ((e = cudaFuncSetAttribute(masks_bin_kernel<II, kMTLarge, true>,                   \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,            \
+                                    (int)zsmem)) != cudaSuccess)                            \
+        return masks_fail("bin kernel smem attribute", e);                                  \
+      masks_bin_kernel<II, kMTLarge, true><<<(unsigned)(M * F), kMTLarge, zsmem, s>>>(      \
+          y2, N, F, w.zs, w.lab, w.fpow, w.bpow, w.cnt, S2);                                \
+    } else {                                                                                \
+      masks_bin_kernel<II, kMTLarge, false><<<(unsigned)(M * F), kMTLarge, 0, s>>>(         \
+          y2, N, F, w.zs, w.lab, w.fpow, w.bpow, w.cnt, S2);                                \
+    }                                                                                       \
     break;
     FFCA_MASK_CASE(1)
     FFCA_MASK_CASE(2)
