@@ -6,6 +6,13 @@
 // registers.
 #pragma once
 
+// Jacobi rotation threshold (squared): rotate (p, q) while
+// |a_pq|^2 > FFCA_JACOBI_TOL2 |a_pp a_qq| (Demmel-Veselic relative criterion)
+#ifndef FFCA_JACOBI_TOL2
+#define FFCA_JACOBI_TOL2 1e-32
+#endif
+
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -210,7 +217,7 @@ FFCA_DEV void jacobi_herm(double2 (&A)[I][I], double2 (&V)[I][I]) {
   // accuracy); stop after a sweep without rotations. A fixed "off(A) < tiny"
   // test would never trigger: rotations keep re-creating roundoff-level
   // off-diagonal entries.
-  constexpr double kTol2 = 1e-32;  // (1e-16)^2
+  constexpr double kTol2 = FFCA_JACOBI_TOL2;
   for (int sweep = 0; sweep < 30; ++sweep) {
     bool rotated = false;
 #pragma unroll

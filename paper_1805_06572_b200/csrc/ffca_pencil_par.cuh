@@ -149,7 +149,7 @@ FFCA_DEV void par_jacobi(const BinView<I>& v, int M, int V, int r, bool act) {
   __syncwarp();
   if (I == 1) return;
   constexpr int n_rounds = (I % 2 == 0) ? I - 1 : I;
-  constexpr double kTol2 = 1e-32;
+  constexpr double kTol2 = FFCA_JACOBI_TOL2;
   double* rot = v.scal;  // [NPAIR][6]: c, s, emi.x, emi.y, -, flag
 #pragma unroll 1
   for (int sweep = 0; sweep < 30; ++sweep) {
