@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--streams", type=int, default=2,
                     help="concurrent streams over independent mixtures (batched configs)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="mixtures/bins in the CPU sample")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: every rank runs its own full config batch (independent "
+                         "mixtures, no collective); strong: the batch is sharded")
     return ap.parse_args()
 
 
@@ -68,11 +71,14 @@ def dist_env():
     return rank, world, local
 
 
-def shard(cfg, rank, world):
-    """Mixture shard for config-3 batches, bin shard for single mixtures
-    (paper_1805_06572_b200.sharding)."""
+def shard(cfg, rank, world, scaling="strong"):
+    """strong: mixture shard for config-3 batches, bin shard for single
+    mixtures (paper_1805_06572_b200.sharding); weak: rank r runs its own full
+    config batch of independent mixtures r*M .. r*M + M-1 (no collective)."""
     from paper_1805_06572_b200.sharding import plan_shard
 
+    if scaling == "weak":
+        return ("mixtures", rank * cfg.M, (rank + 1) * cfg.M)
     sh = plan_shard(cfg.M, cfg.F, rank, world)
     return (sh.axis, sh.start, sh.stop)
 
@@ -186,7 +192,7 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": f"EM TF-bin*iterations/s ({'FastFCA' if args.engine == 'fast' else 'FCA'}, config {cfg.index})",
         "value": value, "unit": "TF-bin*it/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "higher_is_better": True, "scaling": args.scaling,
         "dtype": "c128", "data": "synthetic (seeded, BASELINE.json recipe)",
         "config": {"workload": cfg.description, "engine": args.engine, "iterations": cfg.L},
         "cpu_baseline": {"value": value, "unit": "TF-bin*it/s", "cores": cores, "kind": kind,
@@ -213,7 +219,7 @@ def main():
     from paper_1805_06572_b200 import SpatialModel, fastfca_run, fca_run
     from paper_1805_06572_b200._engine import run_device, torch_types
 
-    sh = shard(cfg, rank, world)
+    sh = shard(cfg, rank, world, args.scaling)
     Y, V, S, FL = make_inputs(cfg, sh)
     M, N, F, I = Y.shape
     L = cfg.L
@@ -228,7 +234,8 @@ def main():
 
     cf, _ = plan_chunks(cfg.M * cfg.F, cfg.N, cfg.I, args.dtype, args.engine)
     tf_it_rank = M * F * N * L
-    tf_it_total = cfg.M * cfg.F * cfg.N * L
+    # whole-job units: all ranks' mixtures (weak) or the one sharded batch (strong)
+    tf_it_total = cfg.M * cfg.F * cfg.N * L * (world if args.scaling == "weak" else 1)
 
     from paper_1805_06572_b200._engine import status_of
 
@@ -415,11 +422,13 @@ def main():
             "metric": f"EM TF-bin*iterations/s ({'FastFCA' if args.engine == 'fast' else 'FCA'}, config {cfg.index})",
             "value": value, "unit": "TF-bin*it/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (seeded, BASELINE.json recipe)",
             "config": {"workload": cfg.description, "engine": args.engine, "iterations": L,
                        "M": cfg.M, "F": cfg.F, "N": cfg.N, "I": cfg.I,
-                       "parallelism": f"{sh[0]}-sharded x{world}",
+                       "parallelism": (f"independent {cfg.M}-mixture batch per GPU x{world}"
+                                       if args.scaling == "weak" else f"{sh[0]}-sharded x{world}"),
+                       "global_batch": cfg.M * (world if args.scaling == "weak" else 1),
                        "streams_per_gpu": nstreams,
                        "l2": "inputs larger than L2 (y = %.2f GB)" % (Y.nbytes / 1e9 * world)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
