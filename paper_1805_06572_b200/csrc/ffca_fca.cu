@@ -10,8 +10,9 @@
 // (regularize_covariances).
 //
 // Mapping as K3: lane <-> bin, warps <-> frame slices. The CTA's 32 bins keep
-// S1, S2, S1^{-1}, S2^{-1} (packed Hermitian) in shared memory, bin-minor so
-// each lane's reads are bank-conflict free.
+// S1, S2 (packed Hermitian) in shared memory, bin-minor so each lane's reads
+// are bank-conflict free. The power-update traces tr(S_j^-1 Phi_j) are taken
+// through identities that need no S_j^-1 (see the trace block).
 #include "ffca_internal.cuh"
 
 namespace ffca {
@@ -22,8 +23,8 @@ __global__ void __launch_bounds__(WARPS * 32) fca_em_kernel(const FcaIterParams 
   constexpr int NP = I * I;
   constexpr int NE = 2 * NP + 1;
   extern __shared__ double smem[];
-  double* sS = smem;                    // [4][NP][32]
-  double* red = smem + 4 * NP * 32;     // [(WARPS-1)][NE][32]
+  double* sS = smem;                    // [2][NP][32]: S1, S2 (the traces need no S^-1)
+  double* red = smem + 2 * NP * 32;     // [(WARPS-1)][NE][32]
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t G = p.G;
@@ -32,7 +33,7 @@ __global__ void __launch_bounds__(WARPS * 32) fca_em_kernel(const FcaIterParams 
   if (!active) g = G - 1;
   const int64_t m = g / p.F;
   const int64_t f = g - m * p.F;
-  for (int e = warp; e < 4 * NP; e += WARPS) sS[e * 32 + lane] = p.Sp[(size_t)e * G + g];
+  for (int e = warp; e < 2 * NP; e += WARPS) sS[e * 32 + lane] = p.Sp[(size_t)e * G + g];
   __syncthreads();
   const int64_t n0 = (int64_t)blockIdx.y * p.chunk_frames;
   const int64_t n1 = min(p.N, n0 + p.chunk_frames);
@@ -94,19 +95,19 @@ __global__ void __launch_bounds__(WARPS * 32) fca_em_kernel(const FcaIterParams 
       }
       llacc += 2.0 * log(prod) + quad;
     }
-    // Rinv = Li^H Li (frame-wise inverse), x = Rinv y
+    // Rinv = Li^H Li (frame-wise inverse; Hermitian: upper triangle computed,
+    // lower mirrored), x = Rinv y
     double2 Ri[I][I];
 #pragma unroll
     for (int a = 0; a < I; ++a)
 #pragma unroll
-      for (int b = 0; b < I; ++b) {
+      for (int b = a; b < I; ++b) {
         double2 s = cmk(0.0, 0.0);
 #pragma unroll
-        for (int k = 0; k < I; ++k) {
-          if (k < a || k < b) continue;
-          s = cadd(s, cconjmul(Li[k][a], Li[k][b]));
-        }
+        for (int k = b; k < I; ++k) s = cadd(s, cconjmul(Li[k][a], Li[k][b]));
+        if (a == b) s.y = 0.0;
         Ri[a][b] = s;
+        Ri[b][a] = cconj(s);
       }
     double2 x[I];
 #pragma unroll
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__(WARPS * 32) fca_em_kernel(const FcaIterParams 
     if (!p.update) continue;
     // cross term Cm = v1 v2 S1 (Rinv S2)  (Hermitian; upper triangle)
     double2 Cm[I][I];
+    double Tdiag[I];  // Re diag(Rinv S2), for the source-1 trace
     {
       double2 T[I][I];
 #pragma unroll
@@ -153,6 +155,8 @@ __global__ void __launch_bounds__(WARPS * 32) fca_em_kernel(const FcaIterParams 
           for (int k = 0; k < I; ++k) s = cadd(s, cmul(Ri[a][k], Sget(1, k, b)));
           T[a][b] = s;
         }
+#pragma unroll
+      for (int a = 0; a < I; ++a) Tdiag[a] = T[a][a].x;
       const double vv = v1 * v2;
 #pragma unroll
       for (int a = 0; a < I; ++a)
@@ -165,25 +169,28 @@ __global__ void __launch_bounds__(WARPS * 32) fca_em_kernel(const FcaIterParams 
           if (a == b) Cm[a][b].y = 0.0;
         }
     }
-    // tr_j = Re tr(Sinv_j (mu_j mu_j^H + Cm))
+    // tr_j = Re tr(S_j^-1 Phi_j), Phi_j = mu_j mu_j^H + Cm, without S_j^-1:
+    //   mu_j^H S_j^-1 mu_j = v_j Re(x^H mu_j)          (mu_j = v_j S_j x)
+    //   tr(S_1^-1 Cm) = v1 v2 Re tr(Rinv S2) = v1 v2 Re tr(T)
+    //   tr(S_2^-1 Cm) = v1 v2 Re tr(S1 Rinv)             (cyclic trace)
+    // every term is non-negative (no cancellation)
     double tr[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const double2* mu = j == 0 ? mu1 : mu2;
-      double t = 0.0;
+    {
+      double q1 = 0.0, q2 = 0.0, tT = 0.0, tSR = 0.0;
 #pragma unroll
       for (int a = 0; a < I; ++a) {
-        const double2 sa = Sget(2 + j, a, a);
-        t += sa.x * (cabs2(mu[a]) + Cm[a][a].x);
+        q1 += x[a].x * mu1[a].x + x[a].y * mu1[a].y;
+        q2 += x[a].x * mu2[a].x + x[a].y * mu2[a].y;
+        tT += Tdiag[a];
 #pragma unroll
-        for (int b = a + 1; b < I; ++b) {
-          // Sinv[a][b] * Phi[b][a] + Sinv[b][a] * Phi[a][b] = 2 Re(Sinv[a][b] Phi[b][a])
-          const double2 sab = Sget(2 + j, a, b);
-          const double2 phi_ba = cadd(cmulc(mu[b], mu[a]), cconj(Cm[a][b]));
-          t += 2.0 * (sab.x * phi_ba.x - sab.y * phi_ba.y);
+        for (int b = 0; b < I; ++b) {  // Re(S1[a][b] Ri[b][a])
+          const double2 s1 = Sget(0, a, b);
+          tSR += s1.x * Ri[b][a].x - s1.y * Ri[b][a].y;
         }
       }
-      tr[j] = t;
+      const double vv = v1 * v2;
+      tr[0] = v1 * q1 + vv * tT;
+      tr[1] = v2 * q2 + vv * tSR;
     }
     const double q1 = tr[0] * invI, q2 = tr[1] * invI;
     const double w1 = (q1 < fl) ? fl : q1;
@@ -253,7 +260,7 @@ template <int I, typename R>
 static cudaError_t launch_fca_em_t(const FcaIterParams& p, cudaStream_t s) {
   constexpr int NP = I * I;
   constexpr int NE = 2 * NP + 1;
-  const size_t smem = ((size_t)4 * NP * 32 + (size_t)(kWarps - 1) * NE * 32) * sizeof(double);
+  const size_t smem = ((size_t)2 * NP * 32 + (size_t)(kWarps - 1) * NE * 32) * sizeof(double);
   auto kern = fca_em_kernel<I, R, kWarps>;
   static bool configured = false;
   if (!configured) {
@@ -271,7 +278,7 @@ template <int I, typename R>
 static int fca_bpsm_t() {
   constexpr int NP = I * I;
   constexpr int NE = 2 * NP + 1;
-  const size_t smem = ((size_t)4 * NP * 32 + (size_t)(kWarps - 1) * NE * 32) * sizeof(double);
+  const size_t smem = ((size_t)2 * NP * 32 + (size_t)(kWarps - 1) * NE * 32) * sizeof(double);
   auto kern = fca_em_kernel<I, R, kWarps>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int n = 0;
