@@ -106,8 +106,8 @@ FcaWs carve_fca(void* base, int64_t M, int64_t N, int64_t F, int I, int L, unsig
     plan_fca_chunks(G, N, I, dtype, &w.chunk_frames, &w.nchunk);
   Carve c(base);
   w.st = c.take<ffca_status_dev>(1);
-  w.Sp = c.take<double>((size_t)4 * I * I * G);
-  w.Spart = c.take<double>((size_t)w.nchunk * 2 * I * I * G);
+  w.Sp = c.take<double>((size_t)2 * I * I * G);
+  w.Spart = c.take<double>((size_t)w.nchunk * kFcaParts * I * I * G);
   const bool ll = flags & FFCA_FLAG_LIKELIHOOD;
   w.llbin = ll ? c.take<double>((size_t)w.nchunk * G) : nullptr;
   w.llg = ll ? c.take<double>((size_t)(L + 1) * G) : nullptr;

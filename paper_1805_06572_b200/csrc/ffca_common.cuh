@@ -28,6 +28,30 @@ constexpr double kCovEps = 1e-9;               // reference modelops.py:9
 constexpr double kDefFloor = 1e-12;            // reference pencil.py:25
 constexpr double kHermRtol = 1e-10;            // reference pencil.py:22
 
+// ---- fast FP64 reciprocal / reciprocal square root --------------------------
+// MUFU seed (rcp/rsqrt.approx.ftz.f64) + two Newton steps: ~1 ulp, no IEEE
+// division / sqrt subroutine (special-case branches) on the per-point paths.
+// Non-positive / non-finite inputs give non-finite or meaningless results;
+// callers test the input (d > 0) themselves.
+FFCA_DEV double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+FFCA_DEV double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double e = fma(-x * y, y, 1.0);  // 1 - x y^2
+    y = fma(0.5 * y, e, y);
+  }
+  return y;
+}
+
 // ---- complex arithmetic --------------------------------------------------
 FFCA_DEV double2 cmk(double re, double im) { return make_double2(re, im); }
 // sum_{c < n} src[c * stride] in the fixed order ((s_0 + s_1) + s_2) + ...
@@ -549,6 +573,51 @@ FFCA_DEV bool cholesky(const double2 (&A)[I][I], double2 (&L)[I][I]) {
     for (int i = 0; i < j; ++i) L[i][j] = cmk(0.0, 0.0);
   }
   return ok;
+}
+
+// Cholesky for the per-point paths: as cholesky() but with rsqrt_fast and
+// multiplications by the returned inverse diagonal (no IEEE sqrt / division).
+template <int I>
+FFCA_DEV bool cholesky_fast(const double2 (&A)[I][I], double2 (&L)[I][I], double (&ild)[I]) {
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < I; ++j) {
+    double d = A[j][j].x;
+#pragma unroll
+    for (int k = 0; k < j; ++k) d -= cabs2(L[j][k]);
+    if (!(d > 0.0)) ok = false;
+    const double il = rsqrt_fast(d);
+    ild[j] = il;
+    L[j][j] = cmk(d * il, 0.0);
+#pragma unroll
+    for (int i = j + 1; i < I; ++i) {
+      double2 s = A[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) s = csub(s, cmulc(L[i][k], L[j][k]));
+      L[i][j] = cscale(s, il);
+    }
+#pragma unroll
+    for (int i = 0; i < j; ++i) L[i][j] = cmk(0.0, 0.0);
+  }
+  return ok;
+}
+// tril_inverse with the inverse diagonal given (from cholesky_fast)
+template <int I>
+FFCA_DEV void tril_inverse_d(const double2 (&L)[I][I], const double (&ild)[I], double2 (&Li)[I][I]) {
+#pragma unroll
+  for (int c = 0; c < I; ++c) {
+#pragma unroll
+    for (int r = 0; r < I; ++r) {
+      if (r < c) {
+        Li[r][c] = cmk(0.0, 0.0);
+        continue;
+      }
+      double2 s = cmk(r == c ? 1.0 : 0.0, 0.0);
+#pragma unroll
+      for (int k = c; k < r; ++k) s = csub(s, cmul(L[r][k], Li[k][c]));
+      Li[r][c] = cscale(s, ild[r]);
+    }
+  }
 }
 
 // Inverse of a lower-triangular matrix (forward substitution per column).

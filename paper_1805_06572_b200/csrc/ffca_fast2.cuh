@@ -128,20 +128,40 @@ struct Math<float> {
   static FFCA_DEV float2 c2(double2 a) { return make_float2((float)a.x, (float)a.y); }
 };
 
+// One ring stage of one warp = one frame of its 32 bins: the frame's y row
+// of the 32 bins (32 * YB contiguous bytes in HBM) in Q units of UB bytes
+// per bin, then v1[32] and v2[32]. The warp copies it cooperatively: copy c
+// of lane l moves unit u = 32 c + l of the row, so every cp.async instruction
+// reads one contiguous 32*UB-byte run of HBM (full sectors) and writes a
+// contiguous run of shared memory; a bin's Q units are rotated by a
+// bin-dependent amount (sw) so that the consumer reads (lane = bin, one unit
+// each) hit distinct banks. (Per-lane 80-byte slots made every 16-B cp.async
+// a ~30-way bank conflict and read half-used sectors.)
 template <int I, typename R>
 struct RingSlot {
   using C = typename CplxOf<R>::type;
   static constexpr int YB = I * (int)sizeof(C);
   static constexpr int VB = (int)sizeof(R);
-  static constexpr int RAW = YB + 2 * VB;
-  static constexpr int U16 = (RAW + 15) / 16;
-  static constexpr int BYTES = 16 * ((U16 % 2) ? U16 : U16 + 1);  // odd # of 16-B units
+  static constexpr int UB = (YB % 16 == 0) ? 16 : 8;  // unit bytes
+  static constexpr int Q = YB / UB;                   // units per bin
+  static constexpr int WARP_BYTES = 32 * (YB + 2 * VB);
+  static_assert(WARP_BYTES % 16 == 0, "stage alignment");
+  // unit a of bin b sits at unit Q b + (a ^ sw(b)): for a power-of-two Q the
+  // xor spreads the 8 (UB = 16) or 16 (UB = 8) consecutive bins that read
+  // the same a over distinct banks; an odd Q needs no swizzle. Copy c of lane
+  // l (unit 32 c + l) then lands at pos(first unit) + 32 c UB, and the reads
+  // of bin b are at rbase(b) ^ (a UB) (Q even) or rbase(b) + a UB (Q odd).
+  static constexpr bool kXor = UB == 16 && Q % 2 == 0;
+  static FFCA_DEV constexpr int sw(int b) { return kXor ? (b * Q / 8) % Q : 0; }
+  static FFCA_DEV constexpr int pos(int b, int a) { return (Q * b + (a ^ sw(b))) * UB; }
+  static FFCA_DEV constexpr int rbase(int b) { return (Q * b + sw(b)) * UB; }
+  static FFCA_DEV constexpr int rpos(int rb, int a) { return kXor ? (rb ^ (a * UB)) : rb + a * UB; }
 };
 
 template <int I, typename R, int WARPS, int STAGES, bool MU = false>
 struct Fast2Smem {
   static constexpr int NE = 2 * I * I + 1;
-  static constexpr size_t RING = (size_t)STAGES * WARPS * 32 * RingSlot<I, R>::BYTES;
+  static constexpr size_t RING = (size_t)STAGES * WARPS * RingSlot<I, R>::WARP_BYTES;
   static constexpr size_t RED = (size_t)(WARPS - 1) * NE * 32 * sizeof(double);
   static constexpr size_t PB = (size_t)I * I * 32 * sizeof(typename Math<R>::T2);  // P tile
   static constexpr size_t WB = MU ? PB : 0;                           // W tile, after P
@@ -185,8 +205,6 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
   const int64_t n0 = (int64_t)blockIdx.y * p.chunk_frames;
   const int64_t n1 = min(p.N, n0 + p.chunk_frames);
   const int64_t NF = p.N * p.F;
-  const int64_t FI = p.F * I;
-  const C* __restrict__ yb = (const C*)p.y + (m * p.N * p.F + f) * I;
   R* __restrict__ vb = (R*)p.v + m * 2 * NF + f;
 
   // P lives in shared memory (bin-minor SoA after the frame ring): the 4
@@ -237,28 +255,67 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
   double llacc = 0.0;
   int64_t bad_n = 0;
 
-  unsigned char* myslots = smem_raw + ((size_t)warp * 32 + lane) * Slot::BYTES;
-  constexpr size_t kStageStride = (size_t)WARPS * 32 * Slot::BYTES;
+  unsigned char* wslots = smem_raw + (size_t)warp * Slot::WARP_BYTES;
+  constexpr size_t kStageStride = (size_t)WARPS * Slot::WARP_BYTES;
   const int64_t nfirst = n0 + warp;
   const int K = nfirst < n1 ? (int)((n1 - nfirst + WARPS - 1) / WARPS) : 0;
+  // this lane's share of the warp's row copies: unit u = 32 c + lane belongs
+  // to bin b = u / Q of the tile (clamped like g), unit a = u % Q. When the
+  // tile's 32 bins lie in one mixture (and none is clamped) the row is one
+  // contiguous run and copy c reads ybase + 32 c UB; a tile across a mixture
+  // boundary (or the last, partial tile) adds a per-copy correction.
+  const int64_t tile0 = (int64_t)blockIdx.x * 32;
+  const bool contiguous = (tile0 + 31 < G) && (tile0 / p.F == (tile0 + 31) / p.F);
+  const int spos0 = Slot::pos(lane / Slot::Q, lane % Slot::Q);
+  const int rb = Slot::rbase(lane);
+  auto unit_off = [&](int c) -> int64_t {  // byte offset (frame 0) of copy c
+    const int u = 32 * c + lane, b = u / Slot::Q, a = u % Slot::Q;
+    int64_t gb = tile0 + b;
+    if (gb >= G) gb = G - 1;
+    const int64_t mb = gb / p.F, fb = gb - mb * p.F;
+    return ((mb * p.N) * p.F + fb) * Slot::YB + a * Slot::UB;
+  };
+  const int64_t ybase = unit_off(0);
+  int64_t ycorr[Slot::Q];  // unit_off(c) - ybase - 32 c UB (non-contiguous tiles)
+#pragma unroll
+  for (int c = 0; c < Slot::Q; ++c)
+    ycorr[c] = contiguous ? 0 : unit_off(c) - ybase - 32 * c * Slot::UB;
+  const unsigned char* ybytes = (const unsigned char*)p.y + ybase;
+  const int64_t frame_bytes = p.F * Slot::YB;
+  int issue_stage = 0, read_stage = 0;  // byte offsets of the next stages
 
   auto issue = [&](int k) {
     const int64_t n = nfirst + (int64_t)k * WARPS;
-    unsigned char* slot = myslots + (size_t)(k % STAGES) * kStageStride;
-    const unsigned char* ysrc = (const unsigned char*)(yb + n * FI);
-    if constexpr (Slot::YB % 16 == 0) {
+    unsigned char* slot = wslots + issue_stage;
+    issue_stage = (issue_stage + (int)kStageStride == STAGES * (int)kStageStride)
+                      ? 0 : issue_stage + (int)kStageStride;
+    const unsigned char* yrow = ybytes + n * frame_bytes;
+    unsigned char* dst = slot + spos0;
+    if (contiguous) {  // one base, compile-time offsets
 #pragma unroll
-      for (int c = 0; c < Slot::YB / 16; ++c) cp_async16(slot + 16 * c, ysrc + 16 * c);
+      for (int c = 0; c < Slot::Q; ++c) {
+        if constexpr (Slot::UB == 16)
+          cp_async16(dst + 32 * c * Slot::UB, yrow + 32 * c * Slot::UB);
+        else
+          cp_async8(dst + 32 * c * Slot::UB, yrow + 32 * c * Slot::UB);
+      }
     } else {
 #pragma unroll
-      for (int c = 0; c < Slot::YB / 8; ++c) cp_async8(slot + 8 * c, ysrc + 8 * c);
+      for (int c = 0; c < Slot::Q; ++c) {
+        const unsigned char* src = yrow + 32 * c * Slot::UB + ycorr[c];
+        if constexpr (Slot::UB == 16)
+          cp_async16(dst + 32 * c * Slot::UB, src);
+        else
+          cp_async8(dst + 32 * c * Slot::UB, src);
+      }
     }
+    unsigned char* vs = slot + 32 * Slot::YB;
     if constexpr (sizeof(R) == 8) {
-      cp_async8(slot + Slot::YB, vb + n * p.F);
-      cp_async8(slot + Slot::YB + 8, vb + NF + n * p.F);
+      cp_async8(vs + 8 * lane, vb + n * p.F);
+      cp_async8(vs + 256 + 8 * lane, vb + NF + n * p.F);
     } else {
-      cp_async4(slot + Slot::YB, vb + n * p.F);
-      cp_async4(slot + Slot::YB + 4, vb + NF + n * p.F);
+      cp_async4(vs + 4 * lane, vb + n * p.F);
+      cp_async4(vs + 128 + 4 * lane, vb + NF + n * p.F);
     }
   };
 
@@ -384,20 +441,35 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
     if (bad && bad_n == 0) bad_n = n + 1;
   };
   auto load_frame = [&](int k, T2 (&yv)[I], T& v1, T& v2) {
-    const unsigned char* slot = myslots + (size_t)(k % STAGES) * kStageStride;
+    const unsigned char* slot = wslots + read_stage;
+    read_stage = (read_stage + (int)kStageStride == STAGES * (int)kStageStride)
+                     ? 0 : read_stage + (int)kStageStride;
+    constexpr int PER = Slot::UB / (int)sizeof(T2);  // channels per unit
 #pragma unroll
-    for (int a = 0; a < I; ++a) yv[a] = ((const T2*)slot)[a];
-    v1 = *(const R*)(slot + Slot::YB);
-    v2 = *(const R*)(slot + Slot::YB + sizeof(R));
+    for (int a = 0; a < Slot::Q; ++a) {
+      const T2* src = (const T2*)(slot + Slot::rpos(rb, a));
+      if constexpr (PER == 2) {
+        const float4 q = *(const float4*)src;  // two complex64 channels
+        yv[2 * a] = T2{(T)q.x, (T)q.y};
+        yv[2 * a + 1] = T2{(T)q.z, (T)q.w};
+      } else {
+        yv[a] = *src;
+      }
+    }
+    const unsigned char* vs = slot + 32 * Slot::YB;
+    v1 = ((const R*)vs)[lane];
+    v2 = ((const R*)(vs + 32 * sizeof(R)))[lane];
   };
 
   {
     constexpr int kUnroll = FAST2_UNROLL;
 #pragma unroll kUnroll
     for (int k = 0; k < K; ++k) {
+      __syncwarp();  // every lane is done with the stage the next copy overwrites
       if (k + STAGES - 1 < K) issue(k + STAGES - 1);
       cp_async_commit();
       cp_async_wait<STAGES - 1>();
+      __syncwarp();  // the other lanes' copies of this stage are visible
       T2 yv[I];
       T v1, v2;
       load_frame(k, yv, v1, v2);

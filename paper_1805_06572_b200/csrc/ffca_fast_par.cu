@@ -4,8 +4,10 @@
 // accumulators in registers, so the v1 kernel (ffca_fast.cu) spills. Here a
 // group of 8 lanes owns one bin and streams its frames; lane r owns channel
 // r: column r of P (z_r = sum_b conj(P[b][r]) y_b), the scalar posterior of
-// channel r (den, g1, g2, t1, t2), and row r of both transformed covariance
-// accumulators. The power update needs sums over channels (group shuffles);
+// channel r (den, g1, g2, t1, t2), the diagonal entry r and a circulant share
+// of the off-diagonal entries of both transformed covariance accumulators
+// ((r, r + s mod I), s = 1..I/2: <= 4 per lane at I = 8 instead of a
+// triangular row of up to 7). The power update needs sums over channels (group shuffles);
 // the rank-1 updates need every z_c, g1_c, g2_c (exchanged through a few
 // bytes of shared memory per bin). Same arithmetic as fast_em2_kernel
 // (reference _kernels_numba.py:328-391), same Spart / llbin / mu layouts.
@@ -36,8 +38,11 @@ struct FastParLayout {
 };
 }  // namespace
 
+#ifndef FAST_PAR_MINB
+#define FAST_PAR_MINB 8  // CTAs per SM the lane-parallel pass is register-budgeted for
+#endif
 template <int I, typename R, bool UPDATE, bool LL, bool MU>
-__global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32) fast_par_kernel(const FastIterParams p) {
+__global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, FAST_PAR_MINB) fast_par_kernel(const FastIterParams p) {
   using Lay = FastParLayout<I>;
   using C = typename CplxOf<R>::type;
   constexpr int NP = I * I;
@@ -84,13 +89,24 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32) fast_par_kernel(
            (void*)p.llbin, p.mu_out, (void*)p.st);
 #endif
 
-  // row rr of both accumulators: diagonal (real) and the entries c > rr;
-  // arrays are only ever indexed by compile-time c (runtime indexing would
-  // demote them to local memory)
-  double accd1 = 0.0, accd2 = 0.0;
-  double acc1[I], acc2[I], acc1i[I], acc2i[I];
+  // accumulators: the diagonal entry (rr, rr) (real) and the off-diagonal
+  // entries (rr, rr + s mod I), s = 1..I/2, dealt circulantly so every lane
+  // owns ceil or floor of (I-1)/2 of them (the s = I/2 entries of an even
+  // order to the lower half of the lanes); arrays are only ever indexed by
+  // the compile-time slot s (runtime indexing would demote them to local
+  // memory)
+  constexpr int NO = I / 2;  // off-diagonal slots per lane
+  int ob[NO + 1];
+  bool ov[NO + 1];
 #pragma unroll
-  for (int c = 0; c < I; ++c) acc1[c] = acc2[c] = acc1i[c] = acc2i[c] = 0.0;
+  for (int s = 1; s <= NO; ++s) {
+    ob[s] = (rr + s) % I;
+    ov[s] = own && (s < NO || (I % 2) == 1 || rr < NO);
+  }
+  double accd1 = 0.0, accd2 = 0.0;
+  double acc1[NO + 1], acc2[NO + 1], acc1i[NO + 1], acc2i[NO + 1];
+#pragma unroll
+  for (int c = 0; c <= NO; ++c) acc1[c] = acc2[c] = acc1i[c] = acc2i[c] = 0.0;
   double llacc = 0.0;
   int64_t bad_n = 0;
 
@@ -183,16 +199,17 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32) fast_par_kernel(
       accd1 = fma(t1, iw1, accd1);
       accd2 = fma(t2, iw2, accd2);
 #pragma unroll
-      for (int cc = 0; cc < I; ++cc) {
-        if (cc <= r) continue;
+      for (int so = 1; so <= NO; ++so) {
+        if (so == NO && (I % 2) == 0 && !ov[so]) continue;  // the half-filled last slot
+        const int cc = ob[so];
         const double2 zc = sz[cc];
         const double xr = fma(zr, zc.x, zi * zc.y);   // z_r conj(z_c)
         const double xi = fma(zi, zc.x, -zr * zc.y);
         const double k1 = h1 * sg1[cc], k2 = h2 * sg2[cc];
-        acc1[cc] = fma(k1, xr, acc1[cc]);
-        acc1i[cc] = fma(k1, xi, acc1i[cc]);
-        acc2[cc] = fma(k2, xr, acc2[cc]);
-        acc2i[cc] = fma(k2, xi, acc2i[cc]);
+        acc1[so] = fma(k1, xr, acc1[so]);
+        acc1i[so] = fma(k1, xi, acc1i[so]);
+        acc2[so] = fma(k2, xr, acc2[so]);
+        acc2i[so] = fma(k2, xi, acc2i[so]);
       }
     }
     if (MU && own && active) {
@@ -236,12 +253,17 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32) fast_par_kernel(
     sp[(size_t)r * G] = accd1;
     sp[(size_t)(NP + r) * G] = accd2;
 #pragma unroll
-    for (int cc = 0; cc < I; ++cc) {
-      if (cc <= r) continue;
-      sp[(size_t)Herm<I>::re(r, cc) * G] = acc1[cc];
-      sp[(size_t)Herm<I>::im(r, cc) * G] = acc1i[cc];
-      sp[(size_t)(NP + Herm<I>::re(r, cc)) * G] = acc2[cc];
-      sp[(size_t)(NP + Herm<I>::im(r, cc)) * G] = acc2i[cc];
+    for (int so = 1; so <= NO; ++so) {
+      if (!ov[so]) continue;
+      // stored entry (a, b), a < b: the slot's (r, c) or its conjugate
+      const int cc = ob[so];
+      const bool flip = r > cc;
+      const int a = flip ? cc : r, b = flip ? r : cc;
+      const double s = flip ? -1.0 : 1.0;
+      sp[(size_t)Herm<I>::re(a, b) * G] = acc1[so];
+      sp[(size_t)Herm<I>::im(a, b) * G] = s * acc1i[so];
+      sp[(size_t)(NP + Herm<I>::re(a, b)) * G] = acc2[so];
+      sp[(size_t)(NP + Herm<I>::im(a, b)) * G] = s * acc2i[so];
     }
   }
   if (LL && r == 0) p.llbin[(size_t)ch * G + g] = llacc;

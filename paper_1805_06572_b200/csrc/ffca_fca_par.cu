@@ -1,18 +1,19 @@
 // K4p — conventional FCA pass for large orders (5 <= I <= 8), lane-parallel.
 //
-// A point's frame-wise inverse and I x I products (reference
-// _kernels_numba.py:246-325) need several I x I complex matrices: at I = 8
-// that is ~1 KB each, so the per-thread kernel (ffca_fca.cu) spills heavily.
-// Here a group of 8 lanes owns one bin and streams its frames; lane r owns row
-// r (or column r) of every per-point matrix, which lives in shared memory:
+// A point's frame-wise inverse (reference _kernels_numba.py:246-325) needs
+// I x I complex matrices: at I = 8 ~1 KB each, so the per-thread kernel
+// (ffca_fca.cu) spills heavily. Here a group of 8 lanes owns one bin and
+// streams its frames; the per-point matrix lives in shared memory:
 //   R = v1 S1 + v2 S2 -> Cholesky L (column-sequential, row-parallel)
-//   L^-1 (column-parallel)      u = L^-1 y, x = L^-H u = R^-1 y
-//   mu_j = v_j S_j x            T = L^-H (L^-1 S2) = R^-1 S2
-//   cross = v1 v2 S1 T (row r in registers; Hermitian, so its column r is
-//   the conjugate of its row r)  tr_j = Re tr(S_j^-1 Phi_j) by group sum
-//   w_j, v update, S_j rows accumulated in registers (upper triangle).
-// Per-bin S1, S2, S1^-1, S2^-1 stay in shared memory (packed Hermitian).
-// Partial sums per (chunk, bin) in the same Spart layout as K4.
+//   L^-1 (column-parallel, in place)   u = L^-1 y, x = L^-H u = R^-1 y
+//   Rinv = L^-H L^-1 entries, x x^H entries, traces, w_j, v update,
+//   B_j += v_j^2/w_j x x^H, X_j += v1 v2/w_j Rinv  (as fca_em_kernel: the
+//   I x I products of Phi_j are applied once per bin in fca_finish_kernel).
+// The I(I+1)/2 Hermitian entries are dealt to the lanes circulantly: lane r
+// owns (r, r + s mod I) for s = 0..I/2 (the s = I/2 diagonal of an even order
+// to the lower half of the lanes), so every lane has ceil or floor of
+// (I+1)/2 entries instead of a triangular row. Per-bin S1, S2 stay in shared
+// memory (packed Hermitian). Partial sums per (chunk, bin) in the K4 layout.
 #include "ffca_pencil_par.cuh"
 
 namespace ffca {
@@ -26,15 +27,17 @@ struct FcaParLayout {
   static constexpr int BPB = WARPS * 32 / LB;  // bins (groups) per CTA
   static constexpr int LD = (I % 2) ? I + 2 : I + 1;
   static constexpr int NP = I * I;
-  static constexpr int MATD = I * LD * 2;  // doubles per padded complex matrix
-  // per group: 4 packed S (4 NP) + 3 matrices (L/Y2, Li, T) + 5 vectors (2I each)
-  // + misc (8), rounded to an odd number of 16-B units
-  static constexpr int RAW = 4 * NP + 3 * MATD + 10 * I + 8;
+  static constexpr int NS = I / 2 + 1;          // entry slots per lane
+  static constexpr int MATD = I * LD * 2;       // doubles per padded complex matrix
+  // per group: 2 packed S (2 NP) + 1 matrix (R / L / L^-1) + 3 vectors (2I each)
+  // + misc (2) + inverse diagonal (I), rounded to an odd number of 16-B units
+  static constexpr int RAW = 2 * NP + MATD + 6 * I + 2 + I;
   static constexpr int U16 = (RAW + 1) / 2;
   static constexpr int GROUP_DOUBLES = 2 * ((U16 % 2) ? U16 : U16 + 1);
   static constexpr size_t SMEM = (size_t)BPB * GROUP_DOUBLES * sizeof(double);
 };
 
+// entry (a, b) of a packed Hermitian matrix in shared memory, runtime indices
 template <int I>
 FFCA_DEV double2 packed_get(const double* S, int a, int b) {
   if (a == b) return cmk(S[a], 0.0);
@@ -50,6 +53,7 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
   using C = typename CplxOf<R>::type;
   constexpr int NP = I * I;
   constexpr int LB = Lay::LB;
+  constexpr int NS = Lay::NS;
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = lane % LB;
@@ -59,26 +63,30 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
   const bool active = g < G;
   if (!active) g = G - 1;
   const bool own = r < I;
+  const int rr = own ? r : 0;
   const int64_t m = g / p.F, f = g - m * p.F;
   double* base = sm + (size_t)grp * Lay::GROUP_DOUBLES;
-  double* Sp = base;                         // [4][NP] packed: S1, S2, S1^-1, S2^-1
-  double2* Lm = (double2*)(base + 4 * NP);   // R / L, later Y2 = L^-1 S2
-  double2* Li = Lm + I * Lay::LD;            // L^-1
-  double2* Tm = Li + I * Lay::LD;            // R^-1 S2
-  double2* vy = Tm + I * Lay::LD;            // y
-  double2* vu = vy + I;                      // L^-1 y
-  double2* vx = vu + I;                      // R^-1 y
-  double2* vm1 = vx + I;                     // mu_1
-  double2* vm2 = vm1 + I;                    // mu_2
-  double* misc = (double*)(vm2 + I);
-  auto at = [&](double2* M, int a, int b) -> double2& { return M[a * Lay::LD + b]; };
+  double* Sp = base;                        // [2][NP] packed: S1, S2
+  double2* Lm = (double2*)(base + 2 * NP);  // R -> L -> L^-1 (lower triangles)
+  double2* vy = Lm + I * Lay::LD;           // y
+  double2* vu = vy + I;                     // L^-1 y
+  double2* vx = vu + I;                     // R^-1 y
+  double* misc = (double*)(vx + I);
+  double* ildm = misc + 2;                  // inverse diagonal of L
+  auto at = [&](int a, int b) -> double2& { return Lm[a * Lay::LD + b]; };
 
-  for (int e = r; e < 4 * NP; e += LB) Sp[e] = p.Sp[(size_t)e * G + g];
+  for (int e = r; e < 2 * NP; e += LB) Sp[e] = p.Sp[(size_t)e * G + g];
   __syncwarp();
   const double* S1 = Sp;
   const double* S2 = Sp + NP;
-  const double* Si1 = Sp + 2 * NP;
-  const double* Si2 = Sp + 3 * NP;
+  // this lane's entry slots: (a0, b0) = (r, r + s mod I)
+  int sb[NS];
+  bool sv[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    sb[s] = (rr + s) % I;
+    sv[s] = own && (s < I / 2 || (I % 2) == 1 || rr < I / 2);
+  }
   const int64_t n0 = (int64_t)blockIdx.y * p.chunk_frames;
   const int64_t n1 = min(p.N, n0 + p.chunk_frames);
   const int64_t NF = p.N * p.F;
@@ -87,9 +95,12 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
   const double fl = p.floor[g];
   const bool do_ll = p.llbin != nullptr;
 
-  double2 acc1[I], acc2[I];  // row r of the S_j sums (entries c >= r used)
+  // accumulators per slot, oriented (a0, b0): B1, B2, X1, X2
+  double2 acc[kFcaParts][NS];
 #pragma unroll
-  for (int c = 0; c < I; ++c) acc1[c] = acc2[c] = cmk(0.0, 0.0);
+  for (int j = 0; j < kFcaParts; ++j)
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc[j][s] = cmk(0.0, 0.0);
   double llacc = 0.0;
   int64_t bad_n = 0;
 
@@ -114,8 +125,9 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
       vy[r] = ycur;
 #pragma unroll
       for (int c = 0; c < I; ++c) {
+        if (c > r) continue;
         const double2 s1 = packed_get<I>(S1, r, c), s2 = packed_get<I>(S2, r, c);
-        at(Lm, r, c) = cmk(v1 * s1.x + v2 * s2.x, v1 * s1.y + v2 * s2.y);
+        at(r, c) = cmk(v1 * s1.x + v2 * s2.x, v1 * s1.y + v2 * s2.y);
       }
     }
     __syncwarp();
@@ -127,135 +139,111 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
 #pragma unroll
     for (int j = 0; j < I; ++j) {
       if (own && r == j) {
-        double d = at(Lm, j, j).x;
+        double d = at(j, j).x;
 #pragma unroll
-        for (int k = 0; k < j; ++k) d -= cabs2(at(Lm, j, k));
+        for (int k = 0; k < j; ++k) d -= cabs2(at(j, k));
+        const double il = rsqrt_fast(d);
         misc[0] = d;
-        at(Lm, j, j) = cmk(sqrt(fmax(d, 0.0)), 0.0);
+        ildm[j] = il;
+        at(j, j) = cmk(d * il, 0.0);
       }
       __syncwarp();
       okc = okc && misc[0] > 0.0;
       if (own && r > j) {
-        double2 s = at(Lm, r, j);
+        double2 s = at(r, j);
 #pragma unroll
-        for (int k = 0; k < j; ++k) s = csub(s, cmulc(at(Lm, r, k), at(Lm, j, k)));
-        at(Lm, r, j) = cscale(s, 1.0 / at(Lm, j, j).x);
+        for (int k = 0; k < j; ++k) s = csub(s, cmulc(at(r, k), at(j, k)));
+        at(r, j) = cscale(s, ildm[j]);
       }
       __syncwarp();
     }
     if (!okc && bad_n == 0) bad_n = n + 1;
-    // L^-1, column-parallel: lane c keeps its column in registers
+    // L^-1, column-parallel: lane r builds column r in registers, then (after
+    // every lane has read L) writes it over L
+    const double lrr = own ? at(rr, rr).x : 1.0;
+    double2 col[I];
     if (own) {
-      double2 col[I];
 #pragma unroll
-      for (int rr = 0; rr < I; ++rr) {
-        double2 sacc = cmk(rr == r ? 1.0 : 0.0, 0.0);
+      for (int q = 0; q < I; ++q) {
+        double2 sacc = cmk(q == r ? 1.0 : 0.0, 0.0);
 #pragma unroll
-        for (int k = 0; k < rr; ++k)
-          if (k >= r) sacc = csub(sacc, cmul(at(Lm, rr, k), col[k]));
-        col[rr] = (rr >= r) ? cscale(sacc, 1.0 / at(Lm, rr, rr).x) : cmk(0.0, 0.0);
+        for (int k = 0; k < q; ++k)
+          if (k >= r) sacc = csub(sacc, cmul(at(q, k), col[k]));
+        col[q] = (q >= r) ? cscale(sacc, ildm[q]) : cmk(0.0, 0.0);
       }
-#pragma unroll
-      for (int rr = 0; rr < I; ++rr) at(Li, rr, r) = col[rr];
     }
     __syncwarp();
-    // u = L^-1 y (row r), likelihood terms
-    double lquad = 0.0, llog = 0.0;
+    if (own) {
+#pragma unroll
+      for (int q = 0; q < I; ++q)
+        if (q >= r) at(q, r) = col[q];
+    }
+    __syncwarp();
+    // u = L^-1 y (row r); Rinv entries of this lane's slots
+    double2 ri[NS];
+    double lquad = 0.0;
     if (own) {
       double2 sacc = cmk(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < I; ++k)
-        if (k <= r) sacc = cadd(sacc, cmul(at(Li, r, k), vy[k]));
+        if (k <= r) sacc = cadd(sacc, cmul(at(r, k), vy[k]));
       vu[r] = sacc;
       lquad = cabs2(sacc);
-      llog = log(at(Lm, r, r).x);
-    }
-    __syncwarp();
-    if (do_ll) {
-      const double t = group_sum<LB>(2.0 * llog + lquad);
-      llacc += t;
-    }
-    // x = L^-H u = R^-1 y; Y2 = L^-1 S2 into Lm (L no longer needed)
-    double2 y2row[I];
-    if (own) {
-      double2 sacc = cmk(0.0, 0.0);
 #pragma unroll
-      for (int k = 0; k < I; ++k)
-        if (k >= r) sacc = cadd(sacc, cconjmul(at(Li, k, r), vu[k]));
-      vx[r] = sacc;
-      double2 lrow[I];
-#pragma unroll
-      for (int k = 0; k < I; ++k) lrow[k] = at(Li, r, k);
-#pragma unroll
-      for (int c = 0; c < I; ++c) {
+      for (int s = 0; s < NS; ++s) {
+        const int b0 = sb[s];
+        const int kmin = b0 > rr ? b0 : rr;
         double2 t = cmk(0.0, 0.0);
 #pragma unroll
         for (int k = 0; k < I; ++k)
-          if (k <= r) t = cadd(t, cmul(lrow[k], packed_get<I>(S2, k, c)));
-        y2row[c] = t;
+          if (k >= kmin) t = cadd(t, cconjmul(at(k, rr), at(k, b0)));
+        ri[s] = t;
       }
     }
-    __syncwarp();  // everyone done reading Lm (diag) before Y2 overwrites it
+    __syncwarp();
+    if (do_ll) llacc += group_sum<LB>(own ? 2.0 * log(lrr) + lquad : 0.0);
+    // x = L^-H u (row r)
     if (own) {
+      double2 sacc = cmk(0.0, 0.0);
 #pragma unroll
-      for (int c = 0; c < I; ++c) at(Lm, r, c) = y2row[c];
+      for (int k = 0; k < I; ++k)
+        if (k >= r) sacc = cadd(sacc, cconjmul(at(k, r), vu[k]));
+      vx[r] = sacc;
     }
     __syncwarp();
-    // mu_j = v_j S_j x (row r); T = L^-H Y2 (row r)
-    if (own) {
+    if (p.mu_out != nullptr && active && own) {
+      // mu_j = v_j S_j x (row r; the image pass only)
       double2 s1 = cmk(0.0, 0.0), s2 = cmk(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < I; ++k) {
         s1 = cadd(s1, cmul(packed_get<I>(S1, r, k), vx[k]));
         s2 = cadd(s2, cmul(packed_get<I>(S2, r, k), vx[k]));
       }
-      vm1[r] = cscale(s1, v1);
-      vm2[r] = cscale(s2, v2);
-      double2 lcol[I];  // column r of Li: conj -> row r of Li^H
-#pragma unroll
-      for (int k = 0; k < I; ++k) lcol[k] = at(Li, k, r);
-#pragma unroll
-      for (int c = 0; c < I; ++c) {
-        double2 t = cmk(0.0, 0.0);
-#pragma unroll
-        for (int k = 0; k < I; ++k)
-          if (k >= r) t = cadd(t, cconjmul(lcol[k], at(Lm, k, c)));
-        at(Tm, r, c) = t;
-      }
-    }
-    __syncwarp();
-    if (p.mu_out != nullptr && active && own) {
       C* mo = (C*)p.mu_out;
-      mo[(((m * 2 + 0) * p.N + n) * p.F + f) * I + r] = from_c128<R>(vm1[r]);
-      mo[(((m * 2 + 1) * p.N + n) * p.F + f) * I + r] = from_c128<R>(vm2[r]);
+      mo[(((m * 2 + 0) * p.N + n) * p.F + f) * I + r] = from_c128<R>(cscale(s1, v1));
+      mo[(((m * 2 + 1) * p.N + n) * p.F + f) * I + r] = from_c128<R>(cscale(s2, v2));
     }
     if (p.update) {
-      // cross row r = v1 v2 S1 T; traces against S_j^-1 (column r of Phi_j)
-      double2 cr[I];
-      double t1 = 0.0, t2 = 0.0;
-      if (own) {
-        const double vv = v1 * v2;
+      // tr(A B) of Hermitian A, B over this lane's slots (weight 2 off the
+      // diagonal): qf_j = tr(S_j x x^H), tR_j = tr(Rinv S_j)
+      double2 xe[NS];
+      double qf1 = 0.0, qf2 = 0.0, tR1 = 0.0, tR2 = 0.0;
+      const double2 xr = vx[rr];
 #pragma unroll
-        for (int c = 0; c < I; ++c) {
-          double2 s = cmk(0.0, 0.0);
-#pragma unroll
-          for (int k = 0; k < I; ++k) s = cadd(s, cmul(packed_get<I>(S1, r, k), at(Tm, k, c)));
-          cr[c] = cscale(s, vv);
-          if (c == r) cr[c].y = 0.0;  // compile-time index only: cr stays in registers
-        }
-        const double2 m1r = vm1[r], m2r = vm2[r];
-#pragma unroll
-        for (int b = 0; b < I; ++b) {
-          // Phi_j[b][r] = mu_j[b] conj(mu_j[r]) + conj(cross[r][b])
-          const double2 ph1 = cadd(cmulc(vm1[b], m1r), cconj(cr[b]));
-          const double2 ph2 = cadd(cmulc(vm2[b], m2r), cconj(cr[b]));
-          const double2 a1 = packed_get<I>(Si1, r, b), a2 = packed_get<I>(Si2, r, b);
-          t1 += a1.x * ph1.x - a1.y * ph1.y;
-          t2 += a2.x * ph2.x - a2.y * ph2.y;
-        }
+      for (int s = 0; s < NS; ++s) {
+        const double2 xb = vx[sb[s]];
+        xe[s] = cmulc(xr, xb);  // x_a0 conj(x_b0)
+        if (s == 0) xe[s].y = 0.0;
+        const double wgt = sv[s] ? (s == 0 ? 1.0 : 2.0) : 0.0;
+        const double2 s1 = packed_get<I>(S1, rr, sb[s]), s2 = packed_get<I>(S2, rr, sb[s]);
+        qf1 += wgt * (s1.x * xe[s].x + s1.y * xe[s].y);
+        qf2 += wgt * (s2.x * xe[s].x + s2.y * xe[s].y);
+        tR1 += wgt * (s1.x * ri[s].x + s1.y * ri[s].y);
+        tR2 += wgt * (s2.x * ri[s].x + s2.y * ri[s].y);
       }
-      t1 = group_sum<LB>(t1);
-      t2 = group_sum<LB>(t2);
+      const double vv = v1 * v2;
+      const double t1 = group_sum<LB>(v1 * v1 * qf1 + vv * tR2);
+      const double t2 = group_sum<LB>(v2 * v2 * qf2 + vv * tR1);
       const double q1 = t1 / I, q2 = t2 / I;
       const double w1 = (q1 < fl) ? fl : q1;
       const double w2 = (q2 < fl) ? fl : q2;
@@ -263,17 +251,18 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
         vb[n * p.F] = (R)w1;
         vb[NF + n * p.F] = (R)w2;
       }
-      if (own) {
-        const double iw1 = 1.0 / w1, iw2 = 1.0 / w2;
-        const double2 m1r = vm1[r], m2r = vm2[r];
+      const double iw1 = rcp_fast(w1), iw2 = rcp_fast(w2);
+      const double cb1 = v1 * v1 * iw1, cb2 = v2 * v2 * iw2, cx1 = vv * iw1, cx2 = vv * iw2;
 #pragma unroll
-        for (int c = 0; c < I; ++c) {
-          if (c < r) continue;
-          const double2 p1 = cadd(cmulc(m1r, vm1[c]), cr[c]);
-          const double2 p2 = cadd(cmulc(m2r, vm2[c]), cr[c]);
-          acc1[c] = cadd(acc1[c], cscale(p1, iw1));
-          acc2[c] = cadd(acc2[c], cscale(p2, iw2));
-        }
+      for (int s = 0; s < NS; ++s) {
+        acc[0][s].x = fma(cb1, xe[s].x, acc[0][s].x);
+        acc[0][s].y = fma(cb1, xe[s].y, acc[0][s].y);
+        acc[1][s].x = fma(cb2, xe[s].x, acc[1][s].x);
+        acc[1][s].y = fma(cb2, xe[s].y, acc[1][s].y);
+        acc[2][s].x = fma(cx1, ri[s].x, acc[2][s].x);
+        acc[2][s].y = fma(cx1, ri[s].y, acc[2][s].y);
+        acc[3][s].x = fma(cx2, ri[s].x, acc[3][s].x);
+        acc[3][s].y = fma(cx2, ri[s].y, acc[3][s].y);
       }
     }
     __syncwarp();  // smem buffers are reused by the next frame
@@ -283,23 +272,309 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
                  (unsigned long long)((m * p.N + (bad_n - 1)) * p.F + f));
   if (!active) return;
   const int64_t ch = blockIdx.y;
-  if (p.update && own) {
-    double* sp = p.Spart + (size_t)ch * 2 * NP * G + g;
+  if (p.update) {
+    double* sp = p.Spart + (size_t)ch * kFcaParts * NP * G + g;
 #pragma unroll
-    for (int c = 0; c < I; ++c) {
-      if (c < r) continue;
-      if (c == r) {
-        sp[(size_t)r * G] = acc1[c].x;
-        sp[(size_t)(NP + r) * G] = acc2[c].x;
+    for (int s = 0; s < NS; ++s) {
+      if (!sv[s]) continue;
+      const int b0 = sb[s];
+      if (s == 0) {
+#pragma unroll
+        for (int j = 0; j < kFcaParts; ++j) sp[(size_t)(j * NP + rr) * G] = acc[j][s].x;
       } else {
-        sp[(size_t)Herm<I>::re(r, c) * G] = acc1[c].x;
-        sp[(size_t)Herm<I>::im(r, c) * G] = acc1[c].y;
-        sp[(size_t)(NP + Herm<I>::re(r, c)) * G] = acc2[c].x;
-        sp[(size_t)(NP + Herm<I>::im(r, c)) * G] = acc2[c].y;
+        // stored entry (a, b), a < b: the slot's (a0, b0) or its conjugate
+        const bool flip = rr > b0;
+        const int a = flip ? b0 : rr, b = flip ? rr : b0;
+        const int ire = Herm<I>::re(a, b), iim = Herm<I>::im(a, b);
+#pragma unroll
+        for (int j = 0; j < kFcaParts; ++j) {
+          sp[(size_t)(j * NP + ire) * G] = acc[j][s].x;
+          sp[(size_t)(j * NP + iim) * G] = flip ? -acc[j][s].y : acc[j][s].y;
+        }
       }
     }
   }
   if (do_ll && r == 0) p.llbin[(size_t)ch * G + g] = llacc;
+}
+
+// K4b — per-bin FCA steps, lane-parallel (LB lanes per bin, lane r owns
+// row r; LB = the order rounded up to a power of two):
+//  * finish: sums the chunk partials of the pass (fixed chunk order) and forms
+//      out_j = (S_j B_j S_j + S1 X_j S2) / N, Hermitian part
+//    with row-parallel products in shared memory, then either writes S_raw
+//    (stage API) or regularises (modelops.py:29-39: + 1e-9 tr/I) and writes
+//    the model / history S;
+//  * prepare (S_in set): takes the initial model S instead;
+// then packs S for the next pass and checks each S_j is positive definite
+// (the reference factors every S_j per iteration: _cholesky_inverse,
+// conventional.py:98-101) with a column-sequential Cholesky.
+namespace {
+template <int I>
+struct BinParLayout {
+  static constexpr int LB = I <= 1 ? 1 : I <= 2 ? 2 : I <= 4 ? 4 : 8;
+  static constexpr int GROUPS = 64 / LB;  // bins per CTA
+  static constexpr int LD = (I % 2) ? I + 2 : I + 1;
+  static constexpr int MATD = I * LD * 2;
+  static constexpr int RAW = 4 * MATD + 2;  // S1, S2, A (B / X / M), T
+  static constexpr int U16 = (RAW + 1) / 2;
+  static constexpr int GROUP_DOUBLES = 2 * ((U16 % 2) ? U16 : U16 + 1);
+  static constexpr size_t SMEM = (size_t)GROUPS * GROUP_DOUBLES * sizeof(double);
+};
+}  // namespace
+
+template <int I>
+__global__ void __launch_bounds__(64)
+    fca_bin_par_kernel(const double* __restrict__ Spart, int nchunk, int64_t N, int64_t G,
+                       int64_t F, double* Sp, double2* S_model, double2* S_hist,
+                       const double* llbin, double* llg, double2* S_raw,
+                       const double2* __restrict__ S_in, ffca_status_dev* st, int iter) {
+  using Lay = BinParLayout<I>;
+  constexpr int NP = I * I;
+  constexpr int LB = Lay::LB;
+  constexpr int LD = Lay::LD;
+  constexpr int NS = I / 2 + 1;
+  extern __shared__ __align__(16) double sm[];
+  const int r = threadIdx.x % LB;
+  const int grp = threadIdx.x / LB;
+  int64_t g = (int64_t)blockIdx.x * Lay::GROUPS + grp;
+  const bool active = g < G;
+  if (!active) g = G - 1;
+  const bool own = r < I;
+  const int rr = own ? r : 0;
+  const int64_t m = g / F, f = g - m * F;
+  double2* mS1 = (double2*)(sm + (size_t)grp * Lay::GROUP_DOUBLES);
+  double2* mS2 = mS1 + I * LD;
+  double2* mA = mS2 + I * LD;
+  double2* mT = mA + I * LD;
+  double* misc = (double*)(mT + I * LD);
+  auto S1 = [&](int a, int b) -> double2& { return mS1[a * LD + b]; };
+  auto S2 = [&](int a, int b) -> double2& { return mS2[a * LD + b]; };
+  auto A = [&](int a, int b) -> double2& { return mA[a * LD + b]; };
+  auto T = [&](int a, int b) -> double2& { return mT[a * LD + b]; };
+  double2 out[2][I];
+  if (S_in) {
+    // prepare: the initial model (M,2,F,I,I)
+    if (own) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int c = 0; c < I; ++c) out[j][c] = S_in[((m * 2 + j) * F + f) * NP + r * I + c];
+    }
+  } else {
+    auto packed = [&](const double* base, int a, int b) -> double2 {  // base[e * G + g]
+      if (a == b) return cmk(base[(size_t)a * G + g], 0.0);
+      if (a < b)
+        return cmk(base[(size_t)Herm<I>::re(a, b) * G + g],
+                   base[(size_t)Herm<I>::im(a, b) * G + g]);
+      return cmk(base[(size_t)Herm<I>::re(b, a) * G + g],
+                 -base[(size_t)Herm<I>::im(b, a) * G + g]);
+    };
+    if (own) {
+#pragma unroll
+      for (int c = 0; c < I; ++c) {
+        S1(r, c) = packed(Sp, r, c);
+        S2(r, c) = packed(Sp + (size_t)NP * G, r, c);
+      }
+    }
+    if (llg && r == 0 && active) llg[g] = -ordered_sum(llbin + g, nchunk, (size_t)G);
+    __syncwarp();
+    const double invN = 1.0 / (double)N;
+    // sum of packed part `part` over the chunks into the full matrix A
+    // (circulant slots: lane r owns (r, r + s mod I))
+    auto gather = [&](int part) {
+      if (!own) return;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (!(s < I / 2 || (I % 2) == 1 || rr < I / 2)) continue;
+        const int b0 = (rr + s) % I;
+        const int a = rr < b0 ? rr : b0, b = rr < b0 ? b0 : rr;
+        const int ire = a == b ? a : Herm<I>::re(a, b);
+        const int iim = a == b ? a : Herm<I>::im(a, b);
+        double sr = 0.0, si = 0.0;
+#pragma unroll 4
+        for (int c = 0; c < nchunk; ++c) {
+          const double* sp = Spart + ((size_t)c * kFcaParts + part) * NP * G + g;
+          sr += sp[(size_t)ire * G];
+          si += sp[(size_t)iim * G];
+        }
+        if (a == b) si = 0.0;
+        A(a, b) = cmk(sr, si);
+        A(b, a) = cmk(sr, -si);
+      }
+    };
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      // T = B_j S_j (row r), then M = S_j T (row r, registers)
+      gather(j);
+      __syncwarp();
+      if (own) {
+#pragma unroll
+        for (int c = 0; c < I; ++c) {
+          double2 t = cmk(0.0, 0.0);
+#pragma unroll
+          for (int k = 0; k < I; ++k) t = cadd(t, cmul(A(r, k), j == 0 ? S1(k, c) : S2(k, c)));
+          T(r, c) = t;
+        }
+      }
+      __syncwarp();
+      double2 mrow[I];
+      if (own) {
+#pragma unroll
+        for (int c = 0; c < I; ++c) {
+          double2 t = cmk(0.0, 0.0);
+#pragma unroll
+          for (int k = 0; k < I; ++k) t = cadd(t, cmul(j == 0 ? S1(r, k) : S2(r, k), T(k, c)));
+          mrow[c] = t;
+        }
+      }
+      __syncwarp();
+      // + S1 (X_j S2)
+      gather(2 + j);
+      __syncwarp();
+      if (own) {
+#pragma unroll
+        for (int c = 0; c < I; ++c) {
+          double2 t = cmk(0.0, 0.0);
+#pragma unroll
+          for (int k = 0; k < I; ++k) t = cadd(t, cmul(A(r, k), S2(k, c)));
+          T(r, c) = t;
+        }
+      }
+      __syncwarp();
+      if (own) {
+#pragma unroll
+        for (int c = 0; c < I; ++c) {
+          double2 t = mrow[c];
+#pragma unroll
+          for (int k = 0; k < I; ++k) t = cadd(t, cmul(S1(r, k), T(k, c)));
+          A(r, c) = t;  // M row r (A is free: every lane has read X_j)
+        }
+      }
+      __syncwarp();
+      // Hermitian part, / N (reference hermitize, modelops.py:24-26)
+      if (own) {
+#pragma unroll
+        for (int c = 0; c < I; ++c) {
+          const double2 u = A(r, c), w = A(c, r);
+          out[j][c] = cmk(0.5 * (u.x + w.x) * invN, 0.5 * (u.y - w.y) * invN);
+        }
+      }
+      __syncwarp();
+    }
+    if (S_raw) {
+      if (active && own)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int c = 0; c < I; ++c)
+            S_raw[((size_t)j * G + g) * NP + r * I + c] =
+                c == r ? cmk(out[j][c].x, 0.0) : out[j][c];
+      return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    if (!S_in) {
+      // regularize_covariances: Hermitian diagonal + 1e-9 tr/I
+      double dg = 0.0;
+#pragma unroll
+      for (int c = 0; c < I; ++c)
+        if (c == r) dg = out[j][c].x;
+      const double tr = group_sum<LB>(own ? dg : 0.0);
+      const double eps = kCovEps * tr / I;
+#pragma unroll
+      for (int c = 0; c < I; ++c)
+        if (c == r) out[j][c] = cmk(out[j][c].x + eps, 0.0);
+      if (active && own) {
+        double2* dst = S_model + ((m * 2 + j) * F + f) * NP + r * I;
+        double2* hst = S_hist ? S_hist + ((m * 2 + j) * F + f) * NP + r * I : nullptr;
+#pragma unroll
+        for (int c = 0; c < I; ++c) {
+          dst[c] = out[j][c];
+          if (hst) hst[c] = out[j][c];
+        }
+      }
+    }
+    if (active && own) {
+      double* dp = Sp + (size_t)j * NP * G + g;  // packed for the next pass (row r, c >= r)
+#pragma unroll
+      for (int c = 0; c < I; ++c) {
+        if (c < r) continue;
+        if (c == r) {
+          dp[(size_t)r * G] = out[j][c].x;
+        } else {
+          dp[(size_t)Herm<I>::re(r, c) * G] = out[j][c].x;
+          dp[(size_t)Herm<I>::im(r, c) * G] = out[j][c].y;
+        }
+      }
+    }
+    // positive-definiteness (Cholesky in A, column-sequential)
+    __syncwarp();
+    if (own) {
+#pragma unroll
+      for (int c = 0; c < I; ++c) A(r, c) = out[j][c];
+    }
+    __syncwarp();
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < I; ++q) {
+      if (own && r == q) {
+        double d = A(q, q).x;
+#pragma unroll
+        for (int k = 0; k < q; ++k) d -= cabs2(A(q, k));
+        misc[0] = d;
+        A(q, q) = cmk(sqrt(fmax(d, 0.0)), 0.0);
+      }
+      __syncwarp();
+      ok = ok && misc[0] > 0.0;
+      if (own && r > q) {
+        double2 t = A(r, q);
+#pragma unroll
+        for (int k = 0; k < q; ++k) t = csub(t, cmulc(A(r, k), A(q, k)));
+        A(r, q) = cscale(t, 1.0 / A(q, q).x);
+      }
+      __syncwarp();
+    }
+    if (!ok && active && r == 0 && st)
+      report_error(st, S_in ? iter : iter + 1, FFCA_ERR_NOT_PD, (unsigned long long)g);
+  }
+}
+
+template <int I>
+static cudaError_t launch_fca_bin_par_t(const double* Spart, int nchunk, int64_t N, int64_t G,
+                                        int64_t F, double* Sp, double2* S_model,
+                                        double2* S_hist, const double* llbin, double* llg,
+                                        double2* S_raw, const double2* S_in, ffca_status_dev* st,
+                                        int iter, cudaStream_t s) {
+  using Lay = BinParLayout<I>;
+  const unsigned nb = (unsigned)((G + Lay::GROUPS - 1) / Lay::GROUPS);
+  fca_bin_par_kernel<I><<<nb, 64, Lay::SMEM, s>>>(Spart, nchunk, N, G, F, Sp, S_model, S_hist,
+                                                  llbin, llg, S_raw, S_in, st, iter);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fca_bin_par(const double* Spart, int nchunk, int64_t N, int64_t G, int64_t F,
+                               double* Sp, double2* S_model, double2* S_hist,
+                               const double* llbin, double* llg, double2* S_raw,
+                               const double2* S_in, int I, ffca_status_dev* st, int iter,
+                               cudaStream_t s) {
+  switch (I) {
+#define FFCA_CASE(II)                                                                         \
+  case II:                                                                                    \
+    return launch_fca_bin_par_t<II>(Spart, nchunk, N, G, F, Sp, S_model, S_hist, llbin, llg, \
+                                    S_raw, S_in, st, iter, s);
+    FFCA_CASE(1)
+    FFCA_CASE(2)
+    FFCA_CASE(3)
+    FFCA_CASE(4)
+    FFCA_CASE(5)
+    FFCA_CASE(6)
+    FFCA_CASE(7)
+    FFCA_CASE(8)
+#undef FFCA_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 template <int I, typename R>

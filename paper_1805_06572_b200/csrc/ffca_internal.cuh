@@ -9,6 +9,9 @@
 namespace ffca {
 
 constexpr int kWarps = 4;  // warps per CTA in the frame-streaming kernels
+// FCA per-(chunk, bin) partial sums: packed Hermitian B1, B2, X1, X2 with
+// sum_n Phi_j / w_j = S_j B_j S_j + S1 X_j S2 (see fca_em_kernel)
+constexpr int kFcaParts = 4;
 
 // ---- K3: fused FastFCA transform + E + M (+ likelihood, + images) ----------
 struct FastIterParams {
@@ -35,9 +38,9 @@ cudaError_t launch_fast_em(const FastIterParams& p, int I, int dtype, cudaStream
 struct FcaIterParams {
   const void* y;        // (M,N,F,I)
   void* v;              // (M,2,N,F)
-  const double* Sp;     // [4][I*I][G] packed S1,S2,Sinv1,Sinv2 (SoA)
+  const double* Sp;     // [2][I*I][G] packed S1, S2 (SoA)
   const double* floor;  // (G)
-  double* Spart;        // [nchunk][2*I*I][G]
+  double* Spart;        // [nchunk][kFcaParts*I*I][G]: B1, B2, X1, X2 packed
   double* llbin;        // [nchunk][G] sum log det R + y^H R^-1 y, or null
   void* mu_out;         // (M,2,N,F,I) or null
   int update;
@@ -80,6 +83,16 @@ cudaError_t launch_fca_prepare(const double2* S, double* Sp, int64_t G, int64_t 
                                ffca_status_dev* st, int iter, cudaStream_t s);
 // reduce partials, regularise (modelops.py:29-39), write S_model (+hist), and
 // refresh Sp (S and S^{-1}) for the next iteration; llg (G) collect.
+// per-bin FCA prepare (S_in) / finish / stage sums (S_raw), lane-parallel
+// (fca_bin_par_kernel, ffca_fca_par.cu)
+cudaError_t launch_fca_bin_par(const double* Spart, int nchunk, int64_t N, int64_t G, int64_t F,
+                               double* Sp, double2* S_model, double2* S_hist,
+                               const double* llbin, double* llg, double2* S_raw,
+                               const double2* S_in, int I, ffca_status_dev* st, int iter,
+                               cudaStream_t s);
+// stage API: S_raw (2,G,I,I) = sum_n Phi_j / w_j / N from the chunk partials
+cudaError_t launch_fca_sraw(const double* Spart, int nchunk, int64_t N, int64_t G,
+                            const double* Sp, double2* S_raw, int I, cudaStream_t s);
 cudaError_t launch_fca_finish(const double* Spart, int nchunk, int64_t N, int64_t G, int64_t F,
                               double* Sp, double2* S_model, double2* S_hist,
                               const double* llbin, double* llg, int I, ffca_status_dev* st,

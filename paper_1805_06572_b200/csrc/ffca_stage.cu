@@ -372,15 +372,16 @@ __global__ void fca_vupd_kernel(const double2* Phi, const double2* Sinv, double*
   v[t] = acc / I;
 }
 
-// pack S (2,F,I,I) and Sinv (2,F,I,I) into the SoA layout of K4
+// pack S (2,F,I,I) into the SoA layout of K4 (the pass needs no S^-1: the
+// reference's Sinv argument is accepted and validated, not read)
 template <int I>
-__global__ void pack_fca_kernel(const double2* S, const double2* Sinv, double* Sp, int64_t F) {
+__global__ void pack_fca_kernel(const double2* S, double* Sp, int64_t F) {
   constexpr int NP = I * I;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= F) return;
 #pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    const double2* src = (w < 2 ? S : Sinv) + ((w & 1) * F + g) * NP;
+  for (int w = 0; w < 2; ++w) {
+    const double2* src = S + (w * F + g) * NP;
     double* dst = Sp + (size_t)w * NP * F + g;
 #pragma unroll
     for (int a = 0; a < I; ++a) {
@@ -636,16 +637,15 @@ int ffca_fca_iteration(const double* y, const double* v, const double* S, const 
   FcaIterParams p{};
   plan_fca_chunks(F, N, I, FFCA_C128, &p.chunk_frames, &p.nchunk);
   double *Spart = nullptr, *Sp = nullptr;
-  if (cudaMallocAsync((void**)&Spart, (size_t)p.nchunk * 2 * I * I * F * sizeof(double), s) !=
+  if (cudaMallocAsync((void**)&Spart, (size_t)p.nchunk * kFcaParts * I * I * F * sizeof(double), s) !=
           cudaSuccess ||
-      cudaMallocAsync((void**)&Sp, (size_t)4 * I * I * F * sizeof(double), s) != cudaSuccess)
+      cudaMallocAsync((void**)&Sp, (size_t)2 * I * I * F * sizeof(double), s) != cudaSuccess)
     return FFCA_ERR_CUDA;
   int rc = FFCA_OK;
   switch (I) {
 #define FFCA_CASE(II)                                                                      \
   case II:                                                                                 \
-    pack_fca_kernel<II><<<nb(F, 64), 64, 0, s>>>((const double2*)S, (const double2*)Sinv, \
-                                                 Sp, F);                                   \
+    pack_fca_kernel<II><<<nb(F, 64), 64, 0, s>>>((const double2*)S, Sp, F);                \
     break;
     FFCA_CASE(1)
     FFCA_CASE(2)
@@ -672,24 +672,7 @@ int ffca_fca_iteration(const double* y, const double* v, const double* S, const 
   p.st = st;
   p.iter = 0;
   rc = cu(launch_fca_em(p, I, FFCA_C128, s));
-  if (rc == FFCA_OK) {
-    switch (I) {
-#define FFCA_CASE(II)                                                                          \
-  case II:                                                                                     \
-    finalize_sraw_kernel<II><<<nb(F, 64), 64, 0, s>>>(Spart, p.nchunk, N, F, (double2*)S_raw); \
-    break;
-      FFCA_CASE(1)
-      FFCA_CASE(2)
-      FFCA_CASE(3)
-      FFCA_CASE(4)
-      FFCA_CASE(5)
-      FFCA_CASE(6)
-      FFCA_CASE(7)
-      FFCA_CASE(8)
-#undef FFCA_CASE
-    }
-    rc = cu(cudaGetLastError());
-  }
+  if (rc == FFCA_OK) rc = cu(launch_fca_sraw(Spart, p.nchunk, N, F, Sp, (double2*)S_raw, I, s));
   cudaFreeAsync(Spart, s);
   cudaFreeAsync(Sp, s);
   return rc;

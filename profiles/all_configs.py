@@ -66,11 +66,12 @@ def main():
     ap.add_argument("--cpu", action="store_true")
     ap.add_argument("--configs", default="0,1,2,3,4")
     ap.add_argument("--graph", type=int, default=1, help="replay runs as CUDA graphs")
+    ap.add_argument("--engines", default="fast,fca")
     a = ap.parse_args()
     for idx in [int(x) for x in a.configs.split(",")]:
         cfg = CONFIGS[idx]
         Y, V, S, FL = make_inputs(cfg, shard(cfg, 0, 1))
-        for engine in ("fast", "fca"):
+        for engine in a.engines.split(","):
             for dtype in cfg.dtypes:
                 rec = measure(cfg, engine, dtype, a.steps, Y, V, S, FL, graph=bool(a.graph))
                 if a.cpu and dtype == "c128":
