@@ -102,6 +102,9 @@ typedef struct ffca_run_args {
                                results however the bins / mixtures are sharded. */
   void* const* kernel_events; /* optional cudaEvent_t[2L]: before/after each fused streaming
                                  pass (the dominant kernel), for roofline timing */
+  const void* v_in; /* optional (M,2,N,F) initial powers, read only: the first pass reads
+                       them here and writes `v` (which then need not be initialised);
+                       NULL = `v` holds the initial powers (in place) */
 } ffca_run_args;
 
 /* ---- library info ------------------------------------------------------ */

@@ -85,13 +85,15 @@ def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, hi
                 f"out[{key!r}] must be a contiguous CUDA {dt} tensor of shape {shp}, got "
                 f"{t.dtype} {tuple(t.shape)}")
     v = D.to_device(v0, rtype)
+    v_in = None  # initial powers read by the first pass (the run writes `v`)
     if res.get("v") is not None:
-        res["v"].copy_(v)  # preallocated work buffer: the run updates v in place
-        v = res["v"]
+        v_in, v = v, res["v"]  # preallocated output: no device copy of the init
     elif D.is_tensor(v0) and v.data_ptr() == v0.data_ptr():
-        v = v.clone()  # never clobber the caller's init
+        v_in, v = v, torch.empty_like(v)  # never clobber the caller's init
     S0 = D.to_device(S0, torch.complex128)
     fl = D.to_device(v_floor, torch.float64)
+    if v_in is not None and (tuple(v_in.shape) != (M, 2, N, F) or not v_in.is_contiguous()):
+        raise ConfigurationError(f"v must be (M, 2, N, F) = {(M, 2, N, F)}, got {tuple(v_in.shape)}")
     if tuple(v.shape) != (M, 2, N, F) or tuple(S0.shape) != (M, 2, F, I, I) or \
             tuple(fl.shape) != (M, F):
         raise ConfigurationError(
@@ -143,7 +145,8 @@ def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, hi
         iter_events=ctypes.cast(ev_arr, ctypes.c_void_p).value if ev_arr is not None else None,
         chunk_frames=int(chunk_frames),
         kernel_events=ctypes.cast(kev_arr, ctypes.c_void_p).value if kev_arr is not None
-        else None)
+        else None,
+        v_in=D.ptr(v_in).value)
     fn = lib.ffca_fastfca_run if fast else lib.ffca_fca_run
     D.check_rc(fn(ctypes.byref(args), D.stream_handle()), fn.__name__)
     run = DeviceRun("FastFCA" if fast else "FCA", img, v, S_out, ll, S_hist, v_hist, [], ws)

@@ -55,7 +55,7 @@ class RunArgs(ctypes.Structure):
         ("y", c_vp), ("v", c_vp), ("S0", c_vp), ("v_floor", c_vp), ("images", c_vp),
         ("S_out", c_vp), ("loglik", c_vp), ("S_hist", c_vp), ("v_hist", c_vp),
         ("workspace", c_vp), ("workspace_bytes", c_sz), ("iter_events", c_vp),
-        ("chunk_frames", c_i64), ("kernel_events", c_vp),
+        ("chunk_frames", c_i64), ("kernel_events", c_vp), ("v_in", c_vp),
     ]
 
 

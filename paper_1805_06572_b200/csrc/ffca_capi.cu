@@ -328,6 +328,11 @@ static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
   p.chunk_frames = w.chunk_frames;
   p.nchunk = w.nchunk;
   p.st = w.st;
+  // v_in: the first pass reads the initial powers there and writes v (no copy)
+  const bool vin = a->v_in && a->v_in != a->v;
+  if (vin && L == 0)
+    FFCA_TRY(cudaMemcpyAsync(a->v, a->v_in, vslice * real_size(a->dtype),
+                             cudaMemcpyDeviceToDevice, s));
 
   if (L == 0) {
     if (ev) FFCA_TRY(cudaEventRecord(ev[0], s));
@@ -347,8 +352,10 @@ static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
       p.mu_out = (last && (fl & FFCA_FLAG_IMAGES)) ? a->images : nullptr;
       p.mu_back = 1;
       p.iter = l + 1;
+      p.v_src = (vin && l == 0) ? a->v_in : nullptr;
       if (kev) FFCA_TRY(cudaEventRecord(kev[2 * l], s));
       FFCA_TRY(launch_fast_em(p, I, a->dtype, s));
+      p.v_src = nullptr;
       if (kev) FFCA_TRY(cudaEventRecord(kev[2 * l + 1], s));
       if (hist && a->v_hist)
         FFCA_TRY(cudaMemcpyAsync((char*)a->v_hist + (size_t)l * vslice * real_size(a->dtype),
@@ -416,6 +423,10 @@ static int fca_enqueue(const ffca_run_args* a, cudaStream_t s) {
   p.chunk_frames = w.chunk_frames;
   p.nchunk = w.nchunk;
   p.st = w.st;
+  const bool vin = a->v_in && a->v_in != a->v;
+  if (vin && L == 0)
+    FFCA_TRY(cudaMemcpyAsync(a->v, a->v_in, vslice * real_size(a->dtype),
+                             cudaMemcpyDeviceToDevice, s));
   if (L == 0) {
     if (ev) FFCA_TRY(cudaEventRecord(ev[0], s));
     p.update = 0;
@@ -432,8 +443,10 @@ static int fca_enqueue(const ffca_run_args* a, cudaStream_t s) {
       const bool last = (l == L - 1);
       p.mu_out = (last && (fl & FFCA_FLAG_IMAGES)) ? a->images : nullptr;
       p.iter = l + 1;
+      p.v_src = (vin && l == 0) ? a->v_in : nullptr;
       if (kev) FFCA_TRY(cudaEventRecord(kev[2 * l], s));
       FFCA_TRY(launch_fca_em(p, I, a->dtype, s));
+      p.v_src = nullptr;
       if (kev) FFCA_TRY(cudaEventRecord(kev[2 * l + 1], s));
       if (hist && a->v_hist)
         FFCA_TRY(cudaMemcpyAsync((char*)a->v_hist + (size_t)l * vslice * real_size(a->dtype),

@@ -205,7 +205,8 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
   const int64_t n0 = (int64_t)blockIdx.y * p.chunk_frames;
   const int64_t n1 = min(p.N, n0 + p.chunk_frames);
   const int64_t NF = p.N * p.F;
-  R* __restrict__ vb = (R*)p.v + m * 2 * NF + f;
+  R* vb = (R*)p.v + m * 2 * NF + f;  // no __restrict__: may alias vr (in place)
+  const R* vr = (p.v_src ? (const R*)p.v_src : (const R*)p.v) + m * 2 * NF + f;
 
   // P lives in shared memory (bin-minor SoA after the frame ring): the 4
   // warps of the CTA work on the same 32 bins, so one 16*I*I-byte column per
@@ -311,11 +312,11 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
     }
     unsigned char* vs = slot + 32 * Slot::YB;
     if constexpr (sizeof(R) == 8) {
-      cp_async8(vs + 8 * lane, vb + n * p.F);
-      cp_async8(vs + 256 + 8 * lane, vb + NF + n * p.F);
+      cp_async8(vs + 8 * lane, vr + n * p.F);
+      cp_async8(vs + 256 + 8 * lane, vr + NF + n * p.F);
     } else {
-      cp_async4(vs + 4 * lane, vb + n * p.F);
-      cp_async4(vs + 128 + 4 * lane, vb + NF + n * p.F);
+      cp_async4(vs + 4 * lane, vr + n * p.F);
+      cp_async4(vs + 128 + 4 * lane, vr + NF + n * p.F);
     }
   };
 

@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, FAST_PAR_MINB) f
   const int64_t n1 = min(p.N, n0 + p.chunk_frames);
   const int64_t NF = p.N * p.F;
   const C* __restrict__ yb = (const C*)p.y + (m * p.N * p.F + f) * I;
-  R* __restrict__ vb = (R*)p.v + m * 2 * NF + f;
+  R* vb = (R*)p.v + m * 2 * NF + f;  // no __restrict__: may alias vr (in place)
+  const R* vr = (p.v_src ? (const R*)p.v_src : (const R*)p.v) + m * 2 * NF + f;
   FFCA_CHECK(g >= 0 && g < G && m < p.M && n0 >= 0 && n1 <= p.N);
 #ifdef FFCA_DEBUG_BOUNDS
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
@@ -128,11 +129,11 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, FAST_PAR_MINB) f
     else
       cp_async8(slot, yb + n * p.F * I + rr);
     if constexpr (VB == 8) {
-      cp_async8(slot + YB, vb + n * p.F);
-      cp_async8(slot + YB + 8, vb + NF + n * p.F);
+      cp_async8(slot + YB, vr + n * p.F);
+      cp_async8(slot + YB + 8, vr + NF + n * p.F);
     } else {
-      cp_async4(slot + YB, vb + n * p.F);
-      cp_async4(slot + YB + 4, vb + NF + n * p.F);
+      cp_async4(slot + YB, vr + n * p.F);
+      cp_async4(slot + YB + 4, vr + NF + n * p.F);
     }
   };
 #pragma unroll

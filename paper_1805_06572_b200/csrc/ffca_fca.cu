@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
   const int64_t n1 = min(p.N, n0 + p.chunk_frames);
   const int64_t NF = p.N * p.F;
   const C* __restrict__ yb = (const C*)p.y + (m * p.N * p.F + f) * I;
-  R* __restrict__ vb = (R*)p.v + m * 2 * NF + f;
+  R* vb = (R*)p.v + m * 2 * NF + f;  // no __restrict__: may alias vr (in place)
+  const R* vr = (p.v_src ? (const R*)p.v_src : (const R*)p.v) + m * 2 * NF + f;
   const double fl = p.floor[g];
   const double invI = 1.0 / I;
 
@@ -76,8 +77,8 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
     double2 yv[I];
 #pragma unroll
     for (int a = 0; a < I; ++a) yv[a] = to_c128(yp[a]);
-    const double v1 = (double)vb[n * p.F];
-    const double v2 = (double)vb[NF + n * p.F];
+    const double v1 = (double)vr[n * p.F];
+    const double v2 = (double)vr[NF + n * p.F];
     // R = v1 S1 + v2 S2 and its Cholesky factor
     double2 Lm[I][I];
     [[maybe_unused]] double ild[I];

@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
   const int64_t n1 = min(p.N, n0 + p.chunk_frames);
   const int64_t NF = p.N * p.F;
   const C* __restrict__ yb = (const C*)p.y + (m * p.N * p.F + f) * I;
-  R* __restrict__ vb = (R*)p.v + m * 2 * NF + f;
+  R* vb = (R*)p.v + m * 2 * NF + f;  // no __restrict__: may alias vr (in place)
+  const R* vr = (p.v_src ? (const R*)p.v_src : (const R*)p.v) + m * 2 * NF + f;
   const double fl = p.floor[g];
   const bool do_ll = p.llbin != nullptr;
 
@@ -109,8 +110,8 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
   double v1n = 0.0, v2n = 0.0;
   if (n0 < n1) {
     if (own) ynext = to_c128(yb[n0 * p.F * I + r]);
-    v1n = (double)vb[n0 * p.F];
-    v2n = (double)vb[NF + n0 * p.F];
+    v1n = (double)vr[n0 * p.F];
+    v2n = (double)vr[NF + n0 * p.F];
   }
 #pragma unroll 1
   for (int64_t n = n0; n < n1; ++n) {
@@ -118,8 +119,8 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(co
     const double v1 = v1n, v2 = v2n;
     if (n + 1 < n1) {
       if (own) ynext = to_c128(yb[(n + 1) * p.F * I + r]);
-      v1n = (double)vb[(n + 1) * p.F];
-      v2n = (double)vb[NF + (n + 1) * p.F];
+      v1n = (double)vr[(n + 1) * p.F];
+      v2n = (double)vr[NF + (n + 1) * p.F];
     }
     if (own) {
       vy[r] = ycur;

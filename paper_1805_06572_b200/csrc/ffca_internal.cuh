@@ -17,6 +17,7 @@ constexpr int kFcaParts = 4;
 struct FastIterParams {
   const void* y;        // (M,N,F,I) complex R
   void* v;              // (M,2,N,F) R, read (and written when update)
+  const void* v_src;    // powers read instead of v (null: v), e.g. the caller's init
   const double2* P;     // (G,I,I)
   const double2* W;     // (G,I,I) = P^{-H}; needed when mu_back
   const double* lam;    // (G,I)
@@ -38,6 +39,7 @@ cudaError_t launch_fast_em(const FastIterParams& p, int I, int dtype, cudaStream
 struct FcaIterParams {
   const void* y;        // (M,N,F,I)
   void* v;              // (M,2,N,F)
+  const void* v_src;    // powers read instead of v (null: v)
   const double* Sp;     // [2][I*I][G] packed S1, S2 (SoA)
   const double* floor;  // (G)
   double* Spart;        // [nchunk][kFcaParts*I*I][G]: B1, B2, X1, X2 packed

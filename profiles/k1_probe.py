@@ -24,11 +24,15 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--iterations", type=int, default=3)
     ap.add_argument("--engine", default="fast")
+    ap.add_argument("--dtype", default="c128")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     Y, V, S, FL = make_inputs(cfg, shard(cfg, 0, 1))
     y, v, s, fl = (torch.from_numpy(x).cuda() for x in (Y, V, S, FL))
-    r = run_device(a.engine, y, v, s, fl, a.iterations, likelihood=False, check=True)
+    if a.dtype == "c64":
+        y, v = y.to(torch.complex64), v.to(torch.float32)
+    r = run_device(a.engine, y, v, s, fl, a.iterations, likelihood=False, check=True,
+                   dtype=a.dtype)
     status_of(r)
     torch.cuda.synchronize()
     print("ok", tuple(Y.shape), a.iterations)

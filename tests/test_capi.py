@@ -56,8 +56,8 @@ def test_library_is_sm100a():
 
 
 def test_run_args_layout_matches_c():
-    # 3 int64 + 4 int32 + 10 pointers + size_t + pointer + int64 + pointer
-    assert ctypes.sizeof(_lib.RunArgs) == 24 + 16 + 8 * 10 + 8 + 8 + 8 + 8
+    # 3 int64 + 4 int32 + 10 pointers + size_t + pointer + int64 + 2 pointers
+    assert ctypes.sizeof(_lib.RunArgs) == 24 + 16 + 8 * 10 + 8 + 8 + 8 + 8 + 8
 
 
 def test_workspace_size_query_needs_no_device():
@@ -106,3 +106,27 @@ def test_package_never_imports_the_oracle():
 def test_missing_library_raises(tmp_path):
     with pytest.raises(BackendUnavailableError):
         _lib.load(tmp_path / "nope.so")
+
+
+def test_run_args_offsets_match_the_header(tmp_path):
+    """Every ctypes field of RunArgs sits at the offset gcc gives the C struct."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    names = [f[0] for f in _lib.RunArgs._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text(
+        "#include <stddef.h>\n#include <stdio.h>\n#include \"fastfca_b200.h\"\n"
+        "int main(void) {\n  printf(\"%zu\\n\", sizeof(ffca_run_args));\n"
+        + "".join(f"  printf(\"%zu\\n\", offsetof(ffca_run_args, {n}));\n" for n in names)
+        + "  return 0;\n}\n")
+    exe = tmp_path / "layout"
+    inc = Path(__file__).resolve().parents[1] / "include"
+    subprocess.run(["gcc", f"-I{inc}", "-I/usr/local/cuda/include", str(src), "-o", str(exe)],
+                   check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    assert got[0] == ctypes.sizeof(_lib.RunArgs)
+    assert got[1:] == [getattr(_lib.RunArgs, n).offset for n in names]
