@@ -137,6 +137,45 @@ struct Math<float> {
 // bin-dependent amount (sw) so that the consumer reads (lane = bin, one unit
 // each) hit distinct banks. (Per-lane 80-byte slots made every 16-B cp.async
 // a ~30-way bank conflict and read half-used sectors.)
+// ---- packed FP32 (sm_100 FFMA2 / FMUL2 / FADD2) ------------------------------
+// Two FP32 lanes per instruction; ptxas folds scalar broadcasts, half swaps
+// and half negations of the operands into operand modifiers (checked in
+// SASS), so (a.x, a.x) or (a.y, -a.x) cost no moves. Used by the complex64
+// pass at even orders, which is issue-bound in scalar FP32.
+namespace f2 {
+FFCA_DEV unsigned long long pk(float2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+FFCA_DEV float2 up(unsigned long long r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+FFCA_DEV float2 fma(float2 a, float2 b, float2 c) {  // a * b + c
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)), "l"(pk(c)));
+  return up(r);
+}
+FFCA_DEV float2 mul(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+  return up(r);
+}
+FFCA_DEV float2 add(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+  return up(r);
+}
+FFCA_DEV float2 bc(float a) { return make_float2(a, a); }
+FFCA_DEV float rcp(float x) {  // MUFU.RCP (~1 ulp), no IEEE slow path
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+}  // namespace f2
+
 template <int I, typename R>
 struct RingSlot {
   using C = typename CplxOf<R>::type;
@@ -191,6 +230,8 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
   using T = typename Math<R>::T;    // per-point compute type
   using T2 = typename Math<R>::T2;
   constexpr bool kBlk = Math<R>::kBlocked;
+  // complex64 at even orders: the per-point math in packed FP32 (f2::)
+  constexpr bool kF2 = kBlk && (I % 2 == 0);
   constexpr int NP = I * I;
   constexpr int NE = 2 * NP + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -236,6 +277,11 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
 #pragma unroll
     for (int e = 0; e < (kBlk ? NP : 1); ++e) accb[j][e] = T(0);
   }
+  float2 acc2[2][kF2 ? NP / 2 : 1];  // packed FP32 block sums (kF2): entries (2i, 2i+1)
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int e = 0; e < (kF2 ? NP / 2 : 1); ++e) acc2[j][e] = make_float2(0.f, 0.f);
   auto accum = [&](int j, int e, T a, T b) {  // acc[j][e] += a * b
     if constexpr (kBlk)
       accb[j][e] = fma(a, b, accb[j][e]);
@@ -243,7 +289,16 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
       acc[j][e] = fma((double)a, (double)b, acc[j][e]);
   };
   auto flush = [&]() {
-    if constexpr (kBlk) {
+    if constexpr (kF2) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < NP / 2; ++e) {
+          acc[j][2 * e] += (double)acc2[j][e].x;
+          acc[j][2 * e + 1] += (double)acc2[j][e].y;
+          acc2[j][e] = make_float2(0.f, 0.f);
+        }
+    } else if constexpr (kBlk) {
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -334,28 +389,61 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
     double lprod = 1.0, quad = 0.0;
     bool bad = false;
     T v1l[I], den[I], rden[I];
+    if constexpr (kF2) {
+      // the same per-channel scalars, two channels per packed instruction
+      float2 tr1p = make_float2(0.f, 0.f), tr2p = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int a = 0; a < I; ++a) {
-      v1l[a] = v1 * lam[a];
-      den[a] = v1l[a] + v2;
-    }
-    Math<R>::template rcp_n<I>(den, rden);
-#pragma unroll
-    for (int a = 0; a < I; ++a) {
-      g1[a] = v1l[a] * rden[a];
-      g2[a] = v2 * rden[a];
-      const T pz = fma(z[a].x, z[a].x, z[a].y * z[a].y);
-      // t_j = g_j^2 |z|^2 + c with c = v2 g1 = v1 lam g2 (reference
-      // _kernels_numba.py:359-363), factored to save one multiply each
-      t1[a] = g1[a] * fma(g1[a], pz, v2);
-      t2[a] = g2[a] * fma(g2[a], pz, v1l[a]);
-      tr1 = fma(t1[a], il[a], tr1);
-      tr2 = fma(t2[a], invI, tr2);
-      if (LL) {
-        lprod *= (double)den[a];
-        quad = fma((double)pz, (double)rden[a], quad);
+      for (int q = 0; q < I / 2; ++q) {
+        const int a = 2 * q;
+        const float2 v1l2 = f2::mul(f2::bc(v1), make_float2(lam[a], lam[a + 1]));
+        const float2 den2 = f2::add(v1l2, f2::bc(v2));
+        const float2 rd2 = make_float2(f2::rcp(den2.x), f2::rcp(den2.y));
+        const float2 g12 = f2::mul(v1l2, rd2), g22 = f2::mul(f2::bc(v2), rd2);
+        const float2 pz2 = make_float2(fmaf(z[a].x, z[a].x, z[a].y * z[a].y),
+                                       fmaf(z[a + 1].x, z[a + 1].x, z[a + 1].y * z[a + 1].y));
+        const float2 t12 = f2::mul(g12, f2::fma(g12, pz2, f2::bc(v2)));
+        const float2 t22 = f2::mul(g22, f2::fma(g22, pz2, v1l2));
+        tr1p = f2::fma(t12, make_float2(il[a], il[a + 1]), tr1p);
+        tr2p = f2::fma(t22, f2::bc(invI), tr2p);
+        v1l[a] = v1l2.x, v1l[a + 1] = v1l2.y;
+        den[a] = den2.x, den[a + 1] = den2.y;
+        rden[a] = rd2.x, rden[a + 1] = rd2.y;
+        g1[a] = g12.x, g1[a + 1] = g12.y;
+        g2[a] = g22.x, g2[a + 1] = g22.y;
+        t1[a] = t12.x, t1[a + 1] = t12.y;
+        t2[a] = t22.x, t2[a + 1] = t22.y;
+        if (LL) {
+          lprod *= (double)den2.x * (double)den2.y;
+          quad = fma((double)pz2.x, (double)rd2.x, quad);
+          quad = fma((double)pz2.y, (double)rd2.y, quad);
+        }
       }
-      // den == 0 needs no test: rcp(0) poisons w below (inf * 0 / NaN)
+      tr1 = tr1p.x + tr1p.y;
+      tr2 = tr2p.x + tr2p.y;
+    } else {
+#pragma unroll
+      for (int a = 0; a < I; ++a) {
+        v1l[a] = v1 * lam[a];
+        den[a] = v1l[a] + v2;
+      }
+      Math<R>::template rcp_n<I>(den, rden);
+#pragma unroll
+      for (int a = 0; a < I; ++a) {
+        g1[a] = v1l[a] * rden[a];
+        g2[a] = v2 * rden[a];
+        const T pz = fma(z[a].x, z[a].x, z[a].y * z[a].y);
+        // t_j = g_j^2 |z|^2 + c with c = v2 g1 = v1 lam g2 (reference
+        // _kernels_numba.py:359-363), factored to save one multiply each
+        t1[a] = g1[a] * fma(g1[a], pz, v2);
+        t2[a] = g2[a] * fma(g2[a], pz, v1l[a]);
+        tr1 = fma(t1[a], il[a], tr1);
+        tr2 = fma(t2[a], invI, tr2);
+        if (LL) {
+          lprod *= (double)den[a];
+          quad = fma((double)pz, (double)rden[a], quad);
+        }
+        // den == 0 needs no test: rcp(0) poisons w below (inf * 0 / NaN)
+      }
     }
     if (LL) llacc += log(lprod) + quad;
     if (UPDATE) {
@@ -372,6 +460,33 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
         bad |= (((b1 >> 52) & 0x7ff) == 0x7ff) | (((b2 >> 52) & 0x7ff) == 0x7ff) | (b1 <= 0) |
                (b2 <= 0);
       }
+      if constexpr (kF2) {
+        const float iw1 = f2::rcp(w1), iw2 = f2::rcp(w2);
+        float h1[I], h2[I];
+#pragma unroll
+        for (int q = 0; q < I / 2; ++q) {  // diagonal entries (2q, 2q+1)
+          const int a = 2 * q;
+          acc2[0][q] = f2::fma(make_float2(t1[a], t1[a + 1]), f2::bc(iw1), acc2[0][q]);
+          acc2[1][q] = f2::fma(make_float2(t2[a], t2[a + 1]), f2::bc(iw2), acc2[1][q]);
+          const float2 h12 = f2::mul(make_float2(g1[a], g1[a + 1]), f2::bc(iw1));
+          const float2 h22 = f2::mul(make_float2(g2[a], g2[a + 1]), f2::bc(iw2));
+          h1[a] = h12.x, h1[a + 1] = h12.y;
+          h2[a] = h22.x, h2[a + 1] = h22.y;
+        }
+#pragma unroll
+        for (int a = 0; a < I; ++a) {
+#pragma unroll
+          for (int b = a + 1; b < I; ++b) {
+            // (re, im) of z_a conj(z_b) in one pair, shared by both sources
+            const float2 x = f2::fma(z[a], f2::bc(z[b].x),
+                                     f2::mul(make_float2(z[a].y, -z[a].x), f2::bc(z[b].y)));
+            const int e = Herm<I>::re(a, b) / 2;  // (re, im) = entries (2e, 2e+1)
+            acc2[0][e] = f2::fma(f2::bc(h1[a] * g1[b]), x, acc2[0][e]);
+            acc2[1][e] = f2::fma(f2::bc(h2[a] * g2[b]), x, acc2[1][e]);
+          }
+        }
+        if ((k % kF32Block) == kF32Block - 1) flush();
+      } else {
       T wv[2] = {w1, w2}, iw[2];
       Math<R>::template rcp_n<2>(wv, iw);
       const T iw1 = iw[0], iw2 = iw[1];
@@ -399,6 +514,7 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
         }
       }
       if (kBlk && ((k % kF32Block) == kF32Block - 1)) flush();
+      }
     }
     if (MU && active) {
       C* mo = (C*)p.mu_out;
@@ -475,6 +591,22 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
       T v1, v2;
       load_frame(k, yv, v1, v2);
       T2 z[I];
+      if constexpr (kF2) {
+        // z_a = sum_b conj(P_ba) y_b: p.x (y.x, y.y) + p.y (y.y, -y.x), packed
+#pragma unroll
+        for (int a = 0; a < I; ++a) {
+          const T2 p0 = sP[(0 * I + a) * 32 + lane];
+          float2 za = f2::fma(f2::bc(p0.y), make_float2(yv[0].y, -yv[0].x),
+                              f2::mul(f2::bc(p0.x), yv[0]));
+#pragma unroll
+          for (int b = 1; b < I; ++b) {
+            const T2 pb = sP[(b * I + a) * 32 + lane];
+            za = f2::fma(f2::bc(pb.x), yv[b], za);
+            za = f2::fma(f2::bc(pb.y), make_float2(yv[b].y, -yv[b].x), za);
+          }
+          z[a] = za;
+        }
+      } else
 #pragma unroll
       for (int a = 0; a < I; ++a) {
         const T2 p0 = sP[(0 * I + a) * 32 + lane];
