@@ -197,6 +197,93 @@ struct RingSlot {
   static FFCA_DEV constexpr int rpos(int rb, int a) { return kXor ? (rb ^ (a * UB)) : rb + a * UB; }
 };
 
+// The RingSlot scheme as a reusable object (used by the FCA pass, K4): a
+// warp's frames n = nfirst + k * WARPS stream through a STAGES-deep ring at
+// `base` (STAGES * WARPS * WARP_BYTES bytes per CTA). Same copies, swizzle and
+// synchronisation as fast_em2_kernel's inline ring.
+template <int I, typename R, int WARPS, int STAGES>
+struct FrameRing {
+  using Slot = RingSlot<I, R>;
+  using C = typename CplxOf<R>::type;
+  static constexpr int kStride = WARPS * Slot::WARP_BYTES;
+  static constexpr size_t BYTES = (size_t)STAGES * kStride;
+  unsigned char* wslots;
+  const unsigned char* ybytes;
+  const R* vr;
+  int64_t frame_bytes, vstride, NF;
+  int64_t ycorr[Slot::Q];
+  int spos0, rb, lane, issue_stage, read_stage;
+  bool contiguous;
+
+  FFCA_DEV void init(unsigned char* base, int warp, int lane_, int64_t tile0, int64_t G,
+                     int64_t N, int64_t F, const void* y, const R* vrow) {
+    lane = lane_;
+    wslots = base + (size_t)warp * Slot::WARP_BYTES;
+    contiguous = (tile0 + 31 < G) && (tile0 / F == (tile0 + 31) / F);
+    spos0 = Slot::pos(lane / Slot::Q, lane % Slot::Q);
+    rb = Slot::rbase(lane);
+    auto unit_off = [&](int c) -> int64_t {
+      const int u = 32 * c + lane, b = u / Slot::Q, a = u % Slot::Q;
+      int64_t gb = tile0 + b;
+      if (gb >= G) gb = G - 1;
+      const int64_t mb = gb / F, fb = gb - mb * F;
+      return ((mb * N) * F + fb) * Slot::YB + a * Slot::UB;
+    };
+    const int64_t ybase = unit_off(0);
+#pragma unroll
+    for (int c = 0; c < Slot::Q; ++c)
+      ycorr[c] = contiguous ? 0 : unit_off(c) - ybase - 32 * c * Slot::UB;
+    ybytes = (const unsigned char*)y + ybase;
+    frame_bytes = F * Slot::YB;
+    vr = vrow;
+    vstride = F;
+    NF = N * F;
+    issue_stage = read_stage = 0;
+  }
+  FFCA_DEV void issue(int64_t n) {
+    unsigned char* slot = wslots + issue_stage;
+    issue_stage = issue_stage + kStride == STAGES * kStride ? 0 : issue_stage + kStride;
+    const unsigned char* yrow = ybytes + n * frame_bytes;
+    unsigned char* dst = slot + spos0;
+#pragma unroll
+    for (int c = 0; c < Slot::Q; ++c) {
+      const unsigned char* src = yrow + 32 * c * Slot::UB + (contiguous ? 0 : ycorr[c]);
+      if constexpr (Slot::UB == 16)
+        cp_async16(dst + 32 * c * Slot::UB, src);
+      else
+        cp_async8(dst + 32 * c * Slot::UB, src);
+    }
+    unsigned char* vs = slot + 32 * Slot::YB;
+    if constexpr (sizeof(R) == 8) {
+      cp_async8(vs + 8 * lane, vr + n * vstride);
+      cp_async8(vs + 256 + 8 * lane, vr + NF + n * vstride);
+    } else {
+      cp_async4(vs + 4 * lane, vr + n * vstride);
+      cp_async4(vs + 128 + 4 * lane, vr + NF + n * vstride);
+    }
+  }
+  // this lane's bin of the next stage, widened to complex128 / float64
+  FFCA_DEV void load(double2 (&yv)[I], double& v1, double& v2) {
+    const unsigned char* slot = wslots + read_stage;
+    read_stage = read_stage + kStride == STAGES * kStride ? 0 : read_stage + kStride;
+    constexpr int PER = Slot::UB / (int)sizeof(C);
+#pragma unroll
+    for (int a = 0; a < Slot::Q; ++a) {
+      const unsigned char* src = slot + Slot::rpos(rb, a);
+      if constexpr (PER == 2) {
+        const float4 q = *(const float4*)src;
+        yv[2 * a] = cmk(q.x, q.y);
+        yv[2 * a + 1] = cmk(q.z, q.w);
+      } else {
+        yv[a] = to_c128(*(const C*)src);
+      }
+    }
+    const unsigned char* vs = slot + 32 * Slot::YB;
+    v1 = (double)((const R*)vs)[lane];
+    v2 = (double)((const R*)(vs + 32 * sizeof(R)))[lane];
+  }
+};
+
 template <int I, typename R, int WARPS, int STAGES, bool MU = false>
 struct Fast2Smem {
   static constexpr int NE = 2 * I * I + 1;

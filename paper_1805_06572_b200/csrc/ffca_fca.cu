@@ -13,7 +13,7 @@
 // S1, S2 (packed Hermitian) in shared memory, bin-minor so each lane's reads
 // are bank-conflict free. The power-update traces tr(S_j^-1 Phi_j) are taken
 // through identities that need no S_j^-1 (see the trace block).
-#include "ffca_internal.cuh"
+#include "ffca_fast2.cuh"  // FrameRing (warp-cooperative frame staging)
 
 namespace ffca {
 
@@ -22,6 +22,9 @@ namespace ffca {
 // I = 4 where the extra live registers add spills)
 #ifndef FFCA_FCA_FASTMATH_MAXI
 #define FFCA_FCA_FASTMATH_MAXI 3
+#endif
+#ifndef FFCA_FCA_STAGES
+#define FFCA_FCA_STAGES 4  // frame ring depth of the FCA pass
 #endif
 #ifndef FFCA_FCA_MINB
 #define FFCA_FCA_MINB 1  // CTAs per SM the I <= 4 pass is register-budgeted for
@@ -33,9 +36,12 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
   constexpr int NP = I * I;
   constexpr int NE = kFcaParts * NP + 1;
   constexpr bool kFastMath = I <= FFCA_FCA_FASTMATH_MAXI;
-  extern __shared__ double smem[];
-  double* sS = smem;                    // [2][NP][32]: S1, S2 (the traces need no S^-1)
-  double* red = smem;                   // [(WARPS-1)][NE][32], after the frame loop
+  using Ring = FrameRing<I, R, WARPS, FFCA_FCA_STAGES>;
+  extern __shared__ __align__(16) double smem[];
+  // frame ring, then S1, S2 ([2][NP][32] packed; the traces need no S^-1); the
+  // cross-warp reduction buffer [(WARPS-1)][NE][32] reuses it after the loop
+  double* sS = (double*)((unsigned char*)smem + Ring::BYTES);
+  double* red = smem;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t G = p.G;
@@ -49,11 +55,19 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
   const int64_t n0 = (int64_t)blockIdx.y * p.chunk_frames;
   const int64_t n1 = min(p.N, n0 + p.chunk_frames);
   const int64_t NF = p.N * p.F;
-  const C* __restrict__ yb = (const C*)p.y + (m * p.N * p.F + f) * I;
   R* vb = (R*)p.v + m * 2 * NF + f;  // no __restrict__: may alias vr (in place)
   const R* vr = (p.v_src ? (const R*)p.v_src : (const R*)p.v) + m * 2 * NF + f;
   const double fl = p.floor[g];
   const double invI = 1.0 / I;
+  Ring ring;
+  ring.init((unsigned char*)smem, warp, lane, (int64_t)blockIdx.x * 32, G, p.N, p.F, p.y, vr);
+  const int64_t nfirst = n0 + warp;
+  const int K = nfirst < n1 ? (int)((n1 - nfirst + WARPS - 1) / WARPS) : 0;
+#pragma unroll
+  for (int s = 0; s < FFCA_FCA_STAGES - 1; ++s) {
+    if (s < K) ring.issue(nfirst + (int64_t)s * WARPS);
+    cp_async_commit();
+  }
 
   auto Sget = [&](int which, int a, int b) -> double2 {
     // full entry (a, b) of packed Hermitian matrix `which`
@@ -72,13 +86,16 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
   const bool do_ll = p.llbin != nullptr;
   int64_t bad_n = 0;
 
-  for (int64_t n = n0 + warp; n < n1; n += WARPS) {
-    const C* yp = yb + n * p.F * I;
+  for (int k = 0; k < K; ++k) {
+    const int64_t n = nfirst + (int64_t)k * WARPS;
+    __syncwarp();  // every lane is done with the stage the next copy overwrites
+    if (k + FFCA_FCA_STAGES - 1 < K) ring.issue(n + (int64_t)(FFCA_FCA_STAGES - 1) * WARPS);
+    cp_async_commit();
+    cp_async_wait<FFCA_FCA_STAGES - 1>();
+    __syncwarp();  // the other lanes' copies of this stage are visible
     double2 yv[I];
-#pragma unroll
-    for (int a = 0; a < I; ++a) yv[a] = to_c128(yp[a]);
-    const double v1 = (double)vr[n * p.F];
-    const double v2 = (double)vr[NF + n * p.F];
+    double v1, v2;
+    ring.load(yv, v1, v2);
     // R = v1 S1 + v2 S2 and its Cholesky factor
     double2 Lm[I][I];
     [[maybe_unused]] double ild[I];
@@ -215,9 +232,10 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
     report_error(p.st, p.iter, FFCA_ERR_SINGULAR_MIXTURE,
                  (unsigned long long)((m * p.N + (bad_n - 1)) * p.F + f));
 
+  cp_async_wait_all();
   if (!p.update && !do_ll) return;
   if (WARPS > 1) {
-    __syncthreads();  // sS is dead: the reduction buffer reuses it
+    __syncthreads();  // ring and sS are dead: the reduction buffer reuses them
     if (warp > 0) {
       double* r = red + (size_t)(warp - 1) * NE * 32;
 #pragma unroll
@@ -250,18 +268,18 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
   if (do_ll) p.llbin[(size_t)c * G + g] = llacc;
 }
 
-template <int I>
+template <int I, typename R>
 constexpr size_t fca_smem_bytes() {
   constexpr size_t NP = (size_t)I * I;
-  constexpr size_t ss = 2 * NP * 32;
-  constexpr size_t red = (size_t)(kWarps - 1) * (kFcaParts * NP + 1) * 32;
-  return (ss > red ? ss : red) * sizeof(double);
+  constexpr size_t ss = FrameRing<I, R, kWarps, FFCA_FCA_STAGES>::BYTES + 2 * NP * 32 * sizeof(double);
+  constexpr size_t red = (size_t)(kWarps - 1) * (kFcaParts * NP + 1) * 32 * sizeof(double);
+  return ss > red ? ss : red;
 }
 
 template <int I, typename R>
 static cudaError_t launch_fca_em_t(const FcaIterParams& p, cudaStream_t s) {
   constexpr int NP = I * I;
-  const size_t smem = fca_smem_bytes<I>();
+  const size_t smem = fca_smem_bytes<I, R>();
   auto kern = fca_em_kernel<I, R, kWarps>;
   static bool configured = false;
   if (!configured) {
@@ -278,7 +296,7 @@ static cudaError_t launch_fca_em_t(const FcaIterParams& p, cudaStream_t s) {
 template <int I, typename R>
 static int fca_bpsm_t() {
   constexpr int NP = I * I;
-  const size_t smem = fca_smem_bytes<I>();
+  const size_t smem = fca_smem_bytes<I, R>();
   auto kern = fca_em_kernel<I, R, kWarps>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int n = 0;
