@@ -48,7 +48,10 @@ FFCA_DEV double2 packed_get(const double* S, int a, int b) {
 }  // namespace
 
 template <int I, typename R>
-__global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32) fca_par_kernel(const FcaIterParams p) {
+#ifndef FCA_PAR_MINB
+#define FCA_PAR_MINB 8  // CTAs per SM the lane-parallel FCA pass is register-budgeted for
+#endif
+__global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32, FCA_PAR_MINB) fca_par_kernel(const FcaIterParams p) {
   using Lay = FcaParLayout<I>;
   using C = typename CplxOf<R>::type;
   constexpr int NP = I * I;
@@ -380,8 +383,37 @@ __global__ void __launch_bounds__(64)
     if (llg && r == 0 && active) llg[g] = -ordered_sum(llbin + g, nchunk, (size_t)G);
     __syncwarp();
     const double invN = 1.0 / (double)N;
-    // sum of packed part `part` over the chunks into the full matrix A
-    // (circulant slots: lane r owns (r, r + s mod I))
+    // chunk sums of this lane's circulant slots (r, r + s mod I) of all four
+    // parts, in one pass over the chunks (all loads of a chunk in flight;
+    // per-entry chunk order fixed)
+    int ire[NS], iim[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int b0 = (rr + s) % I;
+      const int a = rr < b0 ? rr : b0, b = rr < b0 ? b0 : rr;
+      ire[s] = a == b ? a : Herm<I>::re(a, b);
+      iim[s] = a == b ? a : Herm<I>::im(a, b);
+    }
+    double2 sums[kFcaParts][NS];
+#pragma unroll
+    for (int q = 0; q < kFcaParts; ++q)
+#pragma unroll
+      for (int s = 0; s < NS; ++s) sums[q][s] = cmk(0.0, 0.0);
+    if (own) {
+#pragma unroll 2
+      for (int c = 0; c < nchunk; ++c) {
+#pragma unroll
+        for (int q = 0; q < kFcaParts; ++q) {
+          const double* sp = Spart + ((size_t)c * kFcaParts + q) * NP * G + g;
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            sums[q][s].x += sp[(size_t)ire[s] * G];
+            sums[q][s].y += sp[(size_t)iim[s] * G];
+          }
+        }
+      }
+    }
+    // part `part` into the full matrix A
     auto gather = [&](int part) {
       if (!own) return;
 #pragma unroll
@@ -389,16 +421,7 @@ __global__ void __launch_bounds__(64)
         if (!(s < I / 2 || (I % 2) == 1 || rr < I / 2)) continue;
         const int b0 = (rr + s) % I;
         const int a = rr < b0 ? rr : b0, b = rr < b0 ? b0 : rr;
-        const int ire = a == b ? a : Herm<I>::re(a, b);
-        const int iim = a == b ? a : Herm<I>::im(a, b);
-        double sr = 0.0, si = 0.0;
-#pragma unroll 4
-        for (int c = 0; c < nchunk; ++c) {
-          const double* sp = Spart + ((size_t)c * kFcaParts + part) * NP * G + g;
-          sr += sp[(size_t)ire * G];
-          si += sp[(size_t)iim * G];
-        }
-        if (a == b) si = 0.0;
+        const double sr = sums[part][s].x, si = a == b ? 0.0 : sums[part][s].y;
         A(a, b) = cmk(sr, si);
         A(b, a) = cmk(sr, -si);
       }

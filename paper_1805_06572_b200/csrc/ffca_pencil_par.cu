@@ -45,9 +45,25 @@ __global__ void __launch_bounds__(ParLayout<I>::WARPS * 32) pencil_par_kernel(co
 
   // 1. chunk partials -> S~1, S~2 (full Hermitian); entries split over lanes
   bool fin = true;
-  for (int e = r; e < 2 * NP; e += Lay::LB) {
-    double sacc = ordered_sum(p.Spart + (size_t)e * G + g, p.nchunk, (size_t)2 * NP * G);
-    sacc *= 1.0 / (double)p.N;
+  // every entry of this lane accumulates in one pass over the chunks (all
+  // its loads of a chunk in flight together; per-entry chunk order kept,
+  // bitwise equal to ordered_sum)
+  constexpr int EPL = (2 * NP + Lay::LB - 1) / Lay::LB;  // entries per lane
+  double part[EPL];
+#pragma unroll
+  for (int t = 0; t < EPL; ++t) part[t] = 0.0;
+#pragma unroll 2
+  for (int c = 0; c < p.nchunk; ++c) {
+    const double* sp = p.Spart + (size_t)c * 2 * NP * G + g;
+#pragma unroll
+    for (int t = 0; t < EPL; ++t)
+      if (r + Lay::LB * t < 2 * NP) part[t] += sp[(size_t)(r + Lay::LB * t) * G];
+  }
+#pragma unroll
+  for (int t = 0; t < EPL; ++t) {
+    const int e = r + Lay::LB * t;
+    if (e >= 2 * NP) continue;
+    double sacc = part[t] * (1.0 / (double)p.N);
     fin = fin && isfinite(sacc);
     const int j = e < NP ? 0 : 1;
     int a, b, comp;
