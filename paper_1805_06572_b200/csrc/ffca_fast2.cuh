@@ -208,15 +208,15 @@ struct FrameRing {
   static constexpr int kStride = WARPS * Slot::WARP_BYTES;
   static constexpr size_t BYTES = (size_t)STAGES * kStride;
   unsigned char* wslots;
-  const unsigned char* ybytes;
-  const R* vr;
-  int64_t frame_bytes, vstride, NF;
+  const unsigned char* ynext;  // row of the next frame to issue (frames go in order)
+  const R* vnext;
+  int64_t ystep, vstep, NF;
   int64_t ycorr[Slot::Q];
   int spos0, rb, lane, issue_stage, read_stage;
   bool contiguous;
 
   FFCA_DEV void init(unsigned char* base, int warp, int lane_, int64_t tile0, int64_t G,
-                     int64_t N, int64_t F, const void* y, const R* vrow) {
+                     int64_t N, int64_t F, const void* y, const R* vrow, int64_t nfirst) {
     lane = lane_;
     wslots = base + (size_t)warp * Slot::WARP_BYTES;
     contiguous = (tile0 + 31 < G) && (tile0 / F == (tile0 + 31) / F);
@@ -233,17 +233,18 @@ struct FrameRing {
 #pragma unroll
     for (int c = 0; c < Slot::Q; ++c)
       ycorr[c] = contiguous ? 0 : unit_off(c) - ybase - 32 * c * Slot::UB;
-    ybytes = (const unsigned char*)y + ybase;
-    frame_bytes = F * Slot::YB;
-    vr = vrow;
-    vstride = F;
+    ynext = (const unsigned char*)y + ybase + nfirst * F * Slot::YB;
+    ystep = (int64_t)WARPS * F * Slot::YB;
+    vnext = vrow + nfirst * F;
+    vstep = (int64_t)WARPS * F;
     NF = N * F;
     issue_stage = read_stage = 0;
   }
-  FFCA_DEV void issue(int64_t n) {
+  FFCA_DEV void issue() {  // the next frame of this warp
     unsigned char* slot = wslots + issue_stage;
     issue_stage = issue_stage + kStride == STAGES * kStride ? 0 : issue_stage + kStride;
-    const unsigned char* yrow = ybytes + n * frame_bytes;
+    const unsigned char* yrow = ynext;
+    ynext += ystep;
     unsigned char* dst = slot + spos0;
 #pragma unroll
     for (int c = 0; c < Slot::Q; ++c) {
@@ -255,12 +256,13 @@ struct FrameRing {
     }
     unsigned char* vs = slot + 32 * Slot::YB;
     if constexpr (sizeof(R) == 8) {
-      cp_async8(vs + 8 * lane, vr + n * vstride);
-      cp_async8(vs + 256 + 8 * lane, vr + NF + n * vstride);
+      cp_async8(vs + 8 * lane, vnext);
+      cp_async8(vs + 256 + 8 * lane, vnext + NF);
     } else {
-      cp_async4(vs + 4 * lane, vr + n * vstride);
-      cp_async4(vs + 128 + 4 * lane, vr + NF + n * vstride);
+      cp_async4(vs + 4 * lane, vnext);
+      cp_async4(vs + 128 + 4 * lane, vnext + NF);
     }
+    vnext += vstep;
   }
   // this lane's bin of the next stage, widened to complex128 / float64
   FFCA_DEV void load(double2 (&yv)[I], double& v1, double& v2) {
@@ -427,12 +429,17 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
   const int64_t frame_bytes = p.F * Slot::YB;
   int issue_stage = 0, read_stage = 0;  // byte offsets of the next stages
 
-  auto issue = [&](int k) {
-    const int64_t n = nfirst + (int64_t)k * WARPS;
+  // frames are issued and consumed in order: running row pointers instead of
+  // 64-bit n * F products per frame
+  const unsigned char* ynext = ybytes + nfirst * frame_bytes;
+  const R* vnext = vr + nfirst * p.F;
+  const int64_t ystep = (int64_t)WARPS * frame_bytes, vstep = (int64_t)WARPS * p.F;
+  auto issue = [&](int) {
     unsigned char* slot = wslots + issue_stage;
     issue_stage = (issue_stage + (int)kStageStride == STAGES * (int)kStageStride)
                       ? 0 : issue_stage + (int)kStageStride;
-    const unsigned char* yrow = ybytes + n * frame_bytes;
+    const unsigned char* yrow = ynext;
+    ynext += ystep;
     unsigned char* dst = slot + spos0;
     if (contiguous) {  // one base, compile-time offsets
 #pragma unroll
@@ -454,12 +461,13 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
     }
     unsigned char* vs = slot + 32 * Slot::YB;
     if constexpr (sizeof(R) == 8) {
-      cp_async8(vs + 8 * lane, vr + n * p.F);
-      cp_async8(vs + 256 + 8 * lane, vr + NF + n * p.F);
+      cp_async8(vs + 8 * lane, vnext);
+      cp_async8(vs + 256 + 8 * lane, vnext + NF);
     } else {
-      cp_async4(vs + 4 * lane, vr + n * p.F);
-      cp_async4(vs + 128 + 4 * lane, vr + NF + n * p.F);
+      cp_async4(vs + 4 * lane, vnext);
+      cp_async4(vs + 128 + 4 * lane, vnext + NF);
     }
+    vnext += vstep;
   };
 
   constexpr int kAhead = STAGES - 1;  // frames issued ahead
@@ -469,6 +477,7 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
     cp_async_commit();
   }
 
+  R* vwrite = vb + nfirst * p.F;  // v of the frame being processed (advanced per frame)
   // per-frame E+M body once z = P^H y is known
   auto frame = [&](int k, int64_t n, const T2 (&yv)[I], T v1, T v2, const T2 (&z)[I]) {
     T g1[I], g2[I], t1[I], t2[I];
@@ -538,8 +547,8 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
       const T w1 = (q1 < fl) ? fl : q1;  // NaN propagates like np.maximum
       const T w2 = (q2 < fl) ? fl : q2;
       if (active) {
-        vb[n * p.F] = (R)w1;
-        vb[NF + n * p.F] = (R)w2;
+        vwrite[0] = (R)w1;
+        vwrite[NF] = (R)w2;
       }
       {  // non-finite or non-positive w (integer tests keep the FP pipes free)
         const double dw1 = w1, dw2 = w2;
@@ -709,6 +718,7 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
         z[a].y = zi;
       }
       frame(k, nfirst + (int64_t)k * WARPS, yv, v1, v2, z);
+      vwrite += vstep;
     }
   }
   flush();

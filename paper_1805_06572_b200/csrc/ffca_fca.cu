@@ -59,13 +59,14 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
   const R* vr = (p.v_src ? (const R*)p.v_src : (const R*)p.v) + m * 2 * NF + f;
   const double fl = p.floor[g];
   const double invI = 1.0 / I;
-  Ring ring;
-  ring.init((unsigned char*)smem, warp, lane, (int64_t)blockIdx.x * 32, G, p.N, p.F, p.y, vr);
   const int64_t nfirst = n0 + warp;
+  Ring ring;
+  ring.init((unsigned char*)smem, warp, lane, (int64_t)blockIdx.x * 32, G, p.N, p.F, p.y, vr,
+            nfirst);
   const int K = nfirst < n1 ? (int)((n1 - nfirst + WARPS - 1) / WARPS) : 0;
 #pragma unroll
   for (int s = 0; s < FFCA_FCA_STAGES - 1; ++s) {
-    if (s < K) ring.issue(nfirst + (int64_t)s * WARPS);
+    if (s < K) ring.issue();
     cp_async_commit();
   }
 
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
   for (int k = 0; k < K; ++k) {
     const int64_t n = nfirst + (int64_t)k * WARPS;
     __syncwarp();  // every lane is done with the stage the next copy overwrites
-    if (k + FFCA_FCA_STAGES - 1 < K) ring.issue(n + (int64_t)(FFCA_FCA_STAGES - 1) * WARPS);
+    if (k + FFCA_FCA_STAGES - 1 < K) ring.issue();
     cp_async_commit();
     cp_async_wait<FFCA_FCA_STAGES - 1>();
     __syncwarp();  // the other lanes' copies of this stage are visible
