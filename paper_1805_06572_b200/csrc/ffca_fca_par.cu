@@ -400,16 +400,35 @@ __global__ void __launch_bounds__(64)
 #pragma unroll
       for (int s = 0; s < NS; ++s) sums[q][s] = cmk(0.0, 0.0);
     if (own) {
-#pragma unroll 2
-      for (int c = 0; c < nchunk; ++c) {
+      // CB chunks per batch: all their loads issued before the (ordered) adds
+      constexpr int NL = kFcaParts * NS * 2;
+      constexpr int CB = NL >= 64 ? 1 : 64 / NL;
+#pragma unroll 1
+      for (int c0 = 0; c0 < nchunk; c0 += CB) {
+        double t[CB][kFcaParts][NS][2];
 #pragma unroll
-        for (int q = 0; q < kFcaParts; ++q) {
-          const double* sp = Spart + ((size_t)c * kFcaParts + q) * NP * G + g;
+        for (int cb = 0; cb < CB; ++cb) {
+          if (c0 + cb >= nchunk) break;
 #pragma unroll
-          for (int s = 0; s < NS; ++s) {
-            sums[q][s].x += sp[(size_t)ire[s] * G];
-            sums[q][s].y += sp[(size_t)iim[s] * G];
+          for (int q = 0; q < kFcaParts; ++q) {
+            const double* sp = Spart + ((size_t)(c0 + cb) * kFcaParts + q) * NP * G + g;
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+              t[cb][q][s][0] = sp[(size_t)ire[s] * G];
+              t[cb][q][s][1] = sp[(size_t)iim[s] * G];
+            }
           }
+        }
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) {
+          if (c0 + cb >= nchunk) break;
+#pragma unroll
+          for (int q = 0; q < kFcaParts; ++q)
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+              sums[q][s].x += t[cb][q][s][0];
+              sums[q][s].y += t[cb][q][s][1];
+            }
         }
       }
     }

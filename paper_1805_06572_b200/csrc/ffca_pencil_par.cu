@@ -52,12 +52,24 @@ __global__ void __launch_bounds__(ParLayout<I>::WARPS * 32) pencil_par_kernel(co
   double part[EPL];
 #pragma unroll
   for (int t = 0; t < EPL; ++t) part[t] = 0.0;
-#pragma unroll 2
-  for (int c = 0; c < p.nchunk; ++c) {
-    const double* sp = p.Spart + (size_t)c * 2 * NP * G + g;
+  constexpr int CB = EPL >= 64 ? 1 : 64 / EPL;  // chunks per batch of loads
+#pragma unroll 1
+  for (int c0 = 0; c0 < p.nchunk; c0 += CB) {
+    double ld[CB][EPL];
 #pragma unroll
-    for (int t = 0; t < EPL; ++t)
-      if (r + Lay::LB * t < 2 * NP) part[t] += sp[(size_t)(r + Lay::LB * t) * G];
+    for (int cb = 0; cb < CB; ++cb) {
+      if (c0 + cb >= p.nchunk) break;
+      const double* sp = p.Spart + (size_t)(c0 + cb) * 2 * NP * G + g;
+#pragma unroll
+      for (int t = 0; t < EPL; ++t)
+        ld[cb][t] = (r + Lay::LB * t < 2 * NP) ? sp[(size_t)(r + Lay::LB * t) * G] : 0.0;
+    }
+#pragma unroll
+    for (int cb = 0; cb < CB; ++cb) {
+      if (c0 + cb >= p.nchunk) break;
+#pragma unroll
+      for (int t = 0; t < EPL; ++t) part[t] += ld[cb][t];
+    }
   }
 #pragma unroll
   for (int t = 0; t < EPL; ++t) {
