@@ -252,19 +252,24 @@ FFCA_DEV void jacobi_herm(double2 (&A)[I][I], double2 (&V)[I][I]) {
         const double mag2 = cabs2(apq);
         if (mag2 > kTol2 * fabs(A[p][p].x * A[q][q].x) && mag2 > 0.0) {
           rotated = true;
-          const double mag = sqrt(mag2);
+          // rotation parameters with MUFU seeds + Newton (rsqrt_fast /
+          // rcp_fast, ~1 ulp): this chain is the latency of the per-bin
+          // pencil refresh; c^2 + s^2 = 1 holds to rounding as before
+          const double rmag = rsqrt_fast(mag2);
+          const double mag = mag2 * rmag;
           // e^{-i phi} where apq = |apq| e^{i phi}
-          const double2 emi = cmk(apq.x / mag, -apq.y / mag);
+          const double2 emi = cmk(apq.x * rmag, -apq.y * rmag);
           const double app = A[p][p].x, aqq = A[q][q].x;
-          const double theta = (aqq - app) / (2.0 * mag);
+          const double theta = (aqq - app) * (0.5 * rmag);
           double t;
           if (fabs(theta) > 1e150) {
             t = 0.5 / theta;
           } else {
-            t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
+            const double h = fma(theta, theta, 1.0);
+            t = rcp_fast(fabs(theta) + h * rsqrt_fast(h));
             if (theta < 0.0) t = -t;
           }
-          const double c = 1.0 / sqrt(t * t + 1.0);
+          const double c = rsqrt_fast(fma(t, t, 1.0));
           const double s = t * c;
           // columns p, q of A (rows k != p, q), mirrored into rows p, q
 #pragma unroll
@@ -413,6 +418,10 @@ template <int I>
 FFCA_DEV bool cholesky(const double2 (&A)[I][I], double2 (&L)[I][I]);
 template <int I>
 FFCA_DEV void tril_inverse(const double2 (&L)[I][I], double2 (&Li)[I][I]);
+template <int I>
+FFCA_DEV bool cholesky_fast(const double2 (&A)[I][I], double2 (&L)[I][I], double (&ild)[I]);
+template <int I>
+FFCA_DEV void tril_inverse_d(const double2 (&L)[I][I], const double (&ild)[I], double2 (&Li)[I][I]);
 
 // Hermitian-definite pencil decomposition (reference pencil.py:85-135),
 // Cholesky-whitened like LAPACK zhegv: Psi = L L^H, eig(L^-1 Phi L^-H) = Q
@@ -430,9 +439,10 @@ FFCA_DEV int gevd_hpd(const double2 (&Phi)[I][I], const double2 (&Psi)[I][I], do
   for (int a = 0; a < I; ++a) tr += Psi[a][a].x;
   const double thr = kDefFloor * tr / I;
   double2 L[I][I], Li[I][I];
-  bool certified = cholesky<I>(Psi, L);
+  double ild[I];
+  bool certified = cholesky_fast<I>(Psi, L, ild);
   if (certified) {
-    tril_inverse<I>(L, Li);
+    tril_inverse_d<I>(L, ild, Li);
     double s = 0.0;
 #pragma unroll
     for (int a = 0; a < I; ++a)
@@ -527,7 +537,9 @@ FFCA_DEV bool lu_inverse(const double2 (&A)[I][I], double2 (&Inv)[I][I], double*
     }
     if (!(best > 0.0) || !isfinite(best)) ok = false;
     lad += 0.5 * log(best);
-    const double2 ip = cdiv(cmk(1.0, 0.0), M[k][k]);
+    // 1 / m = conj(m) / |m|^2 (the pivot's |m|^2 is `best`; MUFU seed + Newton)
+    const double ib = rcp_fast(best);
+    const double2 ip = cmk(M[k][k].x * ib, -M[k][k].y * ib);
 #pragma unroll
     for (int j = 0; j < I; ++j) {
       M[k][j] = cmul(M[k][j], ip);

@@ -166,20 +166,22 @@ FFCA_DEV void par_jacobi(const BinView<I>& v, int M, int V, int r, bool act) {
           const double mag2 = cabs2(apq);
           const double app = v.at(M, p, p).x, aqq = v.at(M, q, q).x;
           if (mag2 > kTol2 * fabs(app * aqq) && mag2 > 0.0) {
-            const double mag = sqrt(mag2);
-            const double theta = (aqq - app) / (2.0 * mag);
+            // MUFU seeds + Newton (as jacobi_herm)
+            const double rmag = rsqrt_fast(mag2);
+            const double theta = (aqq - app) * (0.5 * rmag);
             double t;
             if (fabs(theta) > 1e150) {
               t = 0.5 / theta;
             } else {
-              t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
+              const double h = fma(theta, theta, 1.0);
+              t = rcp_fast(fabs(theta) + h * rsqrt_fast(h));
               if (theta < 0.0) t = -t;
             }
-            const double c = 1.0 / sqrt(t * t + 1.0);
+            const double c = rsqrt_fast(fma(t, t, 1.0));
             rp[0] = c;
             rp[1] = t * c;
-            rp[2] = apq.x / mag;
-            rp[3] = -apq.y / mag;
+            rp[2] = apq.x * rmag;
+            rp[3] = -apq.y * rmag;
             rp[5] = 1.0;
           }
         }
@@ -267,14 +269,15 @@ FFCA_DEV int par_gevd(const BinView<I>& v, int r, bool own, double* min_sigma) {
       double d = v.at(kS2, j, j).x;
       for (int k = 0; k < j; ++k) d -= cabs2(v.at(kX, j, k));
       misc[0] = d;
-      v.at(kX, j, j) = cmk(sqrt(fmax(d, 0.0)), 0.0);
+      misc[1] = rsqrt_fast(fmax(d, 0.0));  // 1 / L_jj (MUFU seed + Newton)
+      v.at(kX, j, j) = cmk(fmax(d, 0.0) * misc[1], 0.0);
     }
     __syncwarp();
     chol_ok = chol_ok && (misc[0] > 0.0);
     if (own && r > j) {
       double2 sacc = v.at(kS2, r, j);
       for (int k = 0; k < j; ++k) sacc = csub(sacc, cmulc(v.at(kX, r, k), v.at(kX, j, k)));
-      v.at(kX, r, j) = cscale(sacc, 1.0 / v.at(kX, j, j).x);
+      v.at(kX, r, j) = cscale(sacc, misc[1]);
     }
     if (own && r < j) v.at(kX, r, j) = cmk(0.0, 0.0);
     __syncwarp();
@@ -291,7 +294,7 @@ FFCA_DEV int par_gevd(const BinView<I>& v, int r, bool own, double* min_sigma) {
       }
       double2 sacc = cmk(rr == c ? 1.0 : 0.0, 0.0);
       for (int k = c; k < rr; ++k) sacc = csub(sacc, cmul(v.at(kX, rr, k), v.at(kT, k, c)));
-      const double2 val = cscale(sacc, 1.0 / v.at(kX, rr, rr).x);
+      const double2 val = cscale(sacc, rcp_fast(v.at(kX, rr, rr).x));
       v.at(kT, rr, c) = val;
       fro += cabs2(val);
     }
@@ -468,7 +471,9 @@ FFCA_DEV double par_lu_inverse(const BinView<I>& v, int Msrc, int r, bool own, b
     }
     __syncwarp();
     if (own && r == k) {
-      const double2 ip = cdiv(cmk(1.0, 0.0), v.at(kX, k, k));
+      const double2 pv = v.at(kX, k, k);  // 1 / pv = conj(pv) / |pv|^2
+      const double ib = rcp_fast(cabs2(pv));
+      const double2 ip = cmk(pv.x * ib, -pv.y * ib);
 #pragma unroll
       for (int c = 0; c < I; ++c) {
         v.at(kX, k, c) = cmul(v.at(kX, k, c), ip);
