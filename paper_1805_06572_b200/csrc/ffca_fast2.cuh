@@ -16,6 +16,8 @@
 //    update-only pass carries no dead code.
 #pragma once
 
+#include <type_traits>
+
 #include "ffca_internal.cuh"
 
 namespace ffca {
@@ -286,14 +288,24 @@ struct FrameRing {
   }
 };
 
-template <int I, typename R, int WARPS, int STAGES, bool MU = false>
+// complex64 update pass at even orders: its FP64 S~ accumulators live in
+// shared memory (fed every kF32Block frames from the packed FP32 block sums),
+// which frees 64 registers for a 4th CTA per SM (the pass is issue-bound)
+template <int I, typename R, bool UPDATE, bool LL, bool MU>
+struct SmemAcc {
+  static constexpr bool value = std::is_same<R, float>::value && (I % 2 == 0) && UPDATE && !LL && !MU;
+};
+
+template <int I, typename R, int WARPS, int STAGES, bool MU = false, bool SACC = false>
 struct Fast2Smem {
   static constexpr int NE = 2 * I * I + 1;
   static constexpr size_t RING = (size_t)STAGES * WARPS * RingSlot<I, R>::WARP_BYTES;
   static constexpr size_t RED = (size_t)(WARPS - 1) * NE * 32 * sizeof(double);
   static constexpr size_t PB = (size_t)I * I * 32 * sizeof(typename Math<R>::T2);  // P tile
   static constexpr size_t WB = MU ? PB : 0;                           // W tile, after P
-  static constexpr size_t BYTES = (RING + PB + WB) > RED ? (RING + PB + WB) : RED;
+  static constexpr size_t ACC = SACC ? (size_t)2 * I * I * WARPS * 32 * sizeof(double) : 0;
+  static constexpr size_t MAIN = RING + PB + WB + ACC;  // accumulators after the tiles
+  static constexpr size_t BYTES = MAIN > RED ? MAIN : RED;
 };
 
 #ifndef FAST2_MINB
@@ -311,9 +323,20 @@ struct Fast2Smem {
 #ifndef FAST2_UNROLL
 #define FAST2_UNROLL 1  // frames per loop trip (ILP experiments)
 #endif
+#ifndef FAST2_SACC_STAGES
+#define FAST2_SACC_STAGES 3  // ring depth of the complex64 pass with shared accumulators
+#endif
+template <int I, typename R, bool UPDATE, bool LL, bool MU>
+constexpr int fast2_stages() {
+  return MU ? FAST2_MU_STAGES : (SmemAcc<I, R, UPDATE, LL, MU>::value ? FAST2_SACC_STAGES : FAST2_STAGES);
+}
+template <int I, typename R, bool UPDATE, bool LL, bool MU>
+constexpr int fast2_minb() {
+  return MU ? FAST2_MU_MINB : (SmemAcc<I, R, UPDATE, LL, MU>::value ? 4 : FAST2_MINB);
+}
 
 template <int I, typename R, int WARPS, int STAGES, bool UPDATE, bool LL, bool MU>
-__global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) fast_em2_kernel(const FastIterParams p) {
+__global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>())) fast_em2_kernel(const FastIterParams p) {
   using C = typename CplxOf<R>::type;
   using Slot = RingSlot<I, R>;
   using T = typename Math<R>::T;    // per-point compute type
@@ -341,7 +364,9 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
   // P lives in shared memory (bin-minor SoA after the frame ring): the 4
   // warps of the CTA work on the same 32 bins, so one 16*I*I-byte column per
   // lane serves all of them and frees the registers for the accumulators.
-  T2* sP = (T2*)(smem_raw + Fast2Smem<I, R, WARPS, STAGES, MU>::RING);
+  constexpr bool kSacc = SmemAcc<I, R, UPDATE, LL, MU>::value;
+  using Sm = Fast2Smem<I, R, WARPS, STAGES, MU, kSacc>;
+  T2* sP = (T2*)(smem_raw + Sm::RING);
   for (int e = warp; e < NP; e += WARPS) sP[e * 32 + lane] = Math<R>::c2(p.P[g * NP + e]);
   // W = P^{-H} for the image write (last pass only), same bin-minor tile layout
   T2* sW = sP + NP * 32;
@@ -357,12 +382,19 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
   const T fl = (T)p.floor[g];
   constexpr T invI = T(1) / I;
 
-  double acc[2][NP];
+  double acc[2][kSacc ? 1 : NP];  // (kSacc: in shared memory, accS)
+  // accS[(j NP + e) * WARPS * 32 + tid]: thread-minor, conflict-free
+  double* accS = (double*)(smem_raw + Sm::RING + Sm::PB + Sm::WB) + threadIdx.x;
+  constexpr int kAccStride = WARPS * 32;
+  if constexpr (kSacc) {
+#pragma unroll
+    for (int e = 0; e < 2 * NP; ++e) accS[e * kAccStride] = 0.0;
+  }
   T accb[2][kBlk ? NP : 1];  // FP32 block sums (complex64 only)
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
 #pragma unroll
-    for (int e = 0; e < NP; ++e) acc[j][e] = 0.0;
+    for (int e = 0; e < (kSacc ? 1 : NP); ++e) acc[j][e] = 0.0;
 #pragma unroll
     for (int e = 0; e < (kBlk ? NP : 1); ++e) accb[j][e] = T(0);
   }
@@ -378,7 +410,16 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
       acc[j][e] = fma((double)a, (double)b, acc[j][e]);
   };
   auto flush = [&]() {
-    if constexpr (kF2) {
+    if constexpr (kSacc) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < NP / 2; ++e) {
+          accS[(j * NP + 2 * e) * kAccStride] += (double)acc2[j][e].x;
+          accS[(j * NP + 2 * e + 1) * kAccStride] += (double)acc2[j][e].y;
+          acc2[j][e] = make_float2(0.f, 0.f);
+        }
+    } else if constexpr (kF2) {
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -728,6 +769,20 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
                  (unsigned long long)((m * p.N + (bad_n - 1)) * p.F + f));
 
   if (!UPDATE && !LL) return;
+  if constexpr (kSacc) {
+    // --- cross-warp reduction straight from the shared accumulators ---
+    __syncthreads();
+    if (warp != 0 || !active) return;
+    double* sp = p.Spart + (size_t)blockIdx.y * 2 * NP * G + g;
+#pragma unroll
+    for (int e = 0; e < 2 * NP; ++e) {
+      double t = accS[e * kAccStride];
+#pragma unroll
+      for (int w = 1; w < WARPS; ++w) t += accS[e * kAccStride + w * 32];
+      sp[(size_t)e * G] = t;
+    }
+    return;
+  } else {
   // --- cross-warp reduction (fixed order), reusing the ring memory ---
   __syncthreads();
   double* red = (double*)smem_raw;
@@ -765,13 +820,14 @@ __global__ void __launch_bounds__(WARPS * 32, MU ? FAST2_MU_MINB : FAST2_MINB) f
     }
   }
   if (LL) p.llbin[(size_t)c * G + g] = llacc;
+  }
 }
 
 template <int I, typename R, bool UPDATE, bool LL, bool MU>
 cudaError_t launch_fast2_variant(const FastIterParams& p, cudaStream_t s) {
   constexpr int WARPS = kWarps;
-  constexpr int STAGES = MU ? FAST2_MU_STAGES : FAST2_STAGES;
-  using Sm = Fast2Smem<I, R, WARPS, STAGES, MU>;
+  constexpr int STAGES = fast2_stages<I, R, UPDATE, LL, MU>();
+  using Sm = Fast2Smem<I, R, WARPS, STAGES, MU, SmemAcc<I, R, UPDATE, LL, MU>::value>;
   auto kern = fast_em2_kernel<I, R, WARPS, STAGES, UPDATE, LL, MU>;
   static bool configured = false;
   if (!configured) {
@@ -787,8 +843,9 @@ cudaError_t launch_fast2_variant(const FastIterParams& p, cudaStream_t s) {
 
 template <int I, typename R>
 int fast2_blocks_per_sm() {
-  using Sm = Fast2Smem<I, R, kWarps, FAST2_STAGES, false>;
-  auto kern = fast_em2_kernel<I, R, kWarps, FAST2_STAGES, true, false, false>;
+  constexpr int STAGES = fast2_stages<I, R, true, false, false>();
+  using Sm = Fast2Smem<I, R, kWarps, STAGES, false, SmemAcc<I, R, true, false, false>::value>;
+  auto kern = fast_em2_kernel<I, R, kWarps, STAGES, true, false, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sm::BYTES);
   int n = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kWarps * 32, Sm::BYTES);

@@ -186,6 +186,7 @@ def test_graph_replay_equals_stream_launches(algorithm):
     V = torch.stack([i.v for i in inits])
     S = torch.stack([i.S for i in inits])
     FL = torch.stack([i.v_floor for i in inits])
+    V0 = V.clone()
     ref = run_device(algorithm, Y, V, S, FL, 4, likelihood=True, timing=False)
     out = {"images": torch.empty_like(ref.images), "S": torch.empty_like(ref.S),
            "v": torch.empty_like(ref.v), "loglik": torch.empty_like(ref.loglik)}
@@ -201,6 +202,11 @@ def test_graph_replay_equals_stream_launches(algorithm):
     Y.copy_(Y2)
     r = run_device(algorithm, Y, V, S, FL, 4, likelihood=True, timing=False, out=out, graph=True)
     assert torch.equal(r.images, ref2.images) and torch.equal(r.loglik, ref2.loglik)
+    # the initial powers are read through v_in, never written
+    assert torch.equal(V, V0)
+    r0 = run_device(algorithm, Y, V, S, FL, 0, likelihood=True, timing=False,
+                    out={"v": torch.empty_like(V)})
+    assert torch.equal(r0.v, V0) and torch.equal(V, V0)
 
 
 def test_mismatched_output_buffers_are_rejected():
