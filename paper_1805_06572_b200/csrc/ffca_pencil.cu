@@ -28,15 +28,27 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
     double s[2][NP];
 #pragma unroll
     for (int e = 0; e < NP; ++e) s[0][e] = s[1][e] = 0.0;
-    // unrolled: the loads of several chunks are in flight together; the adds
+    // CB chunks per batch: all their loads are issued before the adds, which
     // keep the chunk order (bitwise identical sums)
-#pragma unroll 4
-    for (int c = 0; c < p.nchunk; ++c) {
-      const double* sp = p.Spart + (size_t)c * 2 * NP * G + g;
+    constexpr int CB = 2 * NP >= 64 ? 1 : (64 / (2 * NP) > 8 ? 8 : 64 / (2 * NP));
+#pragma unroll 1
+    for (int c0 = 0; c0 < p.nchunk; c0 += CB) {
+      double ld[CB][2 * NP];
 #pragma unroll
-      for (int e = 0; e < NP; ++e) {
-        s[0][e] += sp[(size_t)e * G];
-        s[1][e] += sp[(size_t)(NP + e) * G];
+      for (int cb = 0; cb < CB; ++cb) {
+        if (c0 + cb >= p.nchunk) break;
+        const double* sp = p.Spart + (size_t)(c0 + cb) * 2 * NP * G + g;
+#pragma unroll
+        for (int e = 0; e < 2 * NP; ++e) ld[cb][e] = sp[(size_t)e * G];
+      }
+#pragma unroll
+      for (int cb = 0; cb < CB; ++cb) {
+        if (c0 + cb >= p.nchunk) break;
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          s[0][e] += ld[cb][e];
+          s[1][e] += ld[cb][NP + e];
+        }
       }
     }
     const double invN = 1.0 / (double)p.N;
