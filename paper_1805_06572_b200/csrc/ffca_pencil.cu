@@ -30,7 +30,8 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
     for (int e = 0; e < NP; ++e) s[0][e] = s[1][e] = 0.0;
     // CB chunks per batch: all their loads are issued before the adds, which
     // keep the chunk order (bitwise identical sums)
-    constexpr int CB = 2 * NP >= 64 ? 1 : (64 / (2 * NP) > 8 ? 8 : 64 / (2 * NP));
+    // loads in flight per batch: ~64 (I = 4: register bound), ~108 at I = 3
+    constexpr int CB = I == 3 ? 6 : (2 * NP >= 64 ? 1 : (64 / (2 * NP) > 8 ? 8 : 64 / (2 * NP)));
 #pragma unroll 1
     for (int c0 = 0; c0 < p.nchunk; c0 += CB) {
       double ld[CB][2 * NP];
