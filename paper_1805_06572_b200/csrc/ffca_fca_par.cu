@@ -3,10 +3,10 @@
 // A point's frame-wise inverse (reference _kernels_numba.py:246-325) needs
 // I x I complex matrices: at I = 8 ~1 KB each, so the per-thread kernel
 // (ffca_fca.cu) spills heavily. Here a group of 8 lanes owns one bin and
-// streams its frames; the per-point matrix lives in shared memory:
-//   R = v1 S1 + v2 S2 -> Cholesky L (column-sequential, row-parallel)
-//   L^-1 (column-parallel, in place)   u = L^-1 y, x = L^-H u = R^-1 y
-//   Rinv = L^-H L^-1 entries, x x^H entries, traces, w_j, v update,
+// streams its frames; lane r owns row r of the per-point matrices:
+//   R = v1 S1 + v2 S2 -> Rinv by Gauss-Jordan (pivot rows published through
+//   shared memory, rows eliminated in registers), x = Rinv y,
+//   Rinv and x x^H entries, traces, w_j, v update,
 //   B_j += v_j^2/w_j x x^H, X_j += v1 v2/w_j Rinv  (as fca_em_kernel: the
 //   I x I products of Phi_j are applied once per bin in fca_finish_kernel).
 // The I(I+1)/2 Hermitian entries are dealt to the lanes circulantly: lane r
@@ -29,9 +29,10 @@ struct FcaParLayout {
   static constexpr int NP = I * I;
   static constexpr int NS = I / 2 + 1;          // entry slots per lane
   static constexpr int MATD = I * LD * 2;       // doubles per padded complex matrix
-  // per group: 2 packed S (2 NP) + 1 matrix (R / L / L^-1) + 3 vectors (2I each)
-  // + misc (2) + inverse diagonal (I), rounded to an odd number of 16-B units
-  static constexpr int RAW = 2 * NP + MATD + 6 * I + 2 + I;
+  // per group: 2 packed S (2 NP) + 1 matrix (rows of Rinv) + 3 vectors (2I
+  // each) + misc (2) + pivot row and its inverse row (4I), rounded to an odd
+  // number of 16-B units
+  static constexpr int RAW = 2 * NP + MATD + 6 * I + 2 + 4 * I;
   static constexpr int U16 = (RAW + 1) / 2;
   static constexpr int GROUP_DOUBLES = 2 * ((U16 % 2) ? U16 : U16 + 1);
   static constexpr size_t SMEM = (size_t)BPB * GROUP_DOUBLES * sizeof(double);
@@ -49,7 +50,7 @@ FFCA_DEV double2 packed_get(const double* S, int a, int b) {
 
 template <int I, typename R>
 #ifndef FCA_PAR_MINB
-#define FCA_PAR_MINB 8  // CTAs per SM the lane-parallel FCA pass is register-budgeted for
+#define FCA_PAR_MINB 6  // CTAs per SM the lane-parallel FCA pass is register-budgeted for
 #endif
 __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32, FCA_PAR_MINB) fca_par_kernel(const FcaIterParams p) {
   using Lay = FcaParLayout<I>;
@@ -72,10 +73,10 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32, FCA_PAR_MINB) fca
   double* Sp = base;                        // [2][NP] packed: S1, S2
   double2* Lm = (double2*)(base + 2 * NP);  // R -> L -> L^-1 (lower triangles)
   double2* vy = Lm + I * Lay::LD;           // y
-  double2* vu = vy + I;                     // L^-1 y
-  double2* vx = vu + I;                     // R^-1 y
+  double2* vx = vy + I;                     // R^-1 y (vy + 2I: spare)
   double* misc = (double*)(vx + I);
-  double* ildm = misc + 2;                  // inverse diagonal of L
+  double2* prow = (double2*)(misc + 2);     // published pivot row of R
+  double2* pinv = prow + I;                 // and of the inverse
   auto at = [&](int a, int b) -> double2& { return Lm[a * Lay::LD + b]; };
 
   for (int e = r; e < 2 * NP; e += LB) Sp[e] = p.Sp[(size_t)e * G + g];
@@ -125,96 +126,74 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32, FCA_PAR_MINB) fca
       v1n = (double)vr[(n + 1) * p.F];
       v2n = (double)vr[NF + (n + 1) * p.F];
     }
+    // R = v1 S1 + v2 S2: row r in registers, with the row of the inverse
+    double2 rrow[I], irow[I];
     if (own) {
       vy[r] = ycur;
 #pragma unroll
       for (int c = 0; c < I; ++c) {
-        if (c > r) continue;
         const double2 s1 = packed_get<I>(S1, r, c), s2 = packed_get<I>(S2, r, c);
-        at(r, c) = cmk(v1 * s1.x + v2 * s2.x, v1 * s1.y + v2 * s2.y);
+        rrow[c] = cmk(v1 * s1.x + v2 * s2.x, v1 * s1.y + v2 * s2.y);
+        irow[c] = cmk(c == r ? 1.0 : 0.0, 0.0);
       }
     }
-    __syncwarp();
-    // Cholesky in place (lower), column-sequential. Every loop below is
-    // unrolled over compile-time indices with the triangular bounds as
-    // predicates: independent products interleave (ILP) instead of forming
-    // one dependent chain of shared-memory loads per loop.
+    // Frame-wise inverse by Gauss-Jordan elimination without pivoting (R is
+    // Hermitian positive definite: the pivots are its LDL^H pivots d_p, all
+    // > 0 iff R is PD — the reference's singular-mixture test). Step p: lane p
+    // publishes its (unnormalised) pivot row, every other lane eliminates
+    // column p from its row in registers (I complex MACs, independent across
+    // columns); each row is scaled by 1/d_r at the end. One warp barrier per
+    // step instead of the column-sequential Cholesky + triangular inverse +
+    // L^-H L^-1 chain.
     bool okc = true;
+    double dr = 1.0;
 #pragma unroll
-    for (int j = 0; j < I; ++j) {
-      if (own && r == j) {
-        double d = at(j, j).x;
+    for (int q = 0; q < I; ++q) {
+      if (own && r == q) {
 #pragma unroll
-        for (int k = 0; k < j; ++k) d -= cabs2(at(j, k));
-        const double il = rsqrt_fast(d);
-        misc[0] = d;
-        ildm[j] = il;
-        at(j, j) = cmk(d * il, 0.0);
+        for (int c = 0; c < I; ++c) {
+          if (c >= q) prow[c] = rrow[c];
+          if (c <= q) pinv[c] = irow[c];
+        }
       }
       __syncwarp();
-      okc = okc && misc[0] > 0.0;
-      if (own && r > j) {
-        double2 s = at(r, j);
+      const double d = prow[q].x;
+      okc = okc && d > 0.0;
+      if (own) {
+        if (r == q) {
+          dr = d;
+        } else {
+          const double2 fct = cscale(rrow[q], rcp_fast(d));
 #pragma unroll
-        for (int k = 0; k < j; ++k) s = csub(s, cmulc(at(r, k), at(j, k)));
-        at(r, j) = cscale(s, ildm[j]);
+          for (int c = 0; c < I; ++c) {
+            if (c > q) rrow[c] = csub(rrow[c], cmul(fct, prow[c]));
+            if (c <= q) irow[c] = csub(irow[c], cmul(fct, pinv[c]));
+          }
+        }
       }
-      __syncwarp();
+      __syncwarp();  // prow / pinv are rewritten by the next pivot
     }
     if (!okc && bad_n == 0) bad_n = n + 1;
-    // L^-1, column-parallel: lane r builds column r in registers, then (after
-    // every lane has read L) writes it over L
-    const double lrr = own ? at(rr, rr).x : 1.0;
-    double2 col[I];
-    if (own) {
-#pragma unroll
-      for (int q = 0; q < I; ++q) {
-        double2 sacc = cmk(q == r ? 1.0 : 0.0, 0.0);
-#pragma unroll
-        for (int k = 0; k < q; ++k)
-          if (k >= r) sacc = csub(sacc, cmul(at(q, k), col[k]));
-        col[q] = (q >= r) ? cscale(sacc, ildm[q]) : cmk(0.0, 0.0);
-      }
-    }
-    __syncwarp();
-    if (own) {
-#pragma unroll
-      for (int q = 0; q < I; ++q)
-        if (q >= r) at(q, r) = col[q];
-    }
-    __syncwarp();
-    // u = L^-1 y (row r); Rinv entries of this lane's slots
+    // row r of Rinv (into shared memory for the slot reads), x = Rinv y
     double2 ri[NS];
     double lquad = 0.0;
     if (own) {
-      double2 sacc = cmk(0.0, 0.0);
+      const double idr = rcp_fast(dr);
+      double2 xr = cmk(0.0, 0.0);
 #pragma unroll
-      for (int k = 0; k < I; ++k)
-        if (k <= r) sacc = cadd(sacc, cmul(at(r, k), vy[k]));
-      vu[r] = sacc;
-      lquad = cabs2(sacc);
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        const int b0 = sb[s];
-        const int kmin = b0 > rr ? b0 : rr;
-        double2 t = cmk(0.0, 0.0);
-#pragma unroll
-        for (int k = 0; k < I; ++k)
-          if (k >= kmin) t = cadd(t, cconjmul(at(k, rr), at(k, b0)));
-        ri[s] = t;
+      for (int c = 0; c < I; ++c) {
+        irow[c] = cscale(irow[c], idr);
+        at(r, c) = irow[c];
+        xr = cadd(xr, cmul(irow[c], vy[c]));
       }
-    }
-    __syncwarp();
-    if (do_ll) llacc += group_sum<LB>(own ? 2.0 * log(lrr) + lquad : 0.0);
-    // x = L^-H u (row r)
-    if (own) {
-      double2 sacc = cmk(0.0, 0.0);
+      vx[r] = xr;
+      lquad = ycur.x * xr.x + ycur.y * xr.y;  // Re conj(y_r) x_r
 #pragma unroll
-      for (int k = 0; k < I; ++k)
-        if (k >= r) sacc = cadd(sacc, cconjmul(at(k, r), vu[k]));
-      vx[r] = sacc;
+      for (int s = 0; s < NS; ++s) ri[s] = at(r, sb[s]);
     }
     __syncwarp();
+    // log det R + y^H Rinv y = sum_r log d_r + Re y^H x
+    if (do_ll) llacc += group_sum<LB>(own ? log(dr) + lquad : 0.0);
     if (p.mu_out != nullptr && active && own) {
       // mu_j = v_j S_j x (row r; the image pass only)
       double2 s1 = cmk(0.0, 0.0), s2 = cmk(0.0, 0.0);
