@@ -29,10 +29,10 @@ struct FcaParLayout {
   static constexpr int NP = I * I;
   static constexpr int NS = I / 2 + 1;          // entry slots per lane
   static constexpr int MATD = I * LD * 2;       // doubles per padded complex matrix
-  // per group: 2 packed S (2 NP) + 1 matrix (rows of Rinv) + 3 vectors (2I
-  // each) + misc (2) + pivot row and its inverse row (4I), rounded to an odd
-  // number of 16-B units
-  static constexpr int RAW = 2 * NP + MATD + 6 * I + 2 + 4 * I;
+  // per group: S1, S2 unpacked (2 MATD) + 1 matrix (rows of Rinv) + 3 vectors
+  // (2I each) + misc (2) + pivot row and its inverse row (4I), rounded to an
+  // odd number of 16-B units
+  static constexpr int RAW = 3 * MATD + 6 * I + 2 + 4 * I;
   static constexpr int U16 = (RAW + 1) / 2;
   static constexpr int GROUP_DOUBLES = 2 * ((U16 % 2) ? U16 : U16 + 1);
   static constexpr size_t SMEM = (size_t)BPB * GROUP_DOUBLES * sizeof(double);
@@ -70,8 +70,8 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32, FCA_PAR_MINB) fca
   const int rr = own ? r : 0;
   const int64_t m = g / p.F, f = g - m * p.F;
   double* base = sm + (size_t)grp * Lay::GROUP_DOUBLES;
-  double* Sp = base;                        // [2][NP] packed: S1, S2
-  double2* Lm = (double2*)(base + 2 * NP);  // R -> L -> L^-1 (lower triangles)
+  double2* SF = (double2*)base;             // [2][I][LD]: S1, S2 unpacked (row reads, no branches)
+  double2* Lm = SF + 2 * I * Lay::LD;       // rows of Rinv
   double2* vy = Lm + I * Lay::LD;           // y
   double2* vx = vy + I;                     // R^-1 y (vy + 2I: spare)
   double* misc = (double*)(vx + I);
@@ -79,10 +79,25 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32, FCA_PAR_MINB) fca
   double2* pinv = prow + I;                 // and of the inverse
   auto at = [&](int a, int b) -> double2& { return Lm[a * Lay::LD + b]; };
 
-  for (int e = r; e < 2 * NP; e += LB) Sp[e] = p.Sp[(size_t)e * G + g];
+  if (own) {  // row r of both covariances from the packed SoA copy
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < I; ++c) {
+        const double* bj = p.Sp + (size_t)j * NP * G + g;
+        double2 e;
+        if (c == r)
+          e = cmk(bj[(size_t)r * G], 0.0);
+        else if (r < c)
+          e = cmk(bj[(size_t)Herm<I>::re(r, c) * G], bj[(size_t)Herm<I>::im(r, c) * G]);
+        else
+          e = cmk(bj[(size_t)Herm<I>::re(c, r) * G], -bj[(size_t)Herm<I>::im(c, r) * G]);
+        SF[(j * I + r) * Lay::LD + c] = e;
+      }
+  }
   __syncwarp();
-  const double* S1 = Sp;
-  const double* S2 = Sp + NP;
+  auto S1 = [&](int a, int b) -> double2 { return SF[a * Lay::LD + b]; };
+  auto S2 = [&](int a, int b) -> double2 { return SF[(I + a) * Lay::LD + b]; };
   // this lane's entry slots: (a0, b0) = (r, r + s mod I)
   int sb[NS];
   bool sv[NS];
@@ -132,7 +147,7 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32, FCA_PAR_MINB) fca
       vy[r] = ycur;
 #pragma unroll
       for (int c = 0; c < I; ++c) {
-        const double2 s1 = packed_get<I>(S1, r, c), s2 = packed_get<I>(S2, r, c);
+        const double2 s1 = S1(r, c), s2 = S2(r, c);
         rrow[c] = cmk(v1 * s1.x + v2 * s2.x, v1 * s1.y + v2 * s2.y);
         irow[c] = cmk(c == r ? 1.0 : 0.0, 0.0);
       }
@@ -199,8 +214,8 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32, FCA_PAR_MINB) fca
       double2 s1 = cmk(0.0, 0.0), s2 = cmk(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < I; ++k) {
-        s1 = cadd(s1, cmul(packed_get<I>(S1, r, k), vx[k]));
-        s2 = cadd(s2, cmul(packed_get<I>(S2, r, k), vx[k]));
+        s1 = cadd(s1, cmul(S1(r, k), vx[k]));
+        s2 = cadd(s2, cmul(S2(r, k), vx[k]));
       }
       C* mo = (C*)p.mu_out;
       mo[(((m * 2 + 0) * p.N + n) * p.F + f) * I + r] = from_c128<R>(cscale(s1, v1));
@@ -218,7 +233,7 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32, FCA_PAR_MINB) fca
         xe[s] = cmulc(xr, xb);  // x_a0 conj(x_b0)
         if (s == 0) xe[s].y = 0.0;
         const double wgt = sv[s] ? (s == 0 ? 1.0 : 2.0) : 0.0;
-        const double2 s1 = packed_get<I>(S1, rr, sb[s]), s2 = packed_get<I>(S2, rr, sb[s]);
+        const double2 s1 = S1(rr, sb[s]), s2 = S2(rr, sb[s]);
         qf1 += wgt * (s1.x * xe[s].x + s1.y * xe[s].y);
         qf2 += wgt * (s2.x * xe[s].x + s2.y * xe[s].y);
         tR1 += wgt * (s1.x * ri[s].x + s1.y * ri[s].y);
