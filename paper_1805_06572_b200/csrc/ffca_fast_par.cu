@@ -29,7 +29,7 @@ struct FastParLayout {
   static constexpr int LB = 8;
   static constexpr int WARPS = 2;
   static constexpr int BPB = WARPS * 32 / LB;  // bins per CTA
-  // per group: y (2I), z (2I), g1 (I), g2 (I) doubles; odd # of 16-B units
+  // per group: y (2I), z (2I), (g1, g2) (2I) doubles; odd # of 16-B units
   static constexpr int RAW = 6 * I;
   static constexpr int U16 = (RAW + 1) / 2;
   static constexpr int GROUP_DOUBLES = 2 * ((U16 % 2) ? U16 : U16 + 1);
@@ -61,8 +61,7 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, FAST_PAR_MINB) f
   double* base = sm + (size_t)grp * Lay::GROUP_DOUBLES;
   double2* sy = (double2*)base;      // y
   double2* sz = sy + I;              // z
-  double* sg1 = (double*)(sz + I);   // g1
-  double* sg2 = sg1 + I;             // g2
+  double2* sgg = sz + I;             // (g1, g2): one 16-B read per exchanged channel
 
   double2 pc[I];  // column rr of P
   double2 wr[I];  // row rr of W = P^-H (images only)
@@ -121,20 +120,25 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, FAST_PAR_MINB) f
                         (size_t)threadIdx.x * SLOT;
   constexpr size_t kStageStride = (size_t)Lay::WARPS * 32 * SLOT;
   const int K = (int)(n1 - n0 > 0 ? n1 - n0 : 0);
+  // frames are issued in order: running pointers, no per-frame n * F products
+  const C* ynext = yb + n0 * p.F * I + rr;
+  const R* vnext = vr + n0 * p.F;
+  const int64_t ystep = p.F * I;
   auto issue = [&](int k) {
-    const int64_t n = n0 + k;
     unsigned char* slot = ring + (size_t)(k % kStages) * kStageStride;
     if constexpr (YB == 16)
-      cp_async16(slot, yb + n * p.F * I + rr);
+      cp_async16(slot, ynext);
     else
-      cp_async8(slot, yb + n * p.F * I + rr);
+      cp_async8(slot, ynext);
     if constexpr (VB == 8) {
-      cp_async8(slot + YB, vr + n * p.F);
-      cp_async8(slot + YB + 8, vr + NF + n * p.F);
+      cp_async8(slot + YB, vnext);
+      cp_async8(slot + YB + 8, vnext + NF);
     } else {
-      cp_async4(slot + YB, vr + n * p.F);
-      cp_async4(slot + YB + 4, vr + NF + n * p.F);
+      cp_async4(slot + YB, vnext);
+      cp_async4(slot + YB + 4, vnext + NF);
     }
+    ynext += ystep;
+    vnext += p.F;
   };
 #pragma unroll
   for (int k = 0; k < kStages - 1; ++k) {
@@ -172,8 +176,7 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, FAST_PAR_MINB) f
     if (LL && own) llacc += log(den) + pz * rden;
     if (own) {
       sz[r] = cmk(zr, zi);
-      sg1[r] = g1;
-      sg2[r] = g2;
+      sgg[r] = cmk(g1, g2);
     }
     double w1 = 0.0, w2 = 0.0;
     if (UPDATE) {
@@ -206,7 +209,8 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, FAST_PAR_MINB) f
         const double2 zc = sz[cc];
         const double xr = fma(zr, zc.x, zi * zc.y);   // z_r conj(z_c)
         const double xi = fma(zi, zc.x, -zr * zc.y);
-        const double k1 = h1 * sg1[cc], k2 = h2 * sg2[cc];
+        const double2 gg = sgg[cc];
+        const double k1 = h1 * gg.x, k2 = h2 * gg.y;
         acc1[so] = fma(k1, xr, acc1[so]);
         acc1i[so] = fma(k1, xi, acc1i[so]);
         acc2[so] = fma(k2, xr, acc2[so]);
@@ -221,7 +225,7 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, FAST_PAR_MINB) f
 #pragma unroll
         for (int b = 0; b < I; ++b) {
           const double2 zb = sz[b];
-          const double gb = sg1[b];
+          const double gb = sgg[b].x;
           const double mx = gb * zb.x, my = gb * zb.y;
           sx = fma(wr[b].x, mx, fma(-wr[b].y, my, sx));
           sy_ = fma(wr[b].x, my, fma(wr[b].y, mx, sy_));
