@@ -220,18 +220,20 @@ FFCA_DEV void par_jacobi(const BinView<I>& v, int M, int V, int r, bool act) {
           const double2 epi = cmk(rp[2], -rp[3]);  // conj(emi)
           const double2 xp = v.at(M, p, r);
           const double2 xq = cmul(v.at(M, q, r), epi);
-          v.at(M, p, r) = cmk(c * xp.x - sn * xq.x, c * xp.y - sn * xq.y);
-          v.at(M, q, r) = cmk(sn * xp.x + c * xq.x, sn * xp.y + c * xq.y);
+          double2 np_ = cmk(c * xp.x - sn * xq.x, c * xp.y - sn * xq.y);
+          double2 nq_ = cmk(sn * xp.x + c * xq.x, sn * xp.y + c * xq.y);
+          // pin the rotated 2x2 block here (its column owners are p and q):
+          // off-diagonal exactly zero, diagonal exactly real
+          if (r == p) {
+            np_.y = 0.0;
+            nq_ = cmk(0.0, 0.0);
+          } else if (r == q) {
+            np_ = cmk(0.0, 0.0);
+            nq_.y = 0.0;
+          }
+          v.at(M, p, r) = np_;
+          v.at(M, q, r) = nq_;
         }
-      }
-      __syncwarp();
-      if (act && r < Lay::NPAIR && rot[6 * r + 5] != 0.0) {  // pin the rotated 2x2 block
-        int p, q;
-        rr_pair<I>(k, r, p, q);
-        v.at(M, p, q) = cmk(0.0, 0.0);
-        v.at(M, q, p) = cmk(0.0, 0.0);
-        v.at(M, p, p).y = 0.0;
-        v.at(M, q, q).y = 0.0;
       }
       rotated = rotated || any;
       __syncwarp();
