@@ -86,6 +86,22 @@ FFCA_DEV double2 cconjmul(double2 a, double2 b) {
   return cmk(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
 }
 FFCA_DEV double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+// Fused complex multiply-accumulates: 4 DFMA per complex MAC instead of the
+// DMUL + DFMA + DADD per component that s + a*b compiles to (the compiler may
+// not reassociate s + (p - q)); rounding differs from the unfused form at the
+// last-bit level.
+FFCA_DEV double2 cmac(double2 s, double2 a, double2 b) {  // s + a b
+  return cmk(fma(a.x, b.x, fma(-a.y, b.y, s.x)), fma(a.x, b.y, fma(a.y, b.x, s.y)));
+}
+FFCA_DEV double2 cmsub(double2 s, double2 a, double2 b) {  // s - a b
+  return cmk(fma(-a.x, b.x, fma(a.y, b.y, s.x)), fma(-a.x, b.y, fma(-a.y, b.x, s.y)));
+}
+FFCA_DEV double2 cmsubc(double2 s, double2 a, double2 b) {  // s - a conj(b)
+  return cmk(fma(-a.x, b.x, fma(-a.y, b.y, s.x)), fma(-a.y, b.x, fma(a.x, b.y, s.y)));
+}
+FFCA_DEV double2 cmac_cj(double2 s, double2 a, double2 b) {  // s + conj(a) b
+  return cmk(fma(a.x, b.x, fma(a.y, b.y, s.x)), fma(a.x, b.y, fma(-a.y, b.x, s.y)));
+}
 FFCA_DEV double2 cdiv(double2 a, double2 b) {
   // Smith's algorithm
   if (fabs(b.x) >= fabs(b.y)) {
@@ -578,7 +594,7 @@ FFCA_DEV bool cholesky(const double2 (&A)[I][I], double2 (&L)[I][I]) {
     for (int i = j + 1; i < I; ++i) {
       double2 s = A[i][j];
 #pragma unroll
-      for (int k = 0; k < j; ++k) s = csub(s, cmulc(L[i][k], L[j][k]));
+      for (int k = 0; k < j; ++k) s = cmsubc(s, L[i][k], L[j][k]);
       L[i][j] = cscale(s, il);
     }
 #pragma unroll
@@ -605,7 +621,7 @@ FFCA_DEV bool cholesky_fast(const double2 (&A)[I][I], double2 (&L)[I][I], double
     for (int i = j + 1; i < I; ++i) {
       double2 s = A[i][j];
 #pragma unroll
-      for (int k = 0; k < j; ++k) s = csub(s, cmulc(L[i][k], L[j][k]));
+      for (int k = 0; k < j; ++k) s = cmsubc(s, L[i][k], L[j][k]);
       L[i][j] = cscale(s, il);
     }
 #pragma unroll
@@ -626,7 +642,7 @@ FFCA_DEV void tril_inverse_d(const double2 (&L)[I][I], const double (&ild)[I], d
       }
       double2 s = cmk(r == c ? 1.0 : 0.0, 0.0);
 #pragma unroll
-      for (int k = c; k < r; ++k) s = csub(s, cmul(L[r][k], Li[k][c]));
+      for (int k = c; k < r; ++k) s = cmsub(s, L[r][k], Li[k][c]);
       Li[r][c] = cscale(s, ild[r]);
     }
   }
@@ -645,7 +661,7 @@ FFCA_DEV void tril_inverse(const double2 (&L)[I][I], double2 (&Li)[I][I]) {
       }
       double2 s = cmk(r == c ? 1.0 : 0.0, 0.0);
 #pragma unroll
-      for (int k = c; k < r; ++k) s = csub(s, cmul(L[r][k], Li[k][c]));
+      for (int k = c; k < r; ++k) s = cmsub(s, L[r][k], Li[k][c]);
       Li[r][c] = cscale(s, 1.0 / L[r][r].x);
     }
   }

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
       for (int b = a; b < I; ++b) {
         double2 s = cmk(0.0, 0.0);
 #pragma unroll
-        for (int k = b; k < I; ++k) s = cadd(s, cconjmul(Li[k][a], Li[k][b]));
+        for (int k = b; k < I; ++k) s = cmac_cj(s, Li[k][a], Li[k][b]);
         if (a == b) {
           Ri[a] = s.x;
         } else {
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
         if (b == a) continue;
         const double2 r = a < b ? cmk(Ri[Herm<I>::re(a, b)], Ri[Herm<I>::im(a, b)])
                                 : cmk(Ri[Herm<I>::re(b, a)], -Ri[Herm<I>::im(b, a)]);
-        s = cadd(s, cmul(r, yv[b]));
+        s = cmac(s, r, yv[b]);
       }
       x[a] = s;
     }
@@ -167,8 +167,8 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
         double2 s1 = cmk(0.0, 0.0), s2 = cmk(0.0, 0.0);
 #pragma unroll
         for (int b = 0; b < I; ++b) {
-          s1 = cadd(s1, cmul(Sget(0, a, b), x[b]));
-          s2 = cadd(s2, cmul(Sget(1, a, b), x[b]));
+          s1 = cmac(s1, Sget(0, a, b), x[b]);
+          s2 = cmac(s2, Sget(1, a, b), x[b]);
         }
         d1[a] = from_c128<R>(cscale(s1, v1));
         d2[a] = from_c128<R>(cscale(s2, v2));

@@ -181,8 +181,8 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32, FCA_PAR_MINB) fca
           const double2 fct = cscale(rrow[q], rcp_fast(d));
 #pragma unroll
           for (int c = 0; c < I; ++c) {
-            if (c > q) rrow[c] = csub(rrow[c], cmul(fct, prow[c]));
-            if (c <= q) irow[c] = csub(irow[c], cmul(fct, pinv[c]));
+            if (c > q) rrow[c] = cmsub(rrow[c], fct, prow[c]);
+            if (c <= q) irow[c] = cmsub(irow[c], fct, pinv[c]);
           }
         }
       }
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32, FCA_PAR_MINB) fca
       for (int c = 0; c < I; ++c) {
         irow[c] = cscale(irow[c], idr);
         at(r, c) = irow[c];
-        xr = cadd(xr, cmul(irow[c], vy[c]));
+        xr = cmac(xr, irow[c], vy[c]);
       }
       vx[r] = xr;
       lquad = ycur.x * xr.x + ycur.y * xr.y;  // Re conj(y_r) x_r
