@@ -204,8 +204,7 @@ FFCA_DEV void matmul(const double2 (&A)[I][I], const double2 (&B)[I][I], double2
       double2 acc = cmk(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < I; ++k) {
-        acc.x += A[a][k].x * B[k][b].x - A[a][k].y * B[k][b].y;
-        acc.y += A[a][k].x * B[k][b].y + A[a][k].y * B[k][b].x;
+        acc = cmac(acc, A[a][k], B[k][b]);
       }
       C[a][b] = acc;
     }
@@ -221,8 +220,7 @@ FFCA_DEV void matmul_hn(const double2 (&A)[I][I], const double2 (&B)[I][I], doub
       double2 acc = cmk(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < I; ++k) {
-        acc.x += A[k][a].x * B[k][b].x + A[k][a].y * B[k][b].y;
-        acc.y += A[k][a].x * B[k][b].y - A[k][a].y * B[k][b].x;
+        acc = cmac_cj(acc, A[k][a], B[k][b]);
       }
       C[a][b] = acc;
     }
@@ -238,8 +236,7 @@ FFCA_DEV void matmul_nh(const double2 (&A)[I][I], const double2 (&B)[I][I], doub
       double2 acc = cmk(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < I; ++k) {
-        acc.x += A[a][k].x * B[b][k].x + A[a][k].y * B[b][k].y;
-        acc.y += A[a][k].y * B[b][k].x - A[a][k].x * B[b][k].y;
+        acc = cmac(acc, A[a][k], cconj(B[b][k]));
       }
       C[a][b] = acc;
     }
@@ -476,7 +473,7 @@ FFCA_DEV int gevd_hpd(const double2 (&Phi)[I][I], const double2 (&Psi)[I][I], do
     for (int b = 0; b < I; ++b) {
       double2 acc = cmk(0.0, 0.0);
 #pragma unroll
-      for (int k = 0; k <= a; ++k) acc = cadd(acc, cmul(Li[a][k], Phi[k][b]));
+      for (int k = 0; k <= a; ++k) acc = cmac(acc, Li[a][k], Phi[k][b]);
       T[a][b] = acc;
     }
 #pragma unroll
@@ -485,7 +482,7 @@ FFCA_DEV int gevd_hpd(const double2 (&Phi)[I][I], const double2 (&Psi)[I][I], do
     for (int b = a; b < I; ++b) {
       double2 acc = cmk(0.0, 0.0);
 #pragma unroll
-      for (int k = 0; k <= b; ++k) acc = cadd(acc, cmulc(T[a][k], Li[b][k]));
+      for (int k = 0; k <= b; ++k) acc = cmac(acc, T[a][k], cconj(Li[b][k]));
       Wh[a][b] = acc;
     }
 #pragma unroll
@@ -567,8 +564,8 @@ FFCA_DEV bool lu_inverse(const double2 (&A)[I][I], double2 (&Inv)[I][I], double*
       const double2 fct = M[i][k];
 #pragma unroll
       for (int j = 0; j < I; ++j) {
-        M[i][j] = csub(M[i][j], cmul(fct, M[k][j]));
-        Inv[i][j] = csub(Inv[i][j], cmul(fct, Inv[k][j]));
+        M[i][j] = cmsub(M[i][j], fct, M[k][j]);
+        Inv[i][j] = cmsub(Inv[i][j], fct, Inv[k][j]);
       }
     }
   }

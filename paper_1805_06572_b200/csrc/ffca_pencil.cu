@@ -432,7 +432,7 @@ __global__ void cholinv_kernel(const double2* S, double2* Sinv, int64_t B, ffca_
 #pragma unroll
       for (int k = 0; k < I; ++k) {
         if (k < a || k < b) continue;
-        acc = cadd(acc, cconjmul(Li[k][a], Li[k][b]));
+        acc = cmac_cj(acc, Li[k][a], Li[k][b]);
       }
       Sinv[g * NP + a * I + b] = acc;
     }
@@ -540,7 +540,7 @@ __global__ void apply_w_kernel(const double2* mu_t, const double2* W, double2* o
   for (int a = 0; a < I; ++a) {
     double2 s = cmk(0.0, 0.0);
 #pragma unroll
-    for (int b = 0; b < I; ++b) s = cadd(s, cmul(W[f * NP + a * I + b], x[b]));
+    for (int b = 0; b < I; ++b) s = cmac(s, W[f * NP + a * I + b], x[b]);
     out[t * I + a] = s;
   }
 }

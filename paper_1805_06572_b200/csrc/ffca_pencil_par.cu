@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(ParLayout<I>::WARPS * 32) pencil_par_kernel(co
     for (int b = 0; b < I; ++b) {
       double2 h = cmk(0.0, 0.0);  // H[b][r] = sum_k conj(W[k][b]) W[k][r]
 #pragma unroll
-      for (int k = 0; k < I; ++k) h = cadd(h, cconjmul(v.at(kX, k, b), v.at(kX, k, r)));
+      for (int k = 0; k < I; ++k) h = cmac_cj(h, v.at(kX, k, b), v.at(kX, k, r));
       const double2 s1 = v.at(kS1, r, b), s2 = v.at(kS2, r, b);
       t1 += s1.x * h.x - s1.y * h.y;
       t2 += s2.x * h.x - s2.y * h.y;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(ParLayout<I>::WARPS * 32) pencil_par_kernel(co
       if (c < r) continue;
       double2 gr = cmk(0.0, 0.0);  // gram[r][c] = sum_k conj(P[k][r]) P[k][c]
 #pragma unroll
-      for (int k = 0; k < I; ++k) gr = cadd(gr, cconjmul(v.at(kP, k, r), v.at(kP, k, c)));
+      for (int k = 0; k < I; ++k) gr = cmac_cj(gr, v.at(kP, k, r), v.at(kP, k, c));
       double2 a1 = cadd(v.at(kS1, r, c), cscale(gr, eps1));
       double2 a2 = cadd(v.at(kS2, r, c), cscale(gr, eps2));
       if (c == r) {
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(ParLayout<I>::WARPS * 32) pencil_par_kernel(co
         for (int c = 0; c < I; ++c) {
           double2 acc = cmk(0.0, 0.0);
 #pragma unroll
-          for (int k = 0; k < I; ++k) acc = cadd(acc, cmul(v.at(kX, r, k), v.at(kT, k, c)));
+          for (int k = 0; k < I; ++k) acc = cmac(acc, v.at(kX, r, k), v.at(kT, k, c));
           if (dst) dst[r * I + c] = acc;
           if (hst) hst[r * I + c] = acc;
         }
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(ParLayout<I>::WARPS * 32) pencil_par_kernel(co
     for (int c = 0; c < I; ++c) {
       double2 acc = cmk(0.0, 0.0);
 #pragma unroll
-      for (int k = 0; k < I; ++k) acc = cadd(acc, cmul(v.at(kP, r, k), v.at(kA, k, c)));
+      for (int k = 0; k < I; ++k) acc = cmac(acc, v.at(kP, r, k), v.at(kA, k, c));
       v.at(kT, r, c) = acc;
       if (wr) p.P[g * NP + r * I + c] = acc;
     }

@@ -126,7 +126,7 @@ FFCA_DEV void row_matmul(const BinView<I>& v, int A, int B, int Cm, int r) {
   for (int c = 0; c < I; ++c) {
     double2 acc = cmk(0.0, 0.0);
 #pragma unroll
-    for (int k = 0; k < I; ++k) acc = cadd(acc, cmul(v.at(A, r, k), v.at(B, k, c)));
+    for (int k = 0; k < I; ++k) acc = cmac(acc, v.at(A, r, k), v.at(B, k, c));
     out[c] = acc;
   }
 #pragma unroll
@@ -278,7 +278,7 @@ FFCA_DEV int par_gevd(const BinView<I>& v, int r, bool own, double* min_sigma) {
     chol_ok = chol_ok && (misc[0] > 0.0);
     if (own && r > j) {
       double2 sacc = v.at(kS2, r, j);
-      for (int k = 0; k < j; ++k) sacc = csub(sacc, cmulc(v.at(kX, r, k), v.at(kX, j, k)));
+      for (int k = 0; k < j; ++k) sacc = cmsubc(sacc, v.at(kX, r, k), v.at(kX, j, k));
       v.at(kX, r, j) = cscale(sacc, misc[1]);
     }
     if (own && r < j) v.at(kX, r, j) = cmk(0.0, 0.0);
@@ -295,7 +295,7 @@ FFCA_DEV int par_gevd(const BinView<I>& v, int r, bool own, double* min_sigma) {
         continue;
       }
       double2 sacc = cmk(rr == c ? 1.0 : 0.0, 0.0);
-      for (int k = c; k < rr; ++k) sacc = csub(sacc, cmul(v.at(kX, rr, k), v.at(kT, k, c)));
+      for (int k = c; k < rr; ++k) sacc = cmsub(sacc, v.at(kX, rr, k), v.at(kT, k, c));
       const double2 val = cscale(sacc, rcp_fast(v.at(kX, rr, rr).x));
       v.at(kT, rr, c) = val;
       fro += cabs2(val);
@@ -310,7 +310,7 @@ FFCA_DEV int par_gevd(const BinView<I>& v, int r, bool own, double* min_sigma) {
     // ---- path A: Wh = Li Phi Li^H -> kS2; B = Li^H -> kX ----
     for (int c = 0; c < I; ++c) {  // kA row r = Li row r * Phi
       double2 acc = cmk(0.0, 0.0);
-      for (int k = 0; k <= r; ++k) acc = cadd(acc, cmul(v.at(kT, r, k), v.at(kS1, k, c)));
+      for (int k = 0; k <= r; ++k) acc = cmac(acc, v.at(kT, r, k), v.at(kS1, k, c));
       v.at(kA, r, c) = acc;
     }
   }
@@ -345,7 +345,7 @@ FFCA_DEV int par_gevd(const BinView<I>& v, int r, bool own, double* min_sigma) {
     if (go) {  // kT = Phi B
       for (int c = 0; c < I; ++c) {
         double2 acc = cmk(0.0, 0.0);
-        for (int k = 0; k < I; ++k) acc = cadd(acc, cmul(v.at(kS1, r, k), v.at(kX, k, c)));
+        for (int k = 0; k < I; ++k) acc = cmac(acc, v.at(kS1, r, k), v.at(kX, k, c));
         v.at(kT, r, c) = acc;
       }
     }
@@ -353,7 +353,7 @@ FFCA_DEV int par_gevd(const BinView<I>& v, int r, bool own, double* min_sigma) {
     if (go) {  // Wh = B^H (Phi B), re-symmetrised from the upper triangle
       for (int c = r; c < I; ++c) {
         double2 acc = cmk(0.0, 0.0);
-        for (int k = 0; k < I; ++k) acc = cadd(acc, cconjmul(v.at(kX, k, r), v.at(kT, k, c)));
+        for (int k = 0; k < I; ++k) acc = cmac_cj(acc, v.at(kX, k, r), v.at(kT, k, c));
         if (c == r) acc.y = 0.0;
         v.at(kS2, r, c) = acc;
       }
@@ -388,7 +388,7 @@ FFCA_DEV int par_gevd(const BinView<I>& v, int r, bool own, double* min_sigma) {
   if (act) {
     for (int c = 0; c < I; ++c) {
       double2 acc = cmk(0.0, 0.0);
-      for (int k = 0; k < I; ++k) acc = cadd(acc, cmul(v.at(kX, r, k), v.at(kV, k, c)));
+      for (int k = 0; k < I; ++k) acc = cmac(acc, v.at(kX, r, k), v.at(kV, k, c));
       v.at(kA, r, c) = acc;
     }
   }
