@@ -18,10 +18,10 @@
 namespace ffca {
 
 // orders up to which the pass uses rsqrt/rcp seeds + Newton instead of the
-// IEEE sqrt / division subroutines (measured: faster for I <= 3, slower at
-// I = 4 where the extra live registers add spills)
+// IEEE sqrt / division subroutines (with the fused complex MACs this is
+// faster at every order: config 3 FCA 15.8 -> 18.4 G at I = 4)
 #ifndef FFCA_FCA_FASTMATH_MAXI
-#define FFCA_FCA_FASTMATH_MAXI 3
+#define FFCA_FCA_FASTMATH_MAXI 4
 #endif
 #ifndef FFCA_FCA_STAGES
 #define FFCA_FCA_STAGES 4  // frame ring depth of the FCA pass
