@@ -26,7 +26,6 @@ struct FcaParLayout {
   static constexpr int WARPS = 2;
   static constexpr int BPB = WARPS * 32 / LB;  // bins (groups) per CTA
   static constexpr int LD = (I % 2) ? I + 2 : I + 1;
-  static constexpr int NP = I * I;
   static constexpr int NS = I / 2 + 1;          // entry slots per lane
   static constexpr int MATD = I * LD * 2;       // doubles per padded complex matrix
   // per group: S1, S2 unpacked (2 MATD) + 1 matrix (rows of Rinv) + 3 vectors
@@ -38,13 +37,6 @@ struct FcaParLayout {
   static constexpr size_t SMEM = (size_t)BPB * GROUP_DOUBLES * sizeof(double);
 };
 
-// entry (a, b) of a packed Hermitian matrix in shared memory, runtime indices
-template <int I>
-FFCA_DEV double2 packed_get(const double* S, int a, int b) {
-  if (a == b) return cmk(S[a], 0.0);
-  if (a < b) return cmk(S[Herm<I>::re(a, b)], S[Herm<I>::im(a, b)]);
-  return cmk(S[Herm<I>::re(b, a)], -S[Herm<I>::im(b, a)]);
-}
 
 }  // namespace
 
@@ -214,8 +206,8 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32, FCA_PAR_MINB) fca
       double2 s1 = cmk(0.0, 0.0), s2 = cmk(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < I; ++k) {
-        s1 = cadd(s1, cmul(S1(r, k), vx[k]));
-        s2 = cadd(s2, cmul(S2(r, k), vx[k]));
+        s1 = cmac(s1, S1(r, k), vx[k]);
+        s2 = cmac(s2, S2(r, k), vx[k]);
       }
       C* mo = (C*)p.mu_out;
       mo[(((m * 2 + 0) * p.N + n) * p.F + f) * I + r] = from_c128<R>(cscale(s1, v1));
@@ -449,7 +441,7 @@ __global__ void __launch_bounds__(64)
         for (int c = 0; c < I; ++c) {
           double2 t = cmk(0.0, 0.0);
 #pragma unroll
-          for (int k = 0; k < I; ++k) t = cadd(t, cmul(A(r, k), j == 0 ? S1(k, c) : S2(k, c)));
+          for (int k = 0; k < I; ++k) t = cmac(t, A(r, k), j == 0 ? S1(k, c) : S2(k, c));
           T(r, c) = t;
         }
       }
@@ -460,7 +452,7 @@ __global__ void __launch_bounds__(64)
         for (int c = 0; c < I; ++c) {
           double2 t = cmk(0.0, 0.0);
 #pragma unroll
-          for (int k = 0; k < I; ++k) t = cadd(t, cmul(j == 0 ? S1(r, k) : S2(r, k), T(k, c)));
+          for (int k = 0; k < I; ++k) t = cmac(t, j == 0 ? S1(r, k) : S2(r, k), T(k, c));
           mrow[c] = t;
         }
       }
@@ -473,7 +465,7 @@ __global__ void __launch_bounds__(64)
         for (int c = 0; c < I; ++c) {
           double2 t = cmk(0.0, 0.0);
 #pragma unroll
-          for (int k = 0; k < I; ++k) t = cadd(t, cmul(A(r, k), S2(k, c)));
+          for (int k = 0; k < I; ++k) t = cmac(t, A(r, k), S2(k, c));
           T(r, c) = t;
         }
       }
@@ -483,7 +475,7 @@ __global__ void __launch_bounds__(64)
         for (int c = 0; c < I; ++c) {
           double2 t = mrow[c];
 #pragma unroll
-          for (int k = 0; k < I; ++k) t = cadd(t, cmul(S1(r, k), T(k, c)));
+          for (int k = 0; k < I; ++k) t = cmac(t, S1(r, k), T(k, c));
           A(r, c) = t;  // M row r (A is free: every lane has read X_j)
         }
       }
@@ -567,7 +559,7 @@ __global__ void __launch_bounds__(64)
       if (own && r > q) {
         double2 t = A(r, q);
 #pragma unroll
-        for (int k = 0; k < q; ++k) t = csub(t, cmulc(A(r, k), A(q, k)));
+        for (int k = 0; k < q; ++k) t = cmsubc(t, A(r, k), A(q, k));
         A(r, q) = cscale(t, 1.0 / A(q, q).x);
       }
       __syncwarp();
