@@ -503,7 +503,7 @@ FFCA_DEV int gevd_hpd(const double2 (&Phi)[I][I], const double2 (&Psi)[I][I], do
     for (int b = 0; b < I; ++b) {
       double2 acc = cmk(0.0, 0.0);
 #pragma unroll
-      for (int k = a; k < I; ++k) acc = cadd(acc, cconjmul(Li[k][a], Q[k][b]));
+      for (int k = a; k < I; ++k) acc = cmac_cj(acc, Li[k][a], Q[k][b]);
       P[a][b] = acc;
     }
   fix_column_phases<I>(P);
