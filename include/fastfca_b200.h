@@ -116,6 +116,11 @@ int ffca_device_arch(void); /* compiled SM arch, e.g. 100 */
  * (algorithm 0 = FastFCA, 1 = FCA; needs a device for the occupancy query). */
 int ffca_plan_chunks(int64_t G, int64_t N, int I, int dtype, int algorithm,
                      int64_t* chunk_frames, int* nchunk);
+/* Grid of the streaming pass for that plan (chunk_frames 0 = the auto plan):
+ * *ctas = bin tiles x frame chunks, *slots = resident CTAs on the whole device
+ * (SM count x CTAs per SM); ctas / slots = waves. Needs a device. */
+int ffca_plan_grid(int64_t G, int64_t N, int I, int dtype, int algorithm, int64_t chunk_frames,
+                   int64_t* ctas, int64_t* slots);
 size_t ffca_fastfca_workspace_size(int64_t M, int64_t N, int64_t F, int I, int iterations,
                                    unsigned flags, int64_t chunk_frames);
 int ffca_fastfca_run(const ffca_run_args* args, void* stream);
@@ -131,6 +136,9 @@ int ffca_run_status(const void* workspace, void* stream, ffca_status* out);
 int ffca_status_reset(ffca_status_dev* st, void* stream);
 /* Synchronises `stream`, copies and decodes. */
 int ffca_status_read(const ffca_status_dev* st, void* stream, ffca_status* out);
+/* Decode a status word that is already in HOST memory (e.g. copied
+ * asynchronously out of a run workspace before the workspace is reused). */
+int ffca_status_decode(const ffca_status_dev* host_word, ffca_status* out);
 
 /* ---- kernel-module contract (_kernels_numpy.py:19-193; M = 1) ---------- */
 /* fast_transform: yt = P^H y  (_kernels_numba.py:147-162) */
@@ -178,6 +186,12 @@ int ffca_propagate_pencil(const double* St1, const double* St2, const double* P_
 /* S^{-1} = L^{-H} L^{-1} (conventional.py:98-101) */
 int ffca_cholesky_inverse(const double* S, double* Sinv, int64_t batch, int D,
                           ffca_status_dev* st, void* stream);
+/* solve_hermitian_system (pencil.py:138-157): X = A^{-1} B per batch entry by LU with
+ * partial pivoting (np.linalg.solve / zgesv); A (batch,D,D), B and X (batch,D,K) complex128;
+ * norms (batch,2) float64 out: ||A X - B||^2 and ||B||^2 of each entry. An exactly
+ * singular A reports FFCA_ERR_SINGULAR_MATRIX (index = batch entry). */
+int ffca_solve(const double* A, const double* B, double* X, double* norms, int64_t batch,
+               int D, int64_t K, ffca_status_dev* st, void* stream);
 /* hermitize + 1e-9 tr/D ridge (modelops.py:29-39) */
 int ffca_regularize_covariances(const double* S, double* out, int64_t batch, int D,
                                 void* stream);

@@ -23,6 +23,7 @@ from .fast import (fast_e_step, fast_m_step_S, fast_m_step_v, fastfca_run, propa
 from .initializers import init_from_masks, init_from_masks_batch, init_random, init_random_batch
 from .pencil import PencilDecomposition, gevd_hpd, hermitian_eig, solve_hermitian_system
 from .pipeline import separate, separate_device
+from .sharding import fastfca_run_sharded, fca_run_sharded
 from .stft import (sqrt_hann, stft_analyze, stft_analyze_device, stft_synthesize,
                    stft_synthesize_device)
 from .types import (AudioBuffer, OpCounts, PosteriorMoments, SeparationResult, SpatialModel,
@@ -54,6 +55,8 @@ __all__ = [
     "fca_run",
     "gevd_hpd",
     "hermitian_eig",
+    "fastfca_run_sharded",
+    "fca_run_sharded",
     "init_from_masks",
     "init_from_masks_batch",
     "init_random",

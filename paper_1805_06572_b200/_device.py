@@ -53,6 +53,10 @@ def to_device(x, dtype, non_blocking=True):
         t = t.to(dtype)
     if not t.is_cuda:
         t = t.to(device(), non_blocking=non_blocking and t.is_pinned())
+    elif t.device != device():
+        # the kernels run on the current device and stream: a tensor on another
+        # GPU would be dereferenced there (illegal address) -> move it
+        t = t.to(device())
     return t.contiguous()
 
 
@@ -102,6 +106,16 @@ def raise_for_status(st, N=None, F=None):
     if code == _lib.FFCA_ERR_NOT_PD:
         raise np.linalg.LinAlgError("Matrix is not positive definite")
     raise RuntimeError(f"fastfca_b200: unknown status code {code}")
+
+
+def decode_status(word):
+    """Decode a 16-byte status word already in host memory (uint8 array / tensor)."""
+    lib = _lib.load()
+    raw = np.ascontiguousarray(np.asarray(word, dtype=np.uint8).reshape(16))
+    st = _lib.Status()
+    check_rc(lib.ffca_status_decode(raw.ctypes.data_as(ctypes.c_void_p), ctypes.byref(st)),
+             "ffca_status_decode")
+    return st
 
 
 class StageStatus:

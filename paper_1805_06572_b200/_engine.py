@@ -266,6 +266,9 @@ def run_host_pipelined(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=
             S=torch.empty((cm, 2, F, I, I), dtype=torch.complex128, device=dev),
             free=torch.cuda.Event()))
     runs = []
+    # every chunk's status word, copied out of its slot's workspace on the
+    # compute stream right after the run (before the slot's next run resets it)
+    status_h = torch.empty((len(bounds), 16), dtype=torch.uint8, pin_memory=True)
     caller = torch.cuda.current_stream()
     s_h2d.wait_stream(caller)
     s_cmp.wait_stream(caller)
@@ -294,6 +297,7 @@ def run_host_pipelined(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=
                              timing=(k == 0), check=False, chunk_frames=chunk_frames,
                              out=o, graph=(k > 0))
             sl["ws"] = run.workspace
+            status_h[k].copy_(run.workspace[:16], non_blocking=True)
             ev_cmp = torch.cuda.Event()
             ev_cmp.record(s_cmp)
         with torch.cuda.stream(s_d2h):
@@ -307,11 +311,28 @@ def run_host_pipelined(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=
         runs.append((run, c))
     for s in (s_h2d, s_cmp, s_d2h):
         s.synchronize()
-    for run, _ in runs:
-        status_of(run, N, F)
+    _raise_first(status_h.numpy(), N, F)
+    _collect_timings(runs[0][0])
     return {"images": out_img.numpy(), "v": out_v.numpy(), "S": out_S.numpy(),
             "floor": fh.numpy(), "loglik": out_ll.numpy() if likelihood else None,
             "iteration_ms": runs[0][0].iteration_ms, "chunks": len(bounds)}
+
+
+def _raise_first(words, N, F):
+    """Raise for the earliest failure over a chunked batch, in the status key
+    order of one run over the whole batch: iteration, then code, then the flat
+    index, whose leading axis is the mixture (chunks cover increasing,
+    disjoint mixture ranges, so chunk order breaks ties before the index)."""
+    best = None
+    for k, word in enumerate(words):
+        st = D.decode_status(word)
+        if st.code == _lib.FFCA_OK:
+            continue
+        key = (st.iteration, st.code, k, int(st.index))
+        if best is None or key < best[0]:
+            best = (key, st)
+    if best is not None:
+        D.raise_for_status(best[1], N, F)
 
 
 class MultiStreamRun:

@@ -65,6 +65,8 @@ SIGNATURES = [
     ("ffca_device_arch", c_int, []),
     ("ffca_plan_chunks", c_int,
      [c_i64, c_i64, c_int, c_int, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_int)]),
+    ("ffca_plan_grid", c_int,
+     [c_i64, c_i64, c_int, c_int, c_int, c_i64, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     ("ffca_fastfca_workspace_size", c_sz,
      [c_i64, c_i64, c_i64, c_int, c_int, ctypes.c_uint, c_i64]),
     ("ffca_fastfca_run", c_int, [ctypes.POINTER(RunArgs), c_vp]),
@@ -74,6 +76,7 @@ SIGNATURES = [
     ("ffca_run_status", c_int, [c_vp, c_vp, ctypes.POINTER(Status)]),
     ("ffca_status_reset", c_int, [c_vp, c_vp]),
     ("ffca_status_read", c_int, [c_vp, c_vp, ctypes.POINTER(Status)]),
+    ("ffca_status_decode", c_int, [c_vp, ctypes.POINTER(Status)]),
     ("ffca_fast_transform", c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_int, c_vp]),
     ("ffca_fast_e_step", c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_int, c_vp]),
     ("ffca_fast_v_update", c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_int, c_vp]),
@@ -91,6 +94,7 @@ SIGNATURES = [
     ("ffca_gevd_hpd", c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp, c_vp]),
     ("ffca_propagate_pencil", c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_vp, c_vp]),
     ("ffca_cholesky_inverse", c_int, [c_vp, c_vp, c_i64, c_int, c_vp, c_vp]),
+    ("ffca_solve", c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_i64, c_vp, c_vp]),
     ("ffca_regularize_covariances", c_int, [c_vp, c_vp, c_i64, c_int, c_vp]),
     ("ffca_regularize_transformed", c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
     ("ffca_back_transform_images", c_int,

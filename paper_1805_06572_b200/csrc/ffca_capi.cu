@@ -22,6 +22,8 @@ cudaError_t launch_gevd_batch(const double2* Phi, const double2* Psi, double* la
 cudaError_t launch_cholinv(const double2* S, double2* Sinv, int64_t B, int I, ffca_status_dev* st,
                            cudaStream_t s);
 cudaError_t launch_regularize(const double2* S, double2* out, int64_t B, int I, cudaStream_t s);
+cudaError_t launch_solve(const double2* A, const double2* B, double2* X, double* norms,
+                         int64_t batch, int I, int64_t K, ffca_status_dev* st, cudaStream_t s);
 cudaError_t launch_reg_transformed(const double2* S, const double2* gram, double2* out,
                                    int64_t B, int I, cudaStream_t s);
 cudaError_t launch_inverse_h(const double2* P, double2* W, double* logdet2, int64_t B, int I,
@@ -32,6 +34,10 @@ cudaError_t launch_conj_w(const double2* S, const double2* W, double2* out, int6
                           int64_t F, int I, cudaStream_t s);
 cudaError_t launch_init_powers(const void* y, void* v, double* floor, int64_t M, int64_t N,
                                int64_t F, int I, int dtype, cudaStream_t s);
+int fast_par_blocks_per_sm(int I, int dtype);
+int fast_par_bins_per_cta();
+int fca_par_blocks_per_sm(int I, int dtype);
+int fca_par_bins_per_cta(int I);
 }  // namespace ffca
 
 using namespace ffca;
@@ -257,6 +263,32 @@ int ffca_plan_chunks(int64_t G, int64_t N, int I, int dtype, int algorithm,
   return FFCA_OK;
 }
 
+int ffca_plan_grid(int64_t G, int64_t N, int I, int dtype, int algorithm, int64_t chunk_frames,
+                   int64_t* ctas, int64_t* slots) {
+  if (G < 1 || N < 1 || I < 1 || I > kMaxOrder || !ctas || !slots) return FFCA_ERR_INVALID;
+  int64_t cf = chunk_frames;
+  int nc = 0;
+  if (cf <= 0) {
+    if (algorithm)
+      plan_fca_chunks(G, N, I, dtype, &cf, &nc);
+    else
+      plan_fast_chunks(G, N, I, dtype, &cf, &nc);
+  }
+  if (cf > N) cf = N;
+  nc = (int)((N + cf - 1) / cf);
+  int bpsm, tile;
+  if (algorithm) {
+    bpsm = I >= 5 ? fca_par_blocks_per_sm(I, dtype) : fca_blocks_per_sm(I, dtype);
+    tile = I >= 5 ? fca_par_bins_per_cta(I) : 32;
+  } else {
+    bpsm = I >= 5 ? fast_par_blocks_per_sm(I, dtype) : fast_blocks_per_sm(I, dtype);
+    tile = I >= 5 ? fast_par_bins_per_cta() : 32;
+  }
+  *ctas = (G + tile - 1) / tile * nc;
+  *slots = (int64_t)sm_count() * bpsm;
+  return FFCA_OK;
+}
+
 size_t ffca_fastfca_workspace_size(int64_t M, int64_t N, int64_t F, int I, int iterations,
                                    unsigned flags, int64_t chunk_frames) {
   if (M < 1 || N < 1 || F < 1 || I < 1 || I > kMaxOrder || iterations < 0) return 0;
@@ -452,10 +484,15 @@ static int fca_enqueue(const ffca_run_args* a, cudaStream_t s) {
         FFCA_TRY(cudaMemcpyAsync((char*)a->v_hist + (size_t)l * vslice * real_size(a->dtype),
                                  a->v, vslice * real_size(a->dtype), cudaMemcpyDeviceToDevice,
                                  s));
+      // the finish's only check is the Cholesky of the new S, which the
+      // reference does at the start of the NEXT iteration (conventional.py:131,
+      // 98-101): after the last iteration nothing inverts S, so a
+      // final non-PD model returns normally there -> no status word
       FFCA_TRY(launch_fca_finish(
           w.Spart, w.nchunk, N, G, F, w.Sp, (double2*)a->S_out,
           (hist && a->S_hist) ? (double2*)a->S_hist + (size_t)l * Sslice : nullptr,
-          ll ? w.llbin : nullptr, ll ? w.llg + (size_t)l * G : nullptr, I, w.st, l + 1, s));
+          ll ? w.llbin : nullptr, ll ? w.llg + (size_t)l * G : nullptr, I,
+          (l == L - 1) ? nullptr : w.st, l + 1, s));
     }
     if (ev) FFCA_TRY(cudaEventRecord(ev[L], s));
     if (ll) {
@@ -473,6 +510,12 @@ static int fca_enqueue(const ffca_run_args* a, cudaStream_t s) {
 int ffca_run_status(const void* workspace, void* stream, ffca_status* out) {
   if (!workspace || !out) return FFCA_ERR_INVALID;
   return ffca_status_read((const ffca_status_dev*)workspace, stream, out);
+}
+
+int ffca_status_decode(const ffca_status_dev* host_word, ffca_status* out) {
+  if (!host_word || !out) return FFCA_ERR_INVALID;
+  decode(*host_word, out);
+  return FFCA_OK;
 }
 
 int ffca_status_reset(ffca_status_dev* st, void* stream) {
@@ -515,6 +558,15 @@ int ffca_cholesky_inverse(const double* S, double* Sinv, int64_t batch, int D,
   if (batch == 0) return FFCA_OK;
   return cu(launch_cholinv((const double2*)S, (double2*)Sinv, batch, D, st,
                            (cudaStream_t)stream));
+}
+
+int ffca_solve(const double* A, const double* B, double* X, double* norms, int64_t batch,
+               int D, int64_t K, ffca_status_dev* st, void* stream) {
+  if (!A || !B || !X || !norms || batch < 0 || D < 1 || D > kMaxOrder || K < 0)
+    return FFCA_ERR_INVALID;
+  if (batch == 0) return FFCA_OK;
+  return cu(launch_solve((const double2*)A, (const double2*)B, (double2*)X, norms, batch, D, K, st,
+                         (cudaStream_t)stream));
 }
 
 int ffca_regularize_covariances(const double* S, double* out, int64_t batch, int D,

@@ -829,13 +829,8 @@ cudaError_t launch_fast2_variant(const FastIterParams& p, cudaStream_t s) {
   constexpr int STAGES = fast2_stages<I, R, UPDATE, LL, MU>();
   using Sm = Fast2Smem<I, R, WARPS, STAGES, MU, SmemAcc<I, R, UPDATE, LL, MU>::value>;
   auto kern = fast_em2_kernel<I, R, WARPS, STAGES, UPDATE, LL, MU>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)Sm::BYTES);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = ensure_smem<fast_em2_kernel<I, R, WARPS, STAGES, UPDATE, LL, MU>>(Sm::BYTES))
+    return e;
   dim3 grid((unsigned)((p.G + 31) / 32), (unsigned)p.nchunk);
   kern<<<grid, WARPS * 32, Sm::BYTES, s>>>(p);
   return cudaGetLastError();

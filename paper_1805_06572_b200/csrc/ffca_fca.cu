@@ -282,13 +282,7 @@ static cudaError_t launch_fca_em_t(const FcaIterParams& p, cudaStream_t s) {
   constexpr int NP = I * I;
   const size_t smem = fca_smem_bytes<I, R>();
   auto kern = fca_em_kernel<I, R, kWarps>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = ensure_smem<fca_em_kernel<I, R, kWarps>>(smem)) return e;
   dim3 grid((unsigned)((p.G + 31) / 32), (unsigned)p.nchunk);
   kern<<<grid, kWarps * 32, smem, s>>>(p);
   return cudaGetLastError();

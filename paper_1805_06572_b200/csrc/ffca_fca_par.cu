@@ -610,13 +610,7 @@ template <int I, typename R>
 cudaError_t launch_fca_par_t(const FcaIterParams& p, cudaStream_t s) {
   using Lay = FcaParLayout<I>;
   auto kern = fca_par_kernel<I, R>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = ensure_smem<fca_par_kernel<I, R>>(Lay::SMEM)) return e;
   dim3 grid((unsigned)((p.G + Lay::BPB - 1) / Lay::BPB), (unsigned)p.nchunk);
   kern<<<grid, Lay::WARPS * 32, Lay::SMEM, s>>>(p);
   return cudaGetLastError();

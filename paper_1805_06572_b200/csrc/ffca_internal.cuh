@@ -4,9 +4,28 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "ffca_common.cuh"
 
 namespace ffca {
+
+// Opt a kernel into > 48 KB of dynamic shared memory on the CURRENT device.
+// The attribute is per (function, device context), so the "done" record is a
+// per-device bit (atomic: several host threads may launch concurrently); a
+// process that drives a second GPU sets it again there.
+template <auto Kern>
+inline cudaError_t ensure_smem(size_t bytes) {
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 constexpr int kWarps = 4;  // warps per CTA in the frame-streaming kernels
 // FCA per-(chunk, bin) partial sums: packed Hermitian B1, B2, X1, X2 with

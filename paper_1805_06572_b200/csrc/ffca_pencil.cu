@@ -438,6 +438,101 @@ __global__ void cholinv_kernel(const double2* S, double2* Sinv, int64_t B, ffca_
     }
 }
 
+// X = A^{-1} B per batch entry (reference pencil.py:138-157, which calls
+// np.linalg.solve = LAPACK zgesv): LU with partial pivoting on |re| + |im|
+// (zgetrf's izamax), one thread per system, then for each of the K right-hand
+// sides the permuted forward / back substitution. Also writes ||A X - B||^2
+// and ||B||^2 of the entry (norms[2g], norms[2g+1]) for the caller's residual
+// test. An exactly zero pivot is zgetrf's "singular" -> FFCA_ERR_SINGULAR_MATRIX.
+template <int I>
+__global__ void solve_kernel(const double2* __restrict__ A, const double2* __restrict__ B,
+                             double2* __restrict__ X, double* __restrict__ norms, int64_t batch,
+                             int64_t K, ffca_status_dev* st) {
+  constexpr int NP = I * I;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= batch) return;
+  double2 LU[I][I];
+  int piv[I];
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) LU[a][b] = A[g * NP + a * I + b];
+  bool singular = false;
+#pragma unroll
+  for (int k = 0; k < I; ++k) {
+    int p = k;
+    double best = fabs(LU[k][k].x) + fabs(LU[k][k].y);
+#pragma unroll
+    for (int r = k + 1; r < I; ++r) {
+      const double c = fabs(LU[r][k].x) + fabs(LU[r][k].y);
+      if (c > best) best = c, p = r;
+    }
+    piv[k] = p;
+#pragma unroll
+    for (int r = k + 1; r < I; ++r)  // swap rows k and p (compile-time indices)
+      if (r == p) {
+#pragma unroll
+        for (int c = 0; c < I; ++c) {
+          const double2 t = LU[k][c];
+          LU[k][c] = LU[r][c];
+          LU[r][c] = t;
+        }
+      }
+    if (best == 0.0) {
+      singular = true;
+      continue;
+    }
+    const double2 inv = cdiv(cmk(1.0, 0.0), LU[k][k]);
+#pragma unroll
+    for (int r = k + 1; r < I; ++r) {
+      const double2 l = cmul(LU[r][k], inv);
+      LU[r][k] = l;
+#pragma unroll
+      for (int c = k + 1; c < I; ++c) LU[r][c] = cmsub(LU[r][c], l, LU[k][c]);
+    }
+  }
+  if (singular) {
+    if (st) report_error(st, 0, FFCA_ERR_SINGULAR_MATRIX, (unsigned long long)g);
+    return;
+  }
+  double res2 = 0.0, nb2 = 0.0;
+  for (int64_t j = 0; j < K; ++j) {
+    double2 b0[I], x[I];
+#pragma unroll
+    for (int a = 0; a < I; ++a) b0[a] = x[a] = B[(g * I + a) * K + j];
+#pragma unroll
+    for (int k = 0; k < I; ++k)
+#pragma unroll
+      for (int r = k + 1; r < I; ++r)
+        if (r == piv[k]) {
+          const double2 t = x[k];
+          x[k] = x[r];
+          x[r] = t;
+        }
+#pragma unroll
+    for (int r = 1; r < I; ++r)
+#pragma unroll
+      for (int c = 0; c < r; ++c) x[r] = cmsub(x[r], LU[r][c], x[c]);
+#pragma unroll
+    for (int r = I - 1; r >= 0; --r) {
+#pragma unroll
+      for (int c = r + 1; c < I; ++c) x[r] = cmsub(x[r], LU[r][c], x[c]);
+      x[r] = cdiv(x[r], LU[r][r]);
+    }
+#pragma unroll
+    for (int a = 0; a < I; ++a) {
+      X[(g * I + a) * K + j] = x[a];
+      double2 t = cmk(-b0[a].x, -b0[a].y);
+#pragma unroll
+      for (int c = 0; c < I; ++c) t = cmac(t, A[g * NP + a * I + c], x[c]);
+      res2 += cabs2(t);
+      nb2 += cabs2(b0[a]);
+    }
+  }
+  norms[2 * g] = res2;
+  norms[2 * g + 1] = nb2;
+}
+
 template <int I>
 __global__ void regularize_kernel(const double2* S, double2* out, int64_t B) {
   constexpr int NP = I * I;
@@ -579,6 +674,12 @@ cudaError_t launch_gevd_batch(const double2* Phi, const double2* Psi, double* la
 cudaError_t launch_cholinv(const double2* S, double2* Sinv, int64_t B, int I, ffca_status_dev* st,
                            cudaStream_t s) {
   FFCA_DISPATCH_I(I, (cholinv_kernel<II><<<nblk(B, 64), 64, 0, s>>>(S, Sinv, B, st)));
+  return cudaGetLastError();
+}
+cudaError_t launch_solve(const double2* A, const double2* B, double2* X, double* norms,
+                         int64_t batch, int I, int64_t K, ffca_status_dev* st, cudaStream_t s) {
+  FFCA_DISPATCH_I(I, (solve_kernel<II><<<nblk(batch, 64), 64, 0, s>>>(A, B, X, norms, batch, K,
+                                                                       st)));
   return cudaGetLastError();
 }
 cudaError_t launch_regularize(const double2* S, double2* out, int64_t B, int I, cudaStream_t s) {

@@ -284,14 +284,7 @@ __global__ void __launch_bounds__(ParLayout<I>::WARPS * 32)
 template <int I>
 static cudaError_t launch_par_t(const PencilParams& p, cudaStream_t s) {
   using Lay = ParLayout<I>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(pencil_par_kernel<I>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)Lay::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = ensure_smem<pencil_par_kernel<I>>(Lay::SMEM)) return e;
   const unsigned nb = (unsigned)((p.G + Lay::BPB - 1) / Lay::BPB);
   pencil_par_kernel<I><<<nb, Lay::WARPS * 32, Lay::SMEM, s>>>(p);
   return cudaGetLastError();
@@ -302,14 +295,7 @@ static cudaError_t launch_init_par_t(const double2* S0, double2* P, double2* W, 
                                      double* logdet2, int64_t G, int64_t F, ffca_status_dev* st,
                                      cudaStream_t s) {
   using Lay = ParLayout<I>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(initial_par_kernel<I>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)Lay::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = ensure_smem<initial_par_kernel<I>>(Lay::SMEM)) return e;
   const unsigned nb = (unsigned)((G + Lay::BPB - 1) / Lay::BPB);
   initial_par_kernel<I><<<nb, Lay::WARPS * 32, Lay::SMEM, s>>>(S0, P, W, lam, logdet2, G, F, st);
   return cudaGetLastError();

@@ -75,24 +75,51 @@ def hermitian_eig(A):
 
 
 def solve_hermitian_system(Psi, B, rtol=1e-10):
-    """Solve ``Psi X = B`` on the device and verify the residual
-    (reference pencil.py:138-157)."""
-    D.require()
+    """Solve ``Psi X = B`` per batch entry and verify the residual
+    (reference pencil.py:138-157) — LU with partial pivoting in the
+    ``ffca_solve`` kernel (the reference's np.linalg.solve / zgesv).
+
+    ``Psi`` (..., D, D) nonsingular square; ``B`` (D,) with a single ``Psi``
+    or (..., D, K). A singular system or a relative residual above ``rtol``
+    (Frobenius norms over the whole batch, as the reference) raises
+    :class:`SingularMatrixError`.
+    """
+    lib = D.require()
     torch = D.torch
     A = D.to_device(Psi, torch.complex128)
     b = D.to_device(B, torch.complex128)
+    if A.dim() < 2 or A.shape[-1] != A.shape[-2]:
+        raise SingularMatrixError(f"singular system: Psi must be square, got {tuple(A.shape)}")
+    d = int(A.shape[-1])
+    if d > 8:
+        raise SingularMatrixError(f"singular system: order {d} > 8 unsupported on the device path")
     vec = b.dim() == 1
     rhs = b[:, None] if vec else b
-    try:
-        X = torch.linalg.solve(A, rhs)
-    except RuntimeError as exc:
-        raise SingularMatrixError(f"singular system: {exc}") from exc
-    norm_b = float(torch.linalg.norm(rhs))
-    resid = float(torch.linalg.norm(A @ X - rhs))
-    if not bool(torch.isfinite(X).all()) or resid > rtol * max(norm_b, 1e-300):
+    if vec and A.dim() != 2:
+        raise SingularMatrixError("singular system: a vector right-hand side needs one Psi")
+    if tuple(rhs.shape[:-1]) != tuple(A.shape[:-1]):
+        raise SingularMatrixError(
+            f"singular system: shapes {tuple(A.shape)} and {tuple(b.shape)} do not match")
+    batch = int(np.prod(A.shape[:-2])) if A.dim() > 2 else 1
+    K = int(rhs.shape[-1])
+    Ad = A.reshape(batch, d, d).contiguous()
+    Bd = rhs.reshape(batch, d, K).contiguous()
+    X = D.empty((batch, d, K), torch.complex128)
+    norms = D.empty((batch, 2), torch.float64)
+    st = D.StageStatus()
+    D.check_rc(lib.ffca_solve(D.ptr(Ad), D.ptr(Bd), D.ptr(X), D.ptr(norms), batch, d, K,
+                              st.handle, D.stream_handle()), "ffca_solve")
+    if st.read().code:
+        raise SingularMatrixError("singular system: Singular matrix")
+    tot = norms.sum(dim=0).cpu().numpy()
+    norm_b = float(np.sqrt(tot[1]))
+    resid = float(np.sqrt(tot[0]))
+    if not bool(torch.isfinite(X).all()) or not np.isfinite(resid) or \
+            resid > rtol * max(norm_b, 1e-300):
         raise SingularMatrixError(
             f"system too ill-conditioned: relative residual {resid / max(norm_b, 1e-300):.3e}")
-    X = X[:, 0] if vec else X
+    X = X.reshape(rhs.shape)
+    X = X[..., 0] if vec else X
     return X if D.is_tensor(Psi) else D.host(X)
 
 

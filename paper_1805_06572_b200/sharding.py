@@ -2,13 +2,20 @@
 inside the EM loop.
 
 Every EM quantity is per frequency bin (and per mixture): nothing couples
-bins inside the loop (the reference is bitwise bin-shard
-invariant). Batches are therefore split by mixture (config 3) and single
-long mixtures by contiguous bin ranges (config 4). Each rank runs its shard
-with the chunking the unsharded problem would use, so per-bin results are
-bitwise identical to a 1-GPU run, and the only cross-GPU traffic is the final
-gather of the per-rank results (NCCL over NVLink for CUDA tensors, gloo for
-host tensors) in fixed rank order.
+bins inside the loop (the reference calls the work
+"embarrassingly parallel over f", /root/reference/SPEC.md:300, and its
+per-bin loop is fast.py:200-223). Batches are therefore split by mixture
+(config 3) and single long mixtures by contiguous bin ranges (config 4).
+
+Every world size 1..MAX_WORLD uses ONE frame chunking — the plan that fills a
+GPU with the shard of the largest world size (:func:`shard_chunk_frames`) —
+so per-bin results are bitwise identical at every N, and the only cross-GPU
+traffic is the final gather of the per-rank results to one rank (NCCL over
+NVLink for CUDA tensors, gloo for host tensors) in fixed rank order.
+
+Entry points: :func:`run_shard` (this rank's share of a global batch; what
+each process runs), :func:`run_sharded` / :func:`fastfca_run_sharded` /
+:func:`fca_run_sharded` (shard + run + gather under ``torch.distributed``).
 """
 
 from __future__ import annotations
@@ -30,6 +37,7 @@ class Shard:
     axis: str  # "mixtures" or "bins"
     start: int
     stop: int
+    total: int = 0  # units of the whole problem along ``axis``
 
     @property
     def size(self):
@@ -39,8 +47,8 @@ class Shard:
 def plan_shard(M, F, rank, world):
     """Mixture shards for batches (M > 1), bin shards for one mixture."""
     if M > 1:
-        return Shard("mixtures", *shard_range(M, rank, world))
-    return Shard("bins", *shard_range(F, rank, world))
+        return Shard("mixtures", *shard_range(M, rank, world), int(M))
+    return Shard("bins", *shard_range(F, rank, world), int(F))
 
 
 def take(shard, y, v, S, floor):
@@ -65,9 +73,10 @@ def gather_results(local, shard, group=None, dst=0):
     """Gather per-rank result arrays to ``dst`` and concatenate in rank order.
 
     ``local``: dict of torch tensors (CUDA with NCCL, CPU with gloo) in the
-    batched layouts. For bin shards the per-rank log-likelihood partial sums
-    are added in rank order (fixed order: deterministic). Returns the full
-    dict on ``dst`` and None elsewhere.
+    batched layouts. Shards are padded to the largest shard and sent with one
+    ``gather`` per array (only ``dst`` receives). For bin shards the per-rank
+    log-likelihood partial sums are added in rank order (fixed order:
+    deterministic). Returns the full dict on ``dst`` and None elsewhere.
     """
     import torch
     import torch.distributed as dist
@@ -76,32 +85,182 @@ def gather_results(local, shard, group=None, dst=0):
     rank = dist.get_rank(group)
     axes = RESULT_AXES[shard.axis]
     out = {} if rank == dst else None
-    for key, t in local.items():
+    # shard sizes are a pure function of (total, world): no size exchange
+    sizes = [b - a for a, b in (shard_range(shard.total, r, world) for r in range(world))]
+    for key in sorted(local):
+        t = local[key]
         if t is None:
             continue
         ax = axes.get(key)
-        t = t.contiguous()
+        cplx = t.is_complex()
+        # complex payloads travel as (..., 2) reals: gloo has no complex
+        # reductions / gathers, and NCCL moves bytes either way
+        t = torch.view_as_real(t.contiguous()) if cplx else t.contiguous()
         if ax is None:  # summed partials (bin-sharded log-likelihood)
-            parts = [torch.empty_like(t) for _ in range(world)]
-            dist.all_gather(parts, t, group=group)
+            parts = [torch.empty_like(t) for _ in range(world)] if rank == dst else None
+            dist.gather(t, parts, dst=dst, group=group)
             if rank == dst:
                 acc = parts[0].clone()
                 for p in parts[1:]:
                     acc += p
                 out[key] = acc
             continue
-        # variable shard sizes: exchange sizes, pad to the max, all_gather
-        n = torch.tensor([t.shape[ax]], device=t.device, dtype=torch.int64)
-        sizes = [torch.empty_like(n) for _ in range(world)]
-        dist.all_gather(sizes, n, group=group)
-        sizes = [int(s.item()) for s in sizes]
         mx = max(sizes)
-        pad_shape = list(t.shape)
-        pad_shape[ax] = mx
-        buf = torch.zeros(pad_shape, dtype=t.dtype, device=t.device)
-        buf.narrow(ax, 0, t.shape[ax]).copy_(t)
-        parts = [torch.empty_like(buf) for _ in range(world)]
-        dist.all_gather(parts, buf, group=group)
+        if t.shape[ax] != mx:
+            pad_shape = list(t.shape)
+            pad_shape[ax] = mx
+            buf = torch.zeros(pad_shape, dtype=t.dtype, device=t.device)
+            buf.narrow(ax, 0, t.shape[ax]).copy_(t)
+        else:
+            buf = t
+        parts = [torch.empty_like(buf) for _ in range(world)] if rank == dst else None
+        dist.gather(buf, parts, dst=dst, group=group)
         if rank == dst:
-            out[key] = torch.cat([p.narrow(ax, 0, s) for p, s in zip(parts, sizes)], dim=ax)
+            full = torch.cat([p.narrow(ax, 0, n) for p, n in zip(parts, sizes)], dim=ax)
+            out[key] = torch.view_as_complex(full) if cplx else full
     return out
+
+
+# ---- sharded runs -------------------------------------------------------------
+MAX_WORLD = 8  # one node of B200s
+
+
+def shard_chunk_frames(M, N, F, I, dtype="c128", algorithm="fast", max_world=MAX_WORLD):
+    """The frame chunking every world size uses: the auto plan of the
+    largest shard at ``max_world`` ranks (rank 0's), which fills one GPU at
+    that world size. Equal chunking at every N => bitwise-equal per-bin
+    results (the per-bin reduction order depends on the chunking only)."""
+    from ._engine import plan_chunks
+
+    sh = plan_shard(M, F, 0, max_world)
+    G = sh.size * F if sh.axis == "mixtures" else sh.size
+    cf, _ = plan_chunks(G, N, I, dtype, algorithm)
+    return cf
+
+
+def grid_model(G, N, I, chunk_frames, dtype="c128", algorithm="fast"):
+    """Modelled grid of one streaming pass: CTAs, resident slots, waves."""
+    import ctypes
+
+    from . import _device as D
+    from ._engine import DTYPES
+
+    lib = D.require()
+    ctas, slots = ctypes.c_int64(), ctypes.c_int64()
+    D.check_rc(lib.ffca_plan_grid(int(G), int(N), int(I), DTYPES[dtype],
+                                  0 if algorithm == "fast" else 1, int(chunk_frames),
+                                  ctypes.byref(ctas), ctypes.byref(slots)), "ffca_plan_grid")
+    return {"ctas": int(ctas.value), "slots": int(slots.value),
+            "waves": round(ctas.value / max(slots.value, 1), 3)}
+
+
+def _host_array(x):
+    if hasattr(x, "detach"):  # torch tensor
+        x = x.detach()
+        return x.cpu().numpy() if x.is_cuda else x.numpy()
+    return np.asarray(x)
+
+
+def _device_runner(algorithm, y, v, S, floor, L, *, chunk_frames, likelihood, images, dtype):
+    from ._engine import run_device
+
+    r = run_device(algorithm, y, v, S, floor, L, likelihood=likelihood, history=False,
+                   images=images, dtype=dtype, timing=False, check=True,
+                   chunk_frames=chunk_frames)
+    return {"images": r.images, "v": r.v, "S": r.S, "loglik": r.loglik}
+
+
+def run_shard(algorithm, y, init, iterations, rank, world, *, chunk_frames=None, runner=None,
+              likelihood=True, images=True, dtype="c128"):
+    """Run this rank's shard of a global problem on the current device.
+
+    ``y`` (M,N,F,I) or (N,F,I) and ``init`` (a SpatialModel of matching
+    shape) are the GLOBAL inputs (host arrays; each rank slices its own
+    contiguous mixture or bin range). Returns ``(shard, local)`` with
+    ``local`` the shard's results in the batched layouts (images, v, S,
+    loglik — for bin shards the partial log-likelihood over the shard's bins,
+    which the gather sums). ``runner`` replaces the CUDA run (tests use the
+    CPU oracle); ``chunk_frames`` defaults to :func:`shard_chunk_frames`.
+    """
+    from ._engine import as_batch
+
+    yb, vb, Sb, fb, _ = as_batch(y, init)
+    M, N, F, I = (int(s) for s in yb.shape)
+    shard = plan_shard(M, F, rank, world)
+    if chunk_frames is None:  # (a custom runner plans its own chunking)
+        chunk_frames = shard_chunk_frames(M, N, F, I, dtype, algorithm) if runner is None else 0
+    ys, vs, Ss, fs = take(shard, *(_host_array(x) for x in (yb, vb, Sb, fb)))
+    run = runner or _device_runner
+    local = run(algorithm, ys, vs, Ss, fs, int(iterations), chunk_frames=chunk_frames,
+                likelihood=likelihood, images=images, dtype=dtype)
+    return shard, {k: t for k, t in local.items() if t is not None}
+
+
+def run_sharded(algorithm, y, init, iterations, *, group=None, dst=0, runner=None,
+                likelihood=True, images=True, dtype="c128", chunk_frames=None):
+    """Shard a run over the ranks of ``group`` (one GPU per rank), run each
+    shard with no collective, and gather the results to ``dst``.
+
+    Returns ``(shard, full)``: ``full`` is the dict of whole-problem results
+    (images, v, S, loglik; tensors on ``dst``'s device) on ``dst`` and None
+    elsewhere.
+    """
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    shard, local = run_shard(algorithm, y, init, iterations, rank, world,
+                             chunk_frames=chunk_frames, runner=runner, likelihood=likelihood,
+                             images=images, dtype=dtype)
+    return shard, gather_results(local, shard, group=group, dst=dst)
+
+
+def _result(algorithm, full, y, init, L):
+    from . import _device as D
+    from ._engine import as_batch
+    from .types import OpCounts, SeparationResult, SpatialModel
+
+    batched = as_batch(y, init)[4]
+    sel = (lambda t: t) if batched else (lambda t: t[0])
+    host = not (D.is_tensor(y) and y.is_cuda)
+    conv = D.host if host else (lambda t: t)
+    M, _, N, F = (int(s) for s in full["v"].shape)
+    L = int(L)
+    counts = OpCounts()
+    if algorithm == "fast":
+        counts.add(gevds=L * F * M, bin_products=2 * L * F * M)
+    else:
+        counts.add(inversions=L * N * F * M, products=3 * L * N * F * M)
+        if L == 0:
+            counts.add(inversions=N * F * M, products=3 * N * F * M)
+    ll = full.get("loglik")
+    if ll is None:
+        trace = []
+    else:
+        llh = ll.cpu().numpy()
+        trace = llh if batched else [float(x) for x in llh[0]]
+    return SeparationResult(
+        algorithm="FastFCA" if algorithm == "fast" else "FCA",
+        images=conv(sel(full["images"])) if full.get("images") is not None else None,
+        loglik_trace=trace, iteration_seconds=[], em_seconds=0.0, op_counts=counts,
+        model=SpatialModel(v=conv(sel(full["v"])), S=conv(sel(full["S"])),
+                           v_floor=init.v_floor),
+        history=[])
+
+
+def fastfca_run_sharded(y, init, iterations, compute_likelihood=True, *, group=None, dst=0,
+                        dtype="c128", runner=None):
+    """``fastfca_run`` (reference fast.py:156-260) over all ranks of ``group``:
+    returns the SeparationResult on ``dst`` (None elsewhere). Batches shard by
+    mixture, single mixtures by bin; NCCL carries only the final gather."""
+    _, full = run_sharded("fast", y, init, iterations, group=group, dst=dst, runner=runner,
+                          likelihood=compute_likelihood, dtype=dtype)
+    return None if full is None else _result("fast", full, y, init, iterations)
+
+
+def fca_run_sharded(y, init, iterations, compute_likelihood=True, *, group=None, dst=0,
+                    dtype="c128", runner=None):
+    """``fca_run`` (reference conventional.py:104-164) over all ranks of
+    ``group`` (see :func:`fastfca_run_sharded`)."""
+    _, full = run_sharded("fca", y, init, iterations, group=group, dst=dst, runner=runner,
+                          likelihood=compute_likelihood, dtype=dtype)
+    return None if full is None else _result("fca", full, y, init, iterations)

@@ -65,21 +65,26 @@ def test_single_mixture_configs_fastfca_and_fca(idx):
         _compare_bins(res, ref, bins)
 
 
-def test_config2_complex64_within_1e4():
+@pytest.mark.parametrize("engine", ["fast", "fca"])
+def test_config2_complex64_within_1e4(engine):
+    """Full config 2 (I = 8) in complex64 against the complex128 oracle on
+    sampled bins, both engines (BASELINE.json configs[2] names c64)."""
     import paper_1805_06572_b200 as P
 
     cfg = CONFIGS[2]
     y = config_mixture(cfg, 0)
     model = P.init_random(y, init_seed(cfg, 0))
     bins = [0, 256, 512]
-    ref = _sampled_oracle(y, model, cfg.L, bins, "fast")
-    res = P.fastfca_run(y, model, cfg.L, dtype="c64")
+    ref = _sampled_oracle(y, model, cfg.L, bins, engine)
+    run = P.fastfca_run if engine == "fast" else P.fca_run
+    res = run(y, model, cfg.L, dtype="c64")
     assert O.scale_dev(res.model.v[:, :, bins], ref.v) <= 1e-4
+    assert O.scale_dev(res.model.S[:, bins], ref.S) <= 1e-4
     assert O.scale_dev(res.images[:, :, bins], ref.images) <= 1e-4
 
 
-@pytest.mark.parametrize("dtype,tol", [("c128", TOL), ("c64", 1e-4)])
-def test_config3_batch_of_256(dtype, tol):
+@pytest.fixture(scope="module")
+def config3_batch():
     import paper_1805_06572_b200 as P
 
     cfg = CONFIGS[3]
@@ -91,10 +96,24 @@ def test_config3_batch_of_256(dtype, tol):
     Y = np.stack(ys)
     batch = P.SpatialModel(v=np.stack([m.v for m in models]), S=np.stack([m.S for m in models]),
                            v_floor=np.stack([m.v_floor for m in models]))
-    res = P.fastfca_run(Y, batch, cfg.L, dtype=dtype)
+    return cfg, ys, models, Y, batch
+
+
+@pytest.mark.parametrize("engine", ["fast", "fca"])
+@pytest.mark.parametrize("dtype,tol", [("c128", TOL), ("c64", 1e-4)])
+def test_config3_batch_of_256(config3_batch, engine, dtype, tol):
+    """The full 256-mixture config-3 batch through the public API (host
+    buffers -> chunked, transfer-overlapped runs), both engines, both
+    precisions; sampled mixtures and bins against the complex128 oracle."""
+    import paper_1805_06572_b200 as P
+
+    cfg, ys, models, Y, batch = config3_batch
+    run = P.fastfca_run if engine == "fast" else P.fca_run
+    res = run(Y, batch, cfg.L, dtype=dtype)
     for m in (0, 131, 255):
         assert _monotone(res.loglik_trace[m])
         bins = [3, 200]
-        ref = _sampled_oracle(ys[m], models[m], cfg.L, bins, "fast")
+        ref = _sampled_oracle(ys[m], models[m], cfg.L, bins, engine)
         assert O.scale_dev(res.model.v[m][:, :, bins], ref.v) <= tol
+        assert O.scale_dev(res.model.S[m][:, bins], ref.S) <= tol
         assert O.scale_dev(res.images[m][:, :, bins], ref.images) <= tol

@@ -83,6 +83,21 @@ def test_complex64_within_1e4_of_reference(case):
     assert _ll_dev(res.loglik_trace, g["fast_ll"]) <= TOL_C64
 
 
+@pytest.mark.parametrize("case", ["cfg3m0", "cfg2", "acc2"])
+def test_fca_complex64_within_1e4_of_reference(case):
+    """fca_run(dtype='c64') against the complex128 reference (conventional.py:
+    104-164; the reference has no c64 path, so the c128 golden run is the bar).
+    The c64 FCA pass streams y / v in complex64 and computes in FP64."""
+    g = load_golden(f"runs_{case}")
+    res = _pkg().fca_run(g["y"], _model(g), int(g["L"]), dtype="c64")
+    stride = int(g["image_stride"])
+    assert res.images.dtype == np.complex64
+    assert O.scale_dev(res.images[:, ::stride], g["fca_images"]) <= TOL_C64
+    assert O.scale_dev(res.model.v, g["fca_v"]) <= TOL_C64
+    assert O.scale_dev(res.model.S, g["fca_S"]) <= TOL_C64
+    assert _ll_dev(res.loglik_trace, g["fca_ll"]) <= TOL_C64
+
+
 @pytest.mark.parametrize("I", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_every_channel_count_matches_oracle(I):
     y, v, S = random_instance(300 + I, n_frames=37, n_bins=6, n_chan=I)
@@ -370,13 +385,28 @@ def test_stage_api_matches_oracle():
     mu_o, phi_o, _, _ = O.fca_e_step(y, v, S)
     assert O.scale_dev(post.mu, mu_o) <= 1e-12
     assert O.scale_dev(back_transform_images(mu_t, Pm), mu_o) <= 1e-10
+    # m_step (conventional.py:83-95) against the oracle's v / S updates
     new = P.m_step(post, model)
+    v_o = np.maximum(O.fca_v_update(phi_o, S), floor[None, None, :])
+    S_o = O.regularize_covariances(O.S_update(phi_o, v_o))
+    assert O.scale_dev(new.v, v_o) <= 1e-12
+    assert O.scale_dev(new.S, S_o) <= 1e-12
+    # fast_m_step_v / fast_m_step_S (fast.py:74-104) against the oracle in the
+    # transformed basis, and back-transformed against the conventional update
+    # (the two engines' M-steps are the same map, test_fast.py:185-252)
+    yt_o = O.fast_transform(y, P_o)
+    mu_to, phi_to = O.fast_e_step(yt_o, v, lam_o)
     v_fast = np.maximum(P.fast_m_step_v(phi_t, lam), floor[None, None, :])
-    assert O.scale_dev(v_fast, new.v) <= 1e-10
+    v_fast_o = np.maximum(O.fast_v_update(phi_to, lam_o), floor[None, None, :])
+    assert O.scale_dev(v_fast, v_fast_o) <= 1e-12
+    assert O.scale_dev(v_fast, v_o) <= 1e-10
     gram = np.conj(np.swapaxes(Pm, -1, -2)) @ Pm
     s_t = P.fast_m_step_S(phi_t, v_fast, gram=gram)
+    gram_o = np.conj(np.swapaxes(P_o, -1, -2)) @ P_o
+    s_to = O.regularize_transformed(O.S_update(phi_to, v_fast_o), gram_o)
     s_back = back_transform_covariances(s_t, Pm)
-    assert O.scale_dev(s_back, new.S) <= 1e-10
+    assert O.scale_dev(s_back, O.back_transform_covariances(s_to, P_o)) <= 1e-10
+    assert O.scale_dev(s_back, S_o) <= 1e-10
     p_next, lam_next = P.propagate_pencil(s_t[0], s_t[1], Pm)
     for f in range(2):
         ph = p_next[f].conj().T
@@ -410,3 +440,161 @@ def test_init_random_matches_oracle():
 def test_kernel_instance_shapes():
     y, v, S, Pm, lam = kernel_instance()
     assert y.shape == (9, 4, 3) and Pm.shape == (4, 3, 3)
+
+
+# ---- exported per-bin helpers (reference pencil.py, conventional.py) ---------
+def _random_hermitian(gen, d):
+    a = gen.standard_normal((d, d)) + 1j * gen.standard_normal((d, d))
+    return 0.5 * (a + a.conj().T)
+
+
+def _random_hpd(gen, d):
+    a = gen.standard_normal((d, d)) + 1j * gen.standard_normal((d, d))
+    return a @ a.conj().T + d * np.eye(d)
+
+
+def test_hermitian_eig_matches_reference_contract():
+    """reference test_pencil.py:37-67 (TestHermitianEig) and eigh's values."""
+    P = _pkg()
+    w, u = P.hermitian_eig(np.eye(2, dtype=complex))
+    assert np.allclose(w, [1.0, 1.0]) and np.allclose(u @ u.conj().T, np.eye(2), atol=1e-14)
+    w, u = P.hermitian_eig(np.diag([2.0, 1.0]).astype(complex))
+    assert np.allclose(w, [2.0, 1.0]) and np.allclose(np.abs(u), np.eye(2), atol=1e-14)
+    gen = np.random.default_rng(7)
+    for d in (2, 3, 4, 8):
+        hs = np.stack([_random_hermitian(gen, d) for _ in range(20)])
+        w, u = P.hermitian_eig(hs)  # batched
+        for h, wk, uk in zip(hs, w, u):
+            scale = max(np.abs(h).max(), 1.0)
+            assert np.abs((uk * wk) @ uk.conj().T - h).max() <= 1e-12 * scale
+            assert np.abs(uk.conj().T @ uk - np.eye(d)).max() <= 1e-12
+            assert np.all(np.diff(wk) <= 1e-12 * scale)
+            assert np.abs(wk - np.linalg.eigvalsh(h)[::-1]).max() <= 1e-12 * scale
+    with pytest.raises(P.NonHermitianError):
+        P.hermitian_eig(np.array([[1.0, 1.0], [0.0, 1.0]], dtype=complex))
+    with pytest.raises(P.NonHermitianError):
+        P.hermitian_eig(np.ones((2, 3), dtype=complex))
+
+
+def test_solve_hermitian_system_matches_reference_contract():
+    """reference test_pencil.py:146-166 (TestSolveHermitianSystem) and
+    np.linalg.solve (the reference's zgesv) on HPD and general systems."""
+    P = _pkg()
+    b = np.arange(6, dtype=complex).reshape(3, 2)
+    assert np.allclose(P.solve_hermitian_system(np.eye(3, dtype=complex), b), b)
+    x = P.solve_hermitian_system(np.diag([2.0, 4.0]).astype(complex), np.array([2.0, 4.0]))
+    assert x.shape == (2,) and np.allclose(x, [1.0, 1.0])
+    gen = np.random.default_rng(3)
+    for d in (2, 4, 8):
+        for _ in range(10):
+            a = _random_hpd(gen, d)
+            rhs = gen.standard_normal((d, 3)) + 1j * gen.standard_normal((d, 3))
+            x = P.solve_hermitian_system(a, rhs)
+            assert np.linalg.norm(a @ x - rhs) <= 1e-10 * np.linalg.norm(rhs)
+            assert O.scale_dev(x, np.linalg.solve(a, rhs)) <= 1e-12
+    # a non-Hermitian nonsingular matrix needs the pivoting (zero leading entry)
+    a = np.array([[0.0, 2.0, 1.0], [1.0, 1.0, 0.0], [3.0, 0.0, 1.0]], dtype=complex)
+    rhs = np.array([1.0, 2.0, 3.0], dtype=complex)
+    assert O.scale_dev(P.solve_hermitian_system(a, rhs), np.linalg.solve(a, rhs)) <= 1e-14
+    # batched
+    A = np.stack([_random_hpd(gen, 4) for _ in range(5)])
+    Bm = gen.standard_normal((5, 4, 2)) + 0j
+    assert O.scale_dev(P.solve_hermitian_system(A, Bm), np.linalg.solve(A, Bm)) <= 1e-12
+    with pytest.raises(P.SingularMatrixError):
+        P.solve_hermitian_system(np.zeros((2, 2), dtype=complex), np.ones(2))
+    with pytest.raises(P.SingularMatrixError):  # numerically singular: residual test
+        P.solve_hermitian_system(np.array([[1.0, 1.0], [1.0, 1.0 + 1e-17]], dtype=complex),
+                                 np.array([1.0, 0.0], dtype=complex))
+
+
+def test_cholesky_inverse_matches_oracle():
+    """conventional._cholesky_inverse (reference conventional.py:98-101)."""
+    from paper_1805_06572_b200.conventional import _cholesky_inverse
+
+    gen = np.random.default_rng(11)
+    for d in (1, 2, 3, 4, 8):
+        S = np.stack([np.stack([_random_hpd(gen, d) for _ in range(6)]) for _ in range(2)])
+        out = _cholesky_inverse(S)
+        assert out.shape == S.shape
+        assert O.scale_dev(out, O.cholesky_inverse(S)) <= 1e-12
+        assert O.scale_dev(out @ S, np.broadcast_to(np.eye(d), S.shape)) <= 1e-12
+    bad = np.stack([np.eye(2, dtype=complex), np.diag([1.0, -1.0]).astype(complex)])[None]
+    with pytest.raises(np.linalg.LinAlgError):
+        _cholesky_inverse(bad)
+
+
+def test_degenerate_mixture_in_any_host_chunk_raises():
+    """A failing mixture in the FIRST chunk of a chunked host batch (whose
+    device slot is reused by later chunks) still raises like a single run."""
+    P = _pkg()
+    gen = np.random.default_rng(31)
+    ys = [random_complex(gen, (40, 5, 2)) for _ in range(5)]
+    ys[0][:] = 0.0  # silent mixture -> collapsed powers (fast.py:39-55)
+    inits = [P.init_random(y, 90 + m) for m, y in enumerate(ys)]
+    Y = np.stack(ys)
+    batch = P.SpatialModel(v=np.stack([i.v for i in inits]), S=np.stack([i.S for i in inits]),
+                           v_floor=np.stack([i.v_floor for i in inits]))
+    from paper_1805_06572_b200._engine import run_host_pipelined
+
+    with pytest.raises(P.SingularMatrixError):
+        run_host_pipelined("fast", Y, batch.v, batch.S, batch.v_floor, 3, chunk_mixtures=1)
+    with pytest.raises(P.SingularMatrixError):
+        P.fastfca_run(Y, batch, 3)  # public API, ~one mixture per chunk
+    ok = run_host_pipelined("fast", Y[1:], batch.v[1:], batch.S[1:], batch.v_floor[1:], 3,
+                            chunk_mixtures=1)
+    assert np.isfinite(ok["images"]).all()
+
+
+def test_second_device_in_one_process():
+    """Kernels opting into > 48 KB of shared memory must be configured per
+    device: a run on cuda:1 after cuda:0 in the same process."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    from paper_1805_06572_b200._engine import run_device
+
+    P = _pkg()
+    gen = np.random.default_rng(5)
+    y = random_complex(gen, (64, 40, 4))
+    init = P.init_random(y, 2)
+    outs = []
+    for dev in (0, 1):
+        with torch.cuda.device(dev):
+            r = run_device("fast", y[None], init.v[None], init.S[None], init.v_floor[None], 3)
+            outs.append(r.images.cpu())
+    assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("M", [1, 5])
+def test_sharded_runs_bitwise_equal_at_every_world_size(M):
+    """sharding.run_shard with the one chunk plan (the largest world size's):
+    the shards of world sizes 1, 2, 3 and 8, run one after another on this
+    GPU and concatenated, are bitwise the 1-rank run (bins and mixtures never
+    couple; equal chunking => equal per-bin reduction order)."""
+    import torch
+
+    from paper_1805_06572_b200.sharding import run_shard
+
+    P = _pkg()
+    gen = np.random.default_rng(17)
+    if M == 1:
+        y = random_complex(gen, (700, 37, 4))
+        init = P.init_random(y, 8)
+        ax = {"images": 3, "v": 3, "S": 2}
+    else:
+        y = random_complex(gen, (M, 300, 9, 3))
+        inits = [P.init_random(y[m], 20 + m) for m in range(M)]
+        init = P.SpatialModel(v=np.stack([i.v for i in inits]), S=np.stack([i.S for i in inits]),
+                              v_floor=np.stack([i.v_floor for i in inits]))
+        ax = {"images": 0, "v": 0, "S": 0, "loglik": 0}
+    for algorithm in ("fast", "fca"):
+        _, one = run_shard(algorithm, y, init, 4, 0, 1)
+        for world in (2, 3, 8):
+            parts = [run_shard(algorithm, y, init, 4, r, world)[1] for r in range(world)]
+            for key, a in ax.items():
+                cat = torch.cat([p[key] for p in parts], dim=a)
+                assert torch.equal(cat, one[key]), (algorithm, world, key)
+            if M == 1:  # bin shards: likelihood partials add up to the full trace
+                tot = sum(p["loglik"] for p in parts)
+                assert torch.allclose(tot, one["loglik"], rtol=1e-12, atol=0)
