@@ -54,13 +54,15 @@ def parse():
     ap.add_argument("--dtype", choices=["c128", "c64"], default="c128")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-pageable", action="store_true", help="skip the numpy-input e2e leg")
     ap.add_argument("--no-other", action="store_true", help="skip the second engine")
     ap.add_argument("--streams", type=int, default=2,
                     help="concurrent streams over independent mixtures (batched configs)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="mixtures/bins in the CPU sample")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
-                    help="weak: every rank runs its own full config batch (independent "
-                         "mixtures, no collective); strong: the batch is sharded")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
+                    help="strong (default): the config's batch is sharded over the ranks "
+                         "(config 3 by mixture, single mixtures by bin) with one chunk plan "
+                         "at every N; weak: every rank runs its own full config batch")
     return ap.parse_args()
 
 
@@ -158,6 +160,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def config_dict(cfg, args, world):
+    """The workload description both arms print (identical dicts)."""
+    axis = "mixtures" if cfg.M > 1 else "bins"
+    y_gb = cfg.M * cfg.N * cfg.F * cfg.I * (16 if args.dtype == "c128" else 8) / 1e9
+    return {"workload": cfg.description, "engine": args.engine, "iterations": cfg.L,
+            "M": cfg.M, "F": cfg.F, "N": cfg.N, "I": cfg.I, "dtype": args.dtype,
+            "parallelism": (f"independent {cfg.M}-mixture batch per GPU x{world}"
+                            if args.scaling == "weak" else f"{axis}-sharded x{world}"),
+            "global_batch": cfg.M * (world if args.scaling == "weak" else 1),
+            "l2": "inputs larger than L2 (y = %.2f GB)" % (y_gb * (world if args.scaling ==
+                                                                   "weak" else 1))}
+
+
 def peaks():
     try:
         d = json.loads(PEAKS.read_text())
@@ -175,28 +190,52 @@ def cpu_port_time(cfg, engine, sample, threads):
 
 
 def run_reference(args, cfg):
-    """--impl reference: the reference algorithm on the host CPU (oracle port)."""
+    """--impl reference: the reference's own CPU implementation on this host's
+    cores — the UNMODIFIED reference package (numba backend) from
+    baseline/_ref, one warmed process per core (baseline/reference_numba.py);
+    the C/OpenMP oracle port only when baseline/_ref is absent. Rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    from oracle import cpu_port
+    sys.path.insert(0, str(REPO / "baseline"))
+    import reference_numba as RN
 
     vals = []
-    desc = kind = None
-    for i in range(args.warmup + args.steps):
-        v, desc, kind, cores = cpu_port.measure(cfg, args.engine, args.cpu_sample, threads)
-        if i >= args.warmup:
-            vals.append(v)
+    extra = {}
+    if RN.available():
+        pool = RN.ReferencePool(cfg, args.engine, threads)
+        try:
+            iters = RN.sample_iterations(cfg, args.engine)
+            for i in range(args.warmup + args.steps):
+                v = pool.step(iters)
+                if i >= args.warmup:
+                    vals.append(v)
+            extra["one_core"] = pool.one_core(iters)
+            desc, kind, cores = RN.describe(cfg, args.engine, pool, iters), "reference", pool.cores
+        finally:
+            pool.close()
+        if not args.no_cpu:  # the C/OpenMP restatement beside it (one sample)
+            from oracle import cpu_port
+
+            pv, pdesc, _, pcores = cpu_port.measure(cfg, args.engine, args.cpu_sample, threads)
+            extra["port"] = {"value": pv, "cores": pcores, "sample": pdesc}
+    else:
+        from oracle import cpu_port
+
+        for i in range(args.warmup + args.steps):
+            v, desc, kind, cores = cpu_port.measure(cfg, args.engine, args.cpu_sample, threads)
+            if i >= args.warmup:
+                vals.append(v)
     value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": f"EM TF-bin*iterations/s ({'FastFCA' if args.engine == 'fast' else 'FCA'}, config {cfg.index})",
         "value": value, "unit": "TF-bin*it/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "higher_is_better": True, "scaling": args.scaling,
-        "dtype": "c128", "data": "synthetic (seeded, BASELINE.json recipe)",
-        "config": {"workload": cfg.description, "engine": args.engine, "iterations": cfg.L},
+        "dtype": args.dtype, "data": "synthetic (seeded, BASELINE.json recipe)",
+        "config": config_dict(cfg, args, world),
         "cpu_baseline": {"value": value, "unit": "TF-bin*it/s", "cores": cores, "kind": kind,
-                         "sample": desc},
+                         "sample": desc, **extra},
         "e2e": {"value": value, "unit": "TF-bin*it/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -213,9 +252,17 @@ def main():
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    # FFCA_DIST_BACKEND=gloo (functional checks of the N>1 code on fewer GPUs
+    # than ranks; never a timing) maps ranks onto the visible devices
+    backend = os.environ.get("FFCA_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_1805_06572_b200 import SpatialModel, fastfca_run, fca_run
     from paper_1805_06572_b200._engine import run_device, torch_types
 
@@ -229,10 +276,20 @@ def main():
     v_d = torch.from_numpy(V).to(dev).to(rtype)
     S_d = torch.from_numpy(S).to(dev)
     fl_d = torch.from_numpy(FL).to(dev)
-    # the chunking the full (unsharded) problem would use -> identical per-bin sums
+    # ONE frame chunking at every world size (the plan that fills a GPU with
+    # the 8-rank shard) -> bitwise-identical per-bin results at N = 1..8
     from paper_1805_06572_b200._engine import plan_chunks
+    from paper_1805_06572_b200.sharding import grid_model, plan_shard, shard_chunk_frames
 
-    cf, _ = plan_chunks(cfg.M * cfg.F, cfg.N, cfg.I, args.dtype, args.engine)
+    if args.scaling == "strong":
+        cf = shard_chunk_frames(cfg.M, cfg.N, cfg.F, cfg.I, args.dtype, args.engine)
+    else:
+        cf, _ = plan_chunks(cfg.M * cfg.F, cfg.N, cfg.I, args.dtype, args.engine)
+    G_rank = M * F
+    sh8 = plan_shard(cfg.M, cfg.F, 0, 8)
+    grid = {"chunk_frames": cf, "this_rank": grid_model(G_rank, N, I, cf, args.dtype, args.engine),
+            "rank0_at_8_gpus": grid_model(sh8.size * (cfg.F if sh8.axis == "mixtures" else 1),
+                                          N, I, cf, args.dtype, args.engine)}
     tf_it_rank = M * F * N * L
     # whole-job units: all ranks' mixtures (weak) or the one sharded batch (strong)
     tf_it_total = cfg.M * cfg.F * cfg.N * L * (world if args.scaling == "weak" else 1)
@@ -341,6 +398,7 @@ def main():
 
     # end-to-end through the public API with pinned host buffers
     e2e = None
+    e2e_more = {}
     if not args.no_e2e:
         yh = torch.from_numpy(Y).to(ctype).pin_memory()
         vh = torch.from_numpy(V).to(rtype).pin_memory()
@@ -350,32 +408,79 @@ def main():
         run = fastfca_run if args.engine == "fast" else fca_run
         kw = dict(compute_likelihood=False, device_output=False, dtype=args.dtype,
                   chunk_frames=cf)
-        res = run(yh, model, L, **kw)  # warm the pinned pools
-        h2d = yh.numel() * yh.element_size() + vh.numel() * vh.element_size() + \
-            Sh.numel() * Sh.element_size() + flh.numel() * flh.element_size()
-        d2h = res.images.nbytes + res.model.v.nbytes + res.model.S.nbytes
+
+        def nbytes(*ts):
+            return int(sum(t.numel() * t.element_size() for t in ts))
+
+        def over_ranks(x, op):
+            t = torch.tensor([float(x)], device=dev, dtype=torch.float64)
+            if world > 1:
+                dist.all_reduce(t, op=op)
+            return float(t.item())
+
+        def timed(fn, reps):
+            fn()  # warm (pinned pools, graphs, NCCL communicators)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                r = fn()
+                ts.append(time.perf_counter() - t0)
+                del r
+            return over_ranks(statistics.median(ts), dist.ReduceOp.MAX if world > 1 else None)
+
+        reps = max(1, min(args.steps, 3))
+        res = run(yh, model, L, **kw)
+        h2d = over_ranks(nbytes(yh, vh, Sh, flh), dist.ReduceOp.SUM if world > 1 else None)
+        d2h = over_ranks(sum(np.asarray(a).nbytes for a in (res.images, res.model.v,
+                                                             res.model.S)),
+                         dist.ReduceOp.SUM if world > 1 else None)
         del res  # results go back to the pinned cache: steady state, not cudaHostAlloc
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e_times = []
-        for _ in range(max(1, min(args.steps, 3))):
-            t0 = time.perf_counter()
-            res = run(yh, model, L, **kw)
-            e_times.append(time.perf_counter() - t0)
-            del res
-        et = torch.tensor([statistics.median(e_times)], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": tf_it_total / float(et.item()), "unit": "TF-bin*it/s",
-               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
-               "s_per_step": round(float(et.item()), 4)}
+        # (1) every rank: public fastfca_run on its own shard, pinned host in -> pinned host out
+        t_sh = timed(lambda: run(yh, model, L, **kw), reps)
+        shards_line = {"value": tf_it_total / t_sh, "unit": "TF-bin*it/s",
+                       "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                       "s_per_step": round(t_sh, 4)}
+        if world > 1 and args.scaling == "strong":
+            # (2) the sharded public entry point: per-rank H2D of its shard, the
+            # run, the NCCL gather of images / v / S / floor to rank 0's GPU and
+            # rank 0's D2H of the whole result
+            from paper_1805_06572_b200.sharding import fastfca_run_sharded, fca_run_sharded
+
+            srun = fastfca_run_sharded if args.engine == "fast" else fca_run_sharded
+            t_g = timed(lambda: srun(yh, model, L, compute_likelihood=False, dtype=args.dtype,
+                                     chunk_frames=cf, global_size=(cfg.M, cfg.F)), reps)
+            e2e = {"value": tf_it_total / t_g, "unit": "TF-bin*it/s",
+                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                   "s_per_step": round(t_g, 4),
+                   "path": "fastfca_run_sharded: per-rank H2D + run, NCCL gather to rank 0, "
+                           "rank-0 D2H"}
+            e2e_more["e2e_host_shards"] = dict(shards_line, path="per-rank fastfca_run on its "
+                                               "shard, pinned host in/out (no gather)")
+        else:
+            e2e = dict(shards_line, path="fastfca_run, pinned host buffers (pipelined "
+                                         "H2D / run / D2H)")
+        if world == 1 and not args.no_pageable:
+            # (3) a numpy caller: pageable host arrays in, numpy out
+            model_np = SpatialModel(v=V.astype(np.float64 if args.dtype == "c128" else
+                                               np.float32), S=S, v_floor=FL)
+            Yc = Y if args.dtype == "c128" else Y.astype(np.complex64)
+            t_pg = timed(lambda: run(Yc, model_np, L, **kw), 1)
+            e2e_more["e2e_pageable"] = {"value": tf_it_total / t_pg, "unit": "TF-bin*it/s",
+                                        "s_per_step": round(t_pg, 4),
+                                        "path": "fastfca_run, numpy (pageable) inputs"}
+            del Yc, model_np
+        del yh, vh, Sh, flh, model
 
     # the other engine on the same resident inputs (the metric names both)
     other = "fca" if args.engine == "fast" else "fast"
     other_line = None
     if not args.no_other:
-        ocf, _ = plan_chunks(cfg.M * cfg.F, cfg.N, cfg.I, args.dtype, other)
+        ocf = (shard_chunk_frames(cfg.M, cfg.N, cfg.F, cfg.I, args.dtype, other)
+               if args.scaling == "strong" else
+               plan_chunks(cfg.M * cfg.F, cfg.N, cfg.I, args.dtype, other)[0])
         obufs = {"images": bufs["images"], "S": bufs["S"], "v": bufs["v"]}
 
         def ostep():
@@ -410,10 +515,21 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        # the unmodified reference (numba, baseline/_ref) on all host cores and
+        # on one core, and the C/OpenMP oracle port beside it
         threads = len(os.sched_getaffinity(0))
         v_cpu, desc, kind, cores = cpu_port_time(cfg, args.engine, args.cpu_sample, threads)
-        cpu = {"value": v_cpu, "unit": "TF-bin*it/s", "cores": cores, "kind": kind,
-               "sample": desc}
+        port = {"value": v_cpu, "unit": "TF-bin*it/s", "cores": cores, "kind": kind,
+                "sample": desc}
+        cpu = port
+        sys.path.insert(0, str(REPO / "baseline"))
+        import reference_numba as RN
+
+        if RN.available():
+            r = RN.measure(cfg, args.engine, threads)
+            cpu = {"value": r["all_cores"], "unit": "TF-bin*it/s", "cores": r["cores"],
+                   "kind": "reference", "sample": r["sample"], "one_core": r["one_core"],
+                   "cpu_model": r["cpu_model"], "port": port}
 
     # status init + initial pencil + L x (fused pass + pencil), per concurrent part
     launches_per_step = (2 + 2 * L) * nstreams
@@ -424,14 +540,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (seeded, BASELINE.json recipe)",
-            "config": {"workload": cfg.description, "engine": args.engine, "iterations": L,
-                       "M": cfg.M, "F": cfg.F, "N": cfg.N, "I": cfg.I,
-                       "parallelism": (f"independent {cfg.M}-mixture batch per GPU x{world}"
-                                       if args.scaling == "weak" else f"{sh[0]}-sharded x{world}"),
-                       "global_batch": cfg.M * (world if args.scaling == "weak" else 1),
-                       "streams_per_gpu": nstreams,
-                       "l2": "inputs larger than L2 (y = %.2f GB)" % (Y.nbytes / 1e9 * world)},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "config": config_dict(cfg, args, world),
+            "layout": {"streams_per_gpu": nstreams, "shard": list(sh), "grid": grid},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, **e2e_more,
             ("fca" if other == "fca" else "fastfca"): other_line,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),

@@ -64,8 +64,8 @@ def take(shard, y, v, S, floor):
 
 # axis of the shard dimension in each result array (batched layouts)
 RESULT_AXES = {
-    "mixtures": {"images": 0, "v": 0, "S": 0, "loglik": 0},
-    "bins": {"images": 3, "v": 3, "S": 2, "loglik": None},
+    "mixtures": {"images": 0, "v": 0, "S": 0, "floor": 0, "loglik": 0},
+    "bins": {"images": 3, "v": 3, "S": 2, "floor": 1, "loglik": None},
 }
 
 
@@ -87,10 +87,14 @@ def gather_results(local, shard, group=None, dst=0):
     out = {} if rank == dst else None
     # shard sizes are a pure function of (total, world): no size exchange
     sizes = [b - a for a, b in (shard_range(shard.total, r, world) for r in range(world))]
+    # gloo gathers host tensors only: CUDA results are staged through the host
+    stage = dist.get_backend(group) == "gloo"
     for key in sorted(local):
         t = local[key]
         if t is None:
             continue
+        if stage and t.is_cuda:
+            t = t.cpu()
         ax = axes.get(key)
         cplx = t.is_complex()
         # complex payloads travel as (..., 2) reals: gloo has no complex
@@ -170,47 +174,100 @@ def _device_runner(algorithm, y, v, S, floor, L, *, chunk_frames, likelihood, im
     return {"images": r.images, "v": r.v, "S": r.S, "loglik": r.loglik}
 
 
+def _empty_local(shard, M, N, F, I, L, dtype, likelihood, images, device):
+    """Results of an empty shard in the batched layouts (zero-size along the
+    shard axis; a bin shard's likelihood partial is an exact zero)."""
+    import torch
+
+    from ._engine import torch_types
+
+    ctype, rtype = torch_types(dtype)
+    if shard.axis == "mixtures":
+        m, f = 0, F
+    else:
+        m, f = M, 0
+    kw = dict(device=device)
+    out = {"v": torch.empty((m, 2, N, f), dtype=rtype, **kw),
+           "S": torch.empty((m, 2, f, I, I), dtype=torch.complex128, **kw),
+           "floor": torch.empty((m, f), dtype=torch.float64, **kw)}
+    if images:
+        out["images"] = torch.empty((m, 2, N, f, I), dtype=ctype, **kw)
+    if likelihood:
+        out["loglik"] = torch.zeros((m, L + 1), dtype=torch.float64, **kw)
+    return out
+
+
 def run_shard(algorithm, y, init, iterations, rank, world, *, chunk_frames=None, runner=None,
-              likelihood=True, images=True, dtype="c128"):
-    """Run this rank's shard of a global problem on the current device.
+              likelihood=True, images=True, dtype="c128", global_size=None):
+    """Run this rank's shard of a problem on the current device.
 
     ``y`` (M,N,F,I) or (N,F,I) and ``init`` (a SpatialModel of matching
-    shape) are the GLOBAL inputs (host arrays; each rank slices its own
-    contiguous mixture or bin range). Returns ``(shard, local)`` with
+    shape) are the GLOBAL inputs (host arrays or tensors; each rank slices its
+    own contiguous mixture or bin range) — or, with ``global_size=(M, F)``
+    (the whole problem's mixture and bin counts), this rank's shard already
+    (what a caller that never holds the global batch passes; pinned host
+    tensors then copy asynchronously). Returns ``(shard, local)`` with
     ``local`` the shard's results in the batched layouts (images, v, S,
-    loglik — for bin shards the partial log-likelihood over the shard's bins,
-    which the gather sums). ``runner`` replaces the CUDA run (tests use the
-    CPU oracle); ``chunk_frames`` defaults to :func:`shard_chunk_frames`.
+    floor, loglik — for bin shards the partial log-likelihood over the
+    shard's bins, which the gather sums). ``runner`` replaces the CUDA run
+    (tests use the CPU oracle); ``chunk_frames`` defaults to
+    :func:`shard_chunk_frames` of the whole problem.
     """
+    import torch
+
     from ._engine import as_batch
 
     yb, vb, Sb, fb, _ = as_batch(y, init)
     M, N, F, I = (int(s) for s in yb.shape)
-    shard = plan_shard(M, F, rank, world)
+    if global_size is None:
+        Mg, Fg = M, F
+    else:
+        Mg, Fg = (int(s) for s in global_size)
+    shard = plan_shard(Mg, Fg, rank, world)
+    if global_size is not None:
+        got = M if shard.axis == "mixtures" else F
+        if got != shard.size or (shard.axis == "mixtures" and F != Fg) or \
+                (shard.axis == "bins" and M != Mg):
+            raise ValueError(f"rank {rank}/{world}: local inputs (M={M}, F={F}) are not the "
+                             f"{shard.axis} shard [{shard.start}, {shard.stop}) of "
+                             f"(M={Mg}, F={Fg})")
     if chunk_frames is None:  # (a custom runner plans its own chunking)
-        chunk_frames = shard_chunk_frames(M, N, F, I, dtype, algorithm) if runner is None else 0
-    ys, vs, Ss, fs = take(shard, *(_host_array(x) for x in (yb, vb, Sb, fb)))
+        chunk_frames = shard_chunk_frames(Mg, N, Fg, I, dtype, algorithm) if runner is None else 0
+    dev = "cpu" if runner is not None else "cuda"
+    if shard.size == 0:  # more ranks than units: this rank only joins the gather
+        return shard, _empty_local(shard, Mg, N, Fg, I, int(iterations), dtype, likelihood,
+                                   images, dev)
+    if global_size is None:
+        ys, vs, Ss, fs = take(shard, *(_host_array(x) for x in (yb, vb, Sb, fb)))
+    else:
+        ys, vs, Ss, fs = yb, vb, Sb, fb
     run = runner or _device_runner
     local = run(algorithm, ys, vs, Ss, fs, int(iterations), chunk_frames=chunk_frames,
                 likelihood=likelihood, images=images, dtype=dtype)
-    return shard, {k: t for k, t in local.items() if t is not None}
+    local = {k: t for k, t in local.items() if t is not None}
+    ref = local["v"]
+    local["floor"] = (fs if torch.is_tensor(fs) else torch.from_numpy(np.asarray(fs))).to(
+        device=ref.device, dtype=torch.float64)
+    return shard, local
 
 
 def run_sharded(algorithm, y, init, iterations, *, group=None, dst=0, runner=None,
-                likelihood=True, images=True, dtype="c128", chunk_frames=None):
+                likelihood=True, images=True, dtype="c128", chunk_frames=None,
+                global_size=None):
     """Shard a run over the ranks of ``group`` (one GPU per rank), run each
-    shard with no collective, and gather the results to ``dst``.
+    shard with no collective, and gather the results to ``dst`` (NCCL for
+    CUDA results; the only cross-GPU traffic of the run).
 
     Returns ``(shard, full)``: ``full`` is the dict of whole-problem results
-    (images, v, S, loglik; tensors on ``dst``'s device) on ``dst`` and None
-    elsewhere.
+    (images, v, S, floor, loglik; tensors on ``dst``'s device) on ``dst`` and
+    None elsewhere. ``global_size``: see :func:`run_shard`.
     """
     import torch.distributed as dist
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     shard, local = run_shard(algorithm, y, init, iterations, rank, world,
                              chunk_frames=chunk_frames, runner=runner, likelihood=likelihood,
-                             images=images, dtype=dtype)
+                             images=images, dtype=dtype, global_size=global_size)
     return shard, gather_results(local, shard, group=group, dst=dst)
 
 
@@ -243,24 +300,28 @@ def _result(algorithm, full, y, init, L):
         images=conv(sel(full["images"])) if full.get("images") is not None else None,
         loglik_trace=trace, iteration_seconds=[], em_seconds=0.0, op_counts=counts,
         model=SpatialModel(v=conv(sel(full["v"])), S=conv(sel(full["S"])),
-                           v_floor=init.v_floor),
+                           v_floor=conv(sel(full["floor"])) if "floor" in full
+                           else init.v_floor),
         history=[])
 
 
 def fastfca_run_sharded(y, init, iterations, compute_likelihood=True, *, group=None, dst=0,
-                        dtype="c128", runner=None):
+                        dtype="c128", runner=None, chunk_frames=None, global_size=None):
     """``fastfca_run`` (reference fast.py:156-260) over all ranks of ``group``:
     returns the SeparationResult on ``dst`` (None elsewhere). Batches shard by
-    mixture, single mixtures by bin; NCCL carries only the final gather."""
+    mixture, single mixtures by bin; NCCL carries only the final gather.
+    ``global_size=(M, F)``: ``y`` / ``init`` are this rank's shard already."""
     _, full = run_sharded("fast", y, init, iterations, group=group, dst=dst, runner=runner,
-                          likelihood=compute_likelihood, dtype=dtype)
+                          likelihood=compute_likelihood, dtype=dtype,
+                          chunk_frames=chunk_frames, global_size=global_size)
     return None if full is None else _result("fast", full, y, init, iterations)
 
 
 def fca_run_sharded(y, init, iterations, compute_likelihood=True, *, group=None, dst=0,
-                    dtype="c128", runner=None):
+                    dtype="c128", runner=None, chunk_frames=None, global_size=None):
     """``fca_run`` (reference conventional.py:104-164) over all ranks of
     ``group`` (see :func:`fastfca_run_sharded`)."""
     _, full = run_sharded("fca", y, init, iterations, group=group, dst=dst, runner=runner,
-                          likelihood=compute_likelihood, dtype=dtype)
+                          likelihood=compute_likelihood, dtype=dtype,
+                          chunk_frames=chunk_frames, global_size=global_size)
     return None if full is None else _result("fca", full, y, init, iterations)

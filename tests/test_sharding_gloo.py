@@ -69,7 +69,7 @@ def _oracle_runner(algorithm, ys, vs, Ss, fs, L, *, chunk_frames, likelihood, im
             else None}
 
 
-def _worker(rank, world, port, M, algorithm, result_q):
+def _worker(rank, world, port, M, algorithm, result_q, local=False):
     import torch.distributed as dist
 
     from paper_1805_06572_b200 import SpatialModel
@@ -81,27 +81,39 @@ def _worker(rank, world, port, M, algorithm, result_q):
     y, v, S, fl = _instance(M, 24, 9, 3, 5)
     if M == 1:  # one mixture in the reference shape -> bin shards
         y, v, S, fl = y[0], v[0], S[0], fl[0]
-    init = SpatialModel(v=v, S=S, v_floor=fl)
     run = fastfca_run_sharded if algorithm == "fast" else fca_run_sharded
-    # the real entry point: shard planning, per-rank slicing, the gather
-    res = run(y, init, 4, runner=_oracle_runner, dst=0)
+    if local:  # each rank holds only its own shard (global_size names the whole problem)
+        Mg, Fg = (M, y.shape[-2])
+        sh = plan_shard(Mg, Fg, rank, world)
+        yb, vb, Sb, fb = (x if M > 1 else x[None] for x in (y, v, S, fl))
+        ys, vs, Ss, fs = take(sh, yb, vb, Sb, fb)
+        if M == 1:
+            ys, vs, Ss, fs = ys[0], vs[0], Ss[0], fs[0]
+        res = run(ys, SpatialModel(v=vs, S=Ss, v_floor=fs), 4, runner=_oracle_runner, dst=0,
+                  global_size=(Mg, Fg))
+    else:
+        init = SpatialModel(v=v, S=S, v_floor=fl)
+        # the real entry point: shard planning, per-rank slicing, the gather
+        res = run(y, init, 4, runner=_oracle_runner, dst=0)
     if rank == 0:
         result_q.put({"images": res.images, "v": res.model.v, "S": res.model.S,
-                      "loglik": np.asarray(res.loglik_trace)})
+                      "floor": res.model.v_floor, "loglik": np.asarray(res.loglik_trace)})
     else:
         assert res is None
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("M,algorithm", [(3, "fast"), (1, "fast"), (3, "fca"), (1, "fca")])
-def test_two_rank_sharded_run_reproduces_unsharded_run(M, algorithm):
+@pytest.mark.parametrize("M,algorithm,local", [(3, "fast", False), (1, "fast", False),
+                                               (3, "fca", False), (1, "fca", False),
+                                               (3, "fast", True), (1, "fca", True)])
+def test_two_rank_sharded_run_reproduces_unsharded_run(M, algorithm, local):
     from oracle import fastfca_oracle as O
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, M, algorithm, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, M, algorithm, q, local)) for r in range(2)]
     for p in procs:
         p.start()
     out = q.get(timeout=300)
@@ -117,7 +129,36 @@ def test_two_rank_sharded_run_reproduces_unsharded_run(M, algorithm):
         assert np.array_equal(got["images"], ref.images)
         assert np.array_equal(got["v"], ref.v)
         assert np.array_equal(got["S"], ref.S)
+        assert np.array_equal(out["floor"][m] if M > 1 else out["floor"], fl[m])
         if M > 1:
             assert np.array_equal(got["loglik"], np.asarray(ref.loglik_trace))
         else:  # bin shards: per-rank partial sums added in rank order
             assert np.allclose(got["loglik"], np.asarray(ref.loglik_trace), rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("M", [1, 3])
+def test_more_ranks_than_units(M):
+    """World sizes above the unit count leave some ranks an empty shard; their
+    zero-size results (and zero likelihood partials) still concatenate to the
+    unsharded run (per-rank compute: the oracle)."""
+    import torch
+
+    from paper_1805_06572_b200 import SpatialModel
+    from paper_1805_06572_b200.sharding import run_shard
+
+    F = 3 if M == 1 else 9
+    y, v, S, fl = _instance(M, 16, F, 2, 9)
+    if M == 1:
+        y, v, S, fl = y[0], v[0], S[0], fl[0]
+    init = SpatialModel(v=v, S=S, v_floor=fl)
+    _, one = run_shard("fast", y, init, 3, 0, 1, runner=_oracle_runner)
+    world = 5
+    parts = [run_shard("fast", y, init, 3, r, world, runner=_oracle_runner)[1]
+             for r in range(world)]
+    assert sum(1 for p in parts if p["v"].numel() == 0) == world - (F if M == 1 else M)
+    ax = {"images": 3, "v": 3, "S": 2} if M == 1 else {"images": 0, "v": 0, "S": 0, "loglik": 0}
+    for key, a in ax.items():
+        assert torch.equal(torch.cat([p[key] for p in parts], dim=a), one[key]), key
+    if M == 1:
+        tot = sum(p["loglik"] for p in parts)
+        assert torch.allclose(tot, one["loglik"], rtol=1e-12, atol=0)
