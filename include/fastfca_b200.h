@@ -48,6 +48,8 @@ extern "C" {
 #define FFCA_ERR_NON_HERMITIAN 4    /* NonHermitianError, pencil.py:40-51 */
 #define FFCA_ERR_SINGULAR_BASIS 5   /* SingularMatrixError, fast.py:137-140 (basis solve) */
 #define FFCA_ERR_NOT_PD 6           /* numpy LinAlgError from cholesky, conventional.py:98-101 */
+#define FFCA_ERR_NO_CONVERGENCE 7   /* numpy LinAlgError from eigh (heevd did not converge),
+                                       pencil.py:72,113,130; here: Jacobi sweep limit */
 #define FFCA_ERR_INVALID 10         /* bad argument (shape, dtype, NULL pointer) */
 #define FFCA_ERR_CUDA 11            /* CUDA runtime failure */
 

@@ -105,6 +105,8 @@ def raise_for_status(st, N=None, F=None):
         raise SingularMatrixError("basis matrix is singular")
     if code == _lib.FFCA_ERR_NOT_PD:
         raise np.linalg.LinAlgError("Matrix is not positive definite")
+    if code == _lib.FFCA_ERR_NO_CONVERGENCE:  # numpy eigh's message (LAPACK heevd info > 0)
+        raise np.linalg.LinAlgError("Eigenvalues did not converge")
     raise RuntimeError(f"fastfca_b200: unknown status code {code}")
 
 

@@ -22,6 +22,7 @@ FFCA_ERR_DEFINITENESS = 3
 FFCA_ERR_NON_HERMITIAN = 4
 FFCA_ERR_SINGULAR_BASIS = 5
 FFCA_ERR_NOT_PD = 6
+FFCA_ERR_NO_CONVERGENCE = 7
 FFCA_ERR_INVALID = 10
 FFCA_ERR_CUDA = 11
 

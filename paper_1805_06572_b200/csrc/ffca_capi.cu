@@ -13,6 +13,8 @@
 #include <string>
 #include <utility>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ffca_internal.cuh"
 
 namespace ffca {
@@ -240,6 +242,29 @@ int run_graph(int algorithm, const ffca_run_args* a, cudaStream_t s) {
   return rc;
 }
 
+// NVTX range around a run's enqueue (header-only NVTX v3: free without a
+// tool attached; named with the run's shape for nsys / ncu --nvtx filters)
+struct NvtxRun {
+  NvtxRun(const char* what, const ffca_run_args* a) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "%s M=%lld N=%lld F=%lld I=%d L=%d %s%s", what, (long long)a->M,
+             (long long)a->N, (long long)a->F, a->I, a->iterations,
+             a->dtype == FFCA_C64 ? "c64" : "c128",
+             (a->flags & FFCA_FLAG_GRAPH) ? " graph" : "");
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRun() { nvtxRangePop(); }
+};
+
+struct NvtxIter {  // one EM iteration's launches
+  explicit NvtxIter(int l) {
+    char buf[32];
+    snprintf(buf, sizeof buf, "em iteration %d", l);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxIter() { nvtxRangePop(); }
+};
+
 bool graph_mode(const ffca_run_args* a) {
   return (a->flags & FFCA_FLAG_GRAPH) && !a->iter_events && !a->kernel_events && !debug_sync();
 }
@@ -308,6 +333,7 @@ int ffca_graph_cache_clear(void) {
 int ffca_fastfca_run(const ffca_run_args* a, void* stream) {
   const int rc = check_args(a);
   if (rc) return rc;
+  const NvtxRun range("ffca_fastfca_run", a);
   if (graph_mode(a)) return run_graph(0, a, (cudaStream_t)stream);
   return fastfca_enqueue(a, (cudaStream_t)stream);
 }
@@ -315,6 +341,7 @@ int ffca_fastfca_run(const ffca_run_args* a, void* stream) {
 int ffca_fca_run(const ffca_run_args* a, void* stream) {
   const int rc = check_args(a);
   if (rc) return rc;
+  const NvtxRun range("ffca_fca_run", a);
   if (graph_mode(a)) return run_graph(1, a, (cudaStream_t)stream);
   return fca_enqueue(a, (cudaStream_t)stream);
 }
@@ -378,6 +405,7 @@ static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
                              cudaMemcpyDeviceToDevice, s));
   } else {
     for (int l = 0; l < L; ++l) {
+      const NvtxIter nvtx_it(l);
       if (ev) FFCA_TRY(cudaEventRecord(ev[l], s));
       p.update = 1;
       const bool last = (l == L - 1);
@@ -470,6 +498,7 @@ static int fca_enqueue(const ffca_run_args* a, cudaStream_t s) {
                              cudaMemcpyDeviceToDevice, s));
   } else {
     for (int l = 0; l < L; ++l) {
+      const NvtxIter nvtx_it(l);
       if (ev) FFCA_TRY(cudaEventRecord(ev[l], s));
       p.update = 1;
       const bool last = (l == L - 1);

@@ -245,17 +245,21 @@ FFCA_DEV void matmul_nh(const double2 (&A)[I][I], const double2 (&B)[I][I], doub
 // Cyclic complex Jacobi on a Hermitian matrix (full storage). On exit A is
 // diagonal (eigenvalues on the diagonal, real parts) and V holds the
 // eigenvectors in its columns: A_in = V diag(A_out) V^H.
+// Returns false when kJacobiSweeps sweeps did not converge (LAPACK's heevd
+// reports that as "Eigenvalues did not converge"; a NaN input stops at once
+// and is caught by the callers' finiteness / definiteness tests).
+constexpr int kJacobiSweeps = 30;
 template <int I>
-FFCA_DEV void jacobi_herm(double2 (&A)[I][I], double2 (&V)[I][I]) {
+FFCA_DEV bool jacobi_herm(double2 (&A)[I][I], double2 (&V)[I][I]) {
   set_identity<I>(V);
-  if (I == 1) return;
+  if (I == 1) return true;
   // Rotate (p, q) only while |a_pq| exceeds eps * sqrt(|a_pp a_qq|) (the
   // Demmel-Veselic threshold: every eigenvalue then carries high relative
   // accuracy); stop after a sweep without rotations. A fixed "off(A) < tiny"
   // test would never trigger: rotations keep re-creating roundoff-level
   // off-diagonal entries.
   constexpr double kTol2 = FFCA_JACOBI_TOL2;
-  for (int sweep = 0; sweep < 30; ++sweep) {
+  for (int sweep = 0; sweep < kJacobiSweeps; ++sweep) {
     bool rotated = false;
 #pragma unroll
     for (int p = 0; p < I - 1; ++p) {
@@ -311,8 +315,9 @@ FFCA_DEV void jacobi_herm(double2 (&A)[I][I], double2 (&V)[I][I]) {
         }
       }
     }
-    if (!rotated) break;  // converged (NaN input also stops: comparisons fail)
+    if (!rotated) return true;  // converged (NaN input also stops: comparisons fail)
   }
+  return false;
 }
 
 // Sort eigenpairs descending (stable for equal keys is not needed).
@@ -380,7 +385,7 @@ FFCA_DEV int gevd_hpd_eig(const double2 (&Phi)[I][I], const double2 (&Psi)[I][I]
     for (int b = 0; b < I; ++b) A[a][b] = (a > b) ? Psi[a][b] : (a == b ? cmk(Psi[a][a].x, 0.0) : cconj(Psi[b][a]));
   }
   double2 U[I][I];
-  jacobi_herm<I>(A, U);
+  if (!jacobi_herm<I>(A, U)) return FFCA_ERR_NO_CONVERGENCE;
   double sig[I];
   double smin = 1e308;
 #pragma unroll
@@ -413,7 +418,7 @@ FFCA_DEV int gevd_hpd_eig(const double2 (&Phi)[I][I], const double2 (&Psi)[I][I]
     }
   }
   double2 Q[I][I];
-  jacobi_herm<I>(W, Q);
+  if (!jacobi_herm<I>(W, Q)) return FFCA_ERR_NO_CONVERGENCE;
 #pragma unroll
   for (int a = 0; a < I; ++a) lam[a] = W[a][a].x;
   sort_desc<I>(lam, Q);
@@ -492,7 +497,7 @@ FFCA_DEV int gevd_hpd(const double2 (&Phi)[I][I], const double2 (&Psi)[I][I], do
     for (int b = a + 1; b < I; ++b) Wh[b][a] = cconj(Wh[a][b]);
   }
   double2 Q[I][I];
-  jacobi_herm<I>(Wh, Q);
+  if (!jacobi_herm<I>(Wh, Q)) return FFCA_ERR_NO_CONVERGENCE;
 #pragma unroll
   for (int a = 0; a < I; ++a) lam[a] = Wh[a][a].x;
   sort_desc<I>(lam, Q);

@@ -139,21 +139,25 @@ FFCA_DEV void row_matmul(const BinView<I>& v, int A, int B, int Cm, int r) {
 // then row owners apply the column updates and column owners the row
 // updates. Demmel-Veselic threshold; sweeps continue while any bin of the
 // warp rotates. `act` predicates the bin's lanes (warp-synchronous).
+// Returns false (on every lane of the warp) when kJacobiSweeps sweeps left a
+// rotation pending in some bin of the warp whose `act` lanes are still rotating
+// (reported by the callers as FFCA_ERR_NO_CONVERGENCE for those bins).
 template <int I>
-FFCA_DEV void par_jacobi(const BinView<I>& v, int M, int V, int r, bool act) {
+FFCA_DEV bool par_jacobi(const BinView<I>& v, int M, int V, int r, bool act) {
   using Lay = ParLayout<I>;
   if (act) {
 #pragma unroll
     for (int c = 0; c < I; ++c) v.at(V, r, c) = cmk(r == c ? 1.0 : 0.0, 0.0);
   }
   __syncwarp();
-  if (I == 1) return;
+  if (I == 1) return true;
   constexpr int n_rounds = (I % 2 == 0) ? I - 1 : I;
   constexpr double kTol2 = FFCA_JACOBI_TOL2;
   double* rot = v.scal;  // [NPAIR][6]: c, s, emi.x, emi.y, -, flag
+  bool rotated = false;
 #pragma unroll 1
-  for (int sweep = 0; sweep < 30; ++sweep) {
-    bool rotated = false;
+  for (int sweep = 0; sweep < kJacobiSweeps; ++sweep) {
+    rotated = false;
 #pragma unroll 1
     for (int k = 0; k < n_rounds; ++k) {
       if (r < Lay::NPAIR) rot[6 * r + 5] = 0.0;
@@ -242,8 +246,9 @@ FFCA_DEV void par_jacobi(const BinView<I>& v, int M, int V, int r, bool act) {
       for (int c = 0; c < r; ++c) v.at(M, r, c) = cconj(v.at(M, c, r));
     }
     __syncwarp();
-    if (!__any_sync(0xffffffffu, rotated)) break;
+    if (!__any_sync(0xffffffffu, rotated)) return true;
   }
+  return !group_any<Lay::LB>(rotated);  // this bin's verdict (its lanes agree)
 }
 
 // Parallel Hermitian-definite GEVD of (Phi = S1, Psi = S2) in the bin's smem.
@@ -333,10 +338,11 @@ FFCA_DEV int par_gevd(const BinView<I>& v, int r, bool own, double* min_sigma) {
     if (fb && own)
       for (int c = 0; c < I; ++c) v.at(kA, r, c) = v.at(kS2, r, c);
     __syncwarp();
-    par_jacobi<I>(v, kA, kV, r, fb && own);
+    const bool conv_b = par_jacobi<I>(v, kA, kV, r, fb && own);
     smin = 1e308;
     for (int a = 0; a < I; ++a) smin = fmin(smin, v.at(kA, a, a).x);
-    if (fb && !(smin > thr)) rc = FFCA_ERR_DEFINITENESS;
+    if (fb && !conv_b) rc = FFCA_ERR_NO_CONVERGENCE;
+    else if (fb && !(smin > thr)) rc = FFCA_ERR_DEFINITENESS;
     const bool go = fb && own && rc == FFCA_OK;
     if (go) {  // B = U diag(sig^-1/2) -> kX
       for (int c = 0; c < I; ++c) v.at(kX, r, c) = cscale(v.at(kV, r, c), 1.0 / sqrt(v.at(kA, c, c).x));
@@ -365,7 +371,7 @@ FFCA_DEV int par_gevd(const BinView<I>& v, int r, bool own, double* min_sigma) {
   }
   const bool act = own && rc == FFCA_OK;
   // ---- eig(Wh): Jacobi into kV ----
-  par_jacobi<I>(v, kS2, kV, r, act);
+  if (!par_jacobi<I>(v, kS2, kV, r, act) && act) rc = FFCA_ERR_NO_CONVERGENCE;
   // ---- sort descending: Qs[r][rank(c)] = V[r][c] (kX free? no: B) -> use kA as staging ----
   if (act) {
     for (int c = 0; c < I; ++c) v.at(kA, r, c) = v.at(kV, r, c);

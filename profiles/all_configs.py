@@ -19,6 +19,7 @@ import torch  # noqa: E402
 
 from bench import make_inputs, shard  # noqa: E402
 from paper_1805_06572_b200._engine import plan_chunks, run_device, status_of, torch_types  # noqa: E402
+from paper_1805_06572_b200.sharding import shard_chunk_frames  # noqa: E402
 from paper_1805_06572_b200.synth import CONFIGS  # noqa: E402
 
 
@@ -29,7 +30,8 @@ def measure(cfg, engine, dtype, steps, Y, V, S, FL, graph=False):
     s = torch.from_numpy(S).cuda()
     fl = torch.from_numpy(FL).cuda()
     M, N, F, I = Y.shape
-    cf, nc = plan_chunks(M * F, N, I, dtype, engine)
+    cf = shard_chunk_frames(cfg.M, cfg.N, cfg.F, cfg.I, dtype, engine)
+    nc = (N + cf - 1) // cf
     bufs = {"images": torch.empty((M, 2, N, F, I), dtype=ctype, device="cuda"),
             "S": torch.empty((M, 2, F, I, I), dtype=torch.complex128, device="cuda"),
             "v": torch.empty_like(v)}

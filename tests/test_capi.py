@@ -130,3 +130,22 @@ def test_run_args_offsets_match_the_header(tmp_path):
                                           check=True).stdout.split()]
     assert got[0] == ctypes.sizeof(_lib.RunArgs)
     assert got[1:] == [getattr(_lib.RunArgs, n).offset for n in names]
+
+
+def test_status_codes_match_the_header():
+    """Every FFCA_* integer constant the header defines has the same value in
+    the ctypes layer (status codes, dtypes, flags)."""
+    import re
+
+    from paper_1805_06572_b200 import _lib
+
+    text = (REPO / "include" / "fastfca_b200.h").read_text()
+    found = 0
+    for name, val in re.findall(r"#define\s+(FFCA_\w+)\s+\(?(0x[0-9a-fA-F]+|\d+)u?\)?", text):
+        py = getattr(_lib, name, None)
+        if py is None:
+            py = getattr(_lib, name.replace("FFCA_", "", 1), None)
+        assert py is not None, f"{name} missing from _lib"
+        assert py == int(val, 0), (name, py, val)
+        found += 1
+    assert found >= 10
