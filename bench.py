@@ -282,14 +282,15 @@ def main():
     from paper_1805_06572_b200.sharding import grid_model, plan_shard, shard_chunk_frames
 
     if args.scaling == "strong":
-        cf = shard_chunk_frames(cfg.M, cfg.N, cfg.F, cfg.I, args.dtype, args.engine)
+        cf = shard_chunk_frames(cfg.M, cfg.N, cfg.F, cfg.I, args.dtype, args.engine, max_world=cfg.max_world)
     else:
         cf, _ = plan_chunks(cfg.M * cfg.F, cfg.N, cfg.I, args.dtype, args.engine)
     G_rank = M * F
-    sh8 = plan_shard(cfg.M, cfg.F, 0, 8)
+    sh8 = plan_shard(cfg.M, cfg.F, 0, cfg.max_world)
     grid = {"chunk_frames": cf, "this_rank": grid_model(G_rank, N, I, cf, args.dtype, args.engine),
-            "rank0_at_8_gpus": grid_model(sh8.size * (cfg.F if sh8.axis == "mixtures" else 1),
-                                          N, I, cf, args.dtype, args.engine)}
+            f"rank0_at_{cfg.max_world}_gpus": grid_model(
+                sh8.size * (cfg.F if sh8.axis == "mixtures" else 1), N, I, cf, args.dtype,
+                args.engine)}
     tf_it_rank = M * F * N * L
     # whole-job units: all ranks' mixtures (weak) or the one sharded batch (strong)
     tf_it_total = cfg.M * cfg.F * cfg.N * L * (world if args.scaling == "weak" else 1)
@@ -478,7 +479,7 @@ def main():
     other = "fca" if args.engine == "fast" else "fast"
     other_line = None
     if not args.no_other:
-        ocf = (shard_chunk_frames(cfg.M, cfg.N, cfg.F, cfg.I, args.dtype, other)
+        ocf = (shard_chunk_frames(cfg.M, cfg.N, cfg.F, cfg.I, args.dtype, other, max_world=cfg.max_world)
                if args.scaling == "strong" else
                plan_chunks(cfg.M * cfg.F, cfg.N, cfg.I, args.dtype, other)[0])
         obufs = {"images": bufs["images"], "S": bufs["S"], "v": bufs["v"]}

@@ -308,6 +308,12 @@ struct Fast2Smem {
   static constexpr size_t BYTES = MAIN > RED ? MAIN : RED;
 };
 
+#ifndef FFCA_K3_RING_FIRST
+#define FFCA_K3_RING_FIRST 0  // 1: issue the frame ring before loading the P tile
+#endif
+#ifndef FFCA_K3_PCOAL
+#define FFCA_K3_PCOAL 1  // coalesced copy of the tile's P / W blocks into shared memory
+#endif
 #ifndef FAST2_MINB
 #define FAST2_MINB 3  // CTAs per SM the update pass is register-budgeted for
 #endif
@@ -360,27 +366,8 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
   const int64_t NF = p.N * p.F;
   R* vb = (R*)p.v + m * 2 * NF + f;  // no __restrict__: may alias vr (in place)
   const R* vr = (p.v_src ? (const R*)p.v_src : (const R*)p.v) + m * 2 * NF + f;
-
-  // P lives in shared memory (bin-minor SoA after the frame ring): the 4
-  // warps of the CTA work on the same 32 bins, so one 16*I*I-byte column per
-  // lane serves all of them and frees the registers for the accumulators.
   constexpr bool kSacc = SmemAcc<I, R, UPDATE, LL, MU>::value;
   using Sm = Fast2Smem<I, R, WARPS, STAGES, MU, kSacc>;
-  T2* sP = (T2*)(smem_raw + Sm::RING);
-  for (int e = warp; e < NP; e += WARPS) sP[e * 32 + lane] = Math<R>::c2(p.P[g * NP + e]);
-  // W = P^{-H} for the image write (last pass only), same bin-minor tile layout
-  T2* sW = sP + NP * 32;
-  if (MU && p.mu_back)
-    for (int e = warp; e < NP; e += WARPS) sW[e * 32 + lane] = Math<R>::c2(p.W[g * NP + e]);
-  __syncthreads();
-  T lam[I], il[I];  // il = 1 / (I lam): the 1/I of v1 = tr1 / I folded in
-#pragma unroll
-  for (int a = 0; a < I; ++a) {
-    lam[a] = (T)p.lam[g * I + a];
-    il[a] = (T)(1.0 / ((double)I * p.lam[g * I + a]));
-  }
-  const T fl = (T)p.floor[g];
-  constexpr T invI = T(1) / I;
 
   double acc[2][kSacc ? 1 : NP];  // (kSacc: in shared memory, accS)
   // accS[(j NP + e) * WARPS * 32 + tid]: thread-minor, conflict-free
@@ -511,14 +498,70 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
     vnext += vstep;
   };
 
+  // P lives in shared memory (bin-minor SoA after the frame ring): the 4
+  // warps of the CTA work on the same 32 bins, so one 16*I*I-byte column per
+  // lane serves all of them and frees the registers for the accumulators.
+  T2* sP = (T2*)(smem_raw + Sm::RING);
+  // W = P^{-H} for the image write (last pass only), same bin-minor tile layout
+  T2* sW = sP + NP * 32;
+  auto load_tile = [&]() {
+    if (FFCA_K3_PCOAL) {
+      // the tile's P block (32 consecutive bins x NP entries) is one
+      // contiguous run: thread t copies 16-B units t, t + 128, ... (bin
+      // b = u / NP of the tile, clamped like g; entry e = u % NP)
+      for (int u = threadIdx.x; u < 32 * NP; u += WARPS * 32) {
+        const int b = u / NP, e = u - (u / NP) * NP;
+        int64_t gb = tile0 + b;
+        if (gb >= G) gb = G - 1;
+        sP[e * 32 + b] = Math<R>::c2(p.P[gb * NP + e]);
+        if (MU && p.mu_back) sW[e * 32 + b] = Math<R>::c2(p.W[gb * NP + e]);
+      }
+    } else {
+      for (int e = warp; e < NP; e += WARPS) sP[e * 32 + lane] = Math<R>::c2(p.P[g * NP + e]);
+      if (MU && p.mu_back)
+        for (int e = warp; e < NP; e += WARPS) sW[e * 32 + lane] = Math<R>::c2(p.W[g * NP + e]);
+    }
+    __syncthreads();
+  };
+  if (!FFCA_K3_RING_FIRST) load_tile();
   constexpr int kAhead = STAGES - 1;  // frames issued ahead
 #pragma unroll
   for (int s = 0; s < kAhead; ++s) {
     if (s < K) issue(s);
     cp_async_commit();
   }
+  if (FFCA_K3_RING_FIRST) load_tile();
+  T lam[I], il[I];  // il = 1 / (I lam): the 1/I of v1 = tr1 / I folded in
+#pragma unroll
+  for (int a = 0; a < I; ++a) {
+    lam[a] = (T)p.lam[g * I + a];
+    il[a] = (T)(1.0 / ((double)I * p.lam[g * I + a]));
+  }
+  const T fl = (T)p.floor[g];
+  constexpr T invI = T(1) / I;
 
   R* vwrite = vb + nfirst * p.F;  // v of the frame being processed (advanced per frame)
+  const unsigned char* cur_slot = wslots;  // ring stage of the frame being processed
+  // image rows (MU): byte offset of (mixture, bin) = tile0's row at source 0,
+  // frame 0, and per store copy c the correction of a tile across a mixture
+  // boundary (as ycorr) and whether its bin exists
+  int64_t mrow0 = 0;
+  int64_t mcorr[MU ? Slot::Q : 1];
+  bool mvalid[MU ? Slot::Q : 1];
+  if constexpr (MU) {
+    const int64_t m0 = tile0 / p.F, f0 = tile0 - m0 * p.F;
+    mrow0 = (m0 * 2 * NF + f0) * Slot::YB;
+#pragma unroll
+    for (int c = 0; c < Slot::Q; ++c) {
+      const int u = 32 * c + lane, b = u / Slot::Q, a = u % Slot::Q;
+      int64_t gb = tile0 + b;
+      mvalid[c] = gb < G;
+      if (gb >= G) gb = G - 1;
+      const int64_t mb = gb / p.F, fb = gb - mb * p.F;
+      mcorr[c] = contiguous ? 0 : (mb * 2 * NF + fb) * Slot::YB + a * Slot::UB - mrow0 -
+                                      (int64_t)u * Slot::UB;
+    }
+  }
   // per-frame E+M body once z = P^H y is known
   auto frame = [&](int k, int64_t n, const T2 (&yv)[I], T v1, T v2, const T2 (&z)[I]) {
     T g1[I], g2[I], t1[I], t2[I];
@@ -653,10 +696,9 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
       if (kBlk && ((k % kF32Block) == kF32Block - 1)) flush();
       }
     }
-    if (MU && active) {
-      C* mo = (C*)p.mu_out;
-      C* d1 = mo + (((m * 2 + 0) * p.N + n) * p.F + f) * I;
-      C* d2 = mo + (((m * 2 + 1) * p.N + n) * p.F + f) * I;
+    if constexpr (MU) {
+      // posterior means of this frame, both sources
+      C o[2][I];
       if (p.mu_back) {
         // images (fast.py:133-141): mu_1 = P^{-H} (g1 z); mu_2 = y - mu_1, the
         // posterior partition mu_1 + mu_2 = y (g1 + g2 = 1, P^{-H} P^H = I),
@@ -671,24 +713,52 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
             sx = fma(w.x, mx, fma(-w.y, my, sx));
             sy = fma(w.x, my, fma(w.y, mx, sy));
           }
-          C o1, o2;
-          o1.x = sx;
-          o1.y = sy;
-          o2.x = yv[a].x - sx;
-          o2.y = yv[a].y - sy;
-          d1[a] = o1;
-          d2[a] = o2;
+          o[0][a].x = sx;
+          o[0][a].y = sy;
+          o[1][a].x = yv[a].x - sx;
+          o[1][a].y = yv[a].y - sy;
         }
       } else {
 #pragma unroll
         for (int a = 0; a < I; ++a) {
-          C o1, o2;
-          o1.x = z[a].x * g1[a];
-          o1.y = z[a].y * g1[a];
-          o2.x = z[a].x * g2[a];
-          o2.y = z[a].y * g2[a];
-          d1[a] = o1;
-          d2[a] = o2;
+          o[0][a].x = z[a].x * g1[a];
+          o[0][a].y = z[a].y * g1[a];
+          o[1][a].x = z[a].x * g2[a];
+          o[1][a].y = z[a].y * g2[a];
+        }
+      }
+      // Write through the consumed ring stage (free until the next
+      // iteration's issue refills it): every lane puts its bin's row in the
+      // ring's swizzled slot layout, then copy c of lane l stores unit
+      // 32 c + l of the warp's 32-bin row — one contiguous 32*UB-byte run per
+      // store instruction instead of a 64-B lane stride (which wrote half
+      // sectors: 2x the L2 store traffic of the image pass).
+      unsigned char* sl = (unsigned char*)cur_slot;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        __syncwarp();  // (j = 0: all lanes read their y; j = 1: source 1 stored)
+#pragma unroll
+        for (int a = 0; a < Slot::Q; ++a) {
+          unsigned char* d = sl + Slot::pos(lane, a);
+          if constexpr (sizeof(C) == 16)
+            *(double2*)d = *(const double2*)&o[j][a];
+          else if constexpr (Slot::UB == 16)
+            *(float4*)d = make_float4(o[j][2 * a].x, o[j][2 * a].y, o[j][2 * a + 1].x,
+                                      o[j][2 * a + 1].y);
+          else
+            *(C*)d = o[j][a];
+        }
+        __syncwarp();
+        unsigned char* row = (unsigned char*)p.mu_out + mrow0 + (j * NF + n * p.F) * Slot::YB;
+#pragma unroll
+        for (int c = 0; c < Slot::Q; ++c) {
+          if (!mvalid[c]) continue;
+          unsigned char* dst = row + (32 * c + lane) * Slot::UB + (contiguous ? 0 : mcorr[c]);
+          const unsigned char* src = sl + spos0 + 32 * c * Slot::UB;
+          if constexpr (Slot::UB == 16)
+            *(uint4*)dst = *(const uint4*)src;
+          else
+            *(uint2*)dst = *(const uint2*)src;
         }
       }
     }
@@ -696,6 +766,7 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
   };
   auto load_frame = [&](int k, T2 (&yv)[I], T& v1, T& v2) {
     const unsigned char* slot = wslots + read_stage;
+    cur_slot = slot;
     read_stage = (read_stage + (int)kStageStride == STAGES * (int)kStageStride)
                      ? 0 : read_stage + (int)kStageStride;
     constexpr int PER = Slot::UB / (int)sizeof(T2);  // channels per unit

@@ -26,6 +26,9 @@ namespace ffca {
 #ifndef FFCA_FCA_STAGES
 #define FFCA_FCA_STAGES 4  // frame ring depth of the FCA pass
 #endif
+#ifndef FFCA_K4_RING_FIRST
+#define FFCA_K4_RING_FIRST 0  // 1: issue the frame ring before loading S1, S2
+#endif
 #ifndef FFCA_FCA_MINB
 #define FFCA_FCA_MINB 1  // CTAs per SM the I <= 4 pass is register-budgeted for
 #endif
@@ -50,8 +53,11 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
   if (!active) g = G - 1;
   const int64_t m = g / p.F;
   const int64_t f = g - m * p.F;
-  for (int e = warp; e < 2 * NP; e += WARPS) sS[e * 32 + lane] = p.Sp[(size_t)e * G + g];
-  __syncthreads();
+  auto load_tile = [&]() {  // S1, S2 of the tile (packed, bin-minor)
+    for (int e = warp; e < 2 * NP; e += WARPS) sS[e * 32 + lane] = p.Sp[(size_t)e * G + g];
+    __syncthreads();
+  };
+  if (!FFCA_K4_RING_FIRST) load_tile();
   const int64_t n0 = (int64_t)blockIdx.y * p.chunk_frames;
   const int64_t n1 = min(p.N, n0 + p.chunk_frames);
   const int64_t NF = p.N * p.F;
@@ -69,6 +75,7 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
     if (s < K) ring.issue();
     cp_async_commit();
   }
+  if (FFCA_K4_RING_FIRST) load_tile();  // (S1, S2 after the ring prologue)
 
   auto Sget = [&](int which, int a, int b) -> double2 {
     // full entry (a, b) of packed Hermitian matrix `which`

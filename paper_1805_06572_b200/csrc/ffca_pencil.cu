@@ -141,8 +141,11 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
   return true;
 }
 
+#ifndef FFCA_K1_MINB
+#define FFCA_K1_MINB 1  // CTAs of 64 per SM the one-thread-per-bin refresh is budgeted for
+#endif
 template <int I>
-__global__ void __launch_bounds__(64) pencil_update_kernel(const PencilParams p) {
+__global__ void __launch_bounds__(64, FFCA_K1_MINB) pencil_update_kernel(const PencilParams p) {
   constexpr int NP = I * I;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= p.G) return;

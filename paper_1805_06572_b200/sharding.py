@@ -129,17 +129,41 @@ def gather_results(local, shard, group=None, dst=0):
 MAX_WORLD = 8  # one node of B200s
 
 
+def _plan_cost(G, N, I, cf, dtype, algorithm):
+    """The drivers' modelled makespan of one streaming pass (ffca_fast.cu
+    plan_chunks): waves x (frames per chunk + per-CTA overhead)."""
+    gm = grid_model(G, N, I, cf, dtype, algorithm)
+    waves = -(-gm["ctas"] // max(gm["slots"], 1))
+    return waves * (min(cf, N) + 24)
+
+
 def shard_chunk_frames(M, N, F, I, dtype="c128", algorithm="fast", max_world=MAX_WORLD):
-    """The frame chunking every world size uses: the auto plan of the
-    largest shard at ``max_world`` ranks (rank 0's), which fills one GPU at
-    that world size. Equal chunking at every N => bitwise-equal per-bin
-    results (the per-bin reduction order depends on the chunking only)."""
+    """The frame chunking every world size 1..``max_world`` uses.
+
+    Equal chunking at every N => bitwise-equal per-bin results (the per-bin
+    reduction order depends on the chunking only). The plan is the one whose
+    worst relative modelled cost over the world sizes 1, 2, 4, ..,
+    ``max_world`` (rank 0's shard, the largest) is smallest: a plan tuned
+    for the 8-GPU shard alone can cost a 1-GPU run >10% (FCA at config 3:
+    56 waves of short chunks instead of 7 of whole-mixture chunks)."""
     from ._engine import plan_chunks
 
-    sh = plan_shard(M, F, 0, max_world)
-    G = sh.size * F if sh.axis == "mixtures" else sh.size
-    cf, _ = plan_chunks(G, N, I, dtype, algorithm)
-    return cf
+    def shard_bins(w):
+        sh = plan_shard(M, F, 0, w)
+        return sh.size * F if sh.axis == "mixtures" else sh.size
+
+    if max_world <= 1:
+        return plan_chunks(M * F, N, I, dtype, algorithm)[0]
+    worlds = sorted({w for w in (1, 2, 4, 8, 16, 32, 64) if w <= max_world} | {max_world})
+    min_frames = 16 if I >= 5 else 32
+    max_nc = max(1, min(4096, -(-N // min_frames)))
+    cands = sorted({-(-N // nc) for nc in range(1, max_nc + 1)}, reverse=True)
+    costs = {w: [_plan_cost(shard_bins(w), N, I, cf, dtype, algorithm) for cf in cands]
+             for w in worlds}
+    best = {w: min(c) for w, c in costs.items()}
+    score = [max(costs[w][i] / best[w] for w in worlds) for i in range(len(cands))]
+    i = min(range(len(cands)), key=lambda k: (round(score[k], 9), -cands[k]))
+    return cands[i]
 
 
 def grid_model(G, N, I, chunk_frames, dtype="c128", algorithm="fast"):

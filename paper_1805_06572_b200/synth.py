@@ -55,6 +55,14 @@ class Config:
     def tf_bins(self):
         return self.M * self.F * self.N
 
+    @property
+    def max_world(self):
+        """GPUs the config is sharded over (BASELINE.json: config 3 by mixture
+        and config 4 by bin across 1/2/4/8 GPUs; configs 0-2 are 1-GPU
+        configs). The one chunk plan of every world size is the plan of the
+        shard at this world size."""
+        return 8 if self.index in (3, 4) else 1
+
 
 CONFIGS = {
     0: Config(0, 1, 2, 257, 500, 10, 2, 1e-3, 1.5, False, ("c128",),

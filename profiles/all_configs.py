@@ -30,7 +30,7 @@ def measure(cfg, engine, dtype, steps, Y, V, S, FL, graph=False):
     s = torch.from_numpy(S).cuda()
     fl = torch.from_numpy(FL).cuda()
     M, N, F, I = Y.shape
-    cf = shard_chunk_frames(cfg.M, cfg.N, cfg.F, cfg.I, dtype, engine)
+    cf = shard_chunk_frames(cfg.M, cfg.N, cfg.F, cfg.I, dtype, engine, max_world=cfg.max_world)
     nc = (N + cf - 1) // cf
     bufs = {"images": torch.empty((M, 2, N, F, I), dtype=ctype, device="cuda"),
             "S": torch.empty((M, 2, F, I, I), dtype=torch.complex128, device="cuda"),

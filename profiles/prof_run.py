@@ -39,7 +39,7 @@ def main():
     v = torch.from_numpy(V).cuda().to(rtype)
     s = torch.from_numpy(S).cuda()
     fl = torch.from_numpy(FL).cuda()
-    cf = shard_chunk_frames(cfg.M, cfg.N, cfg.F, cfg.I, a.dtype, a.engine)
+    cf = shard_chunk_frames(cfg.M, cfg.N, cfg.F, cfg.I, a.dtype, a.engine, max_world=cfg.max_world)
     r = run_device(a.engine, y, v, s, fl, a.iters, likelihood=a.likelihood, check=False,
                    chunk_frames=cf, dtype=a.dtype, timing=False)
     status_of(r)
