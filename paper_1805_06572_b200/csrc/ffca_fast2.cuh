@@ -267,8 +267,10 @@ struct FrameRing {
     vnext += vstep;
   }
   // this lane's bin of the next stage, widened to complex128 / float64
+  unsigned char* cur = nullptr;  // stage of the frame last loaded (free until the next issue)
   FFCA_DEV void load(double2 (&yv)[I], double& v1, double& v2) {
     const unsigned char* slot = wslots + read_stage;
+    cur = wslots + read_stage;
     read_stage = read_stage + kStride == STAGES * kStride ? 0 : read_stage + kStride;
     constexpr int PER = Slot::UB / (int)sizeof(C);
 #pragma unroll
@@ -285,6 +287,78 @@ struct FrameRing {
     const unsigned char* vs = slot + 32 * Slot::YB;
     v1 = (double)((const R*)vs)[lane];
     v2 = (double)((const R*)(vs + 32 * sizeof(R)))[lane];
+  }
+};
+
+// Warp-cooperative store of one frame's posterior means (images) of the
+// warp's 32 bins, (M,2,N,F,I) layout, through a ring stage the warp has
+// consumed (free until the next issue refills it): every lane puts its bin's
+// row in the ring's swizzled slot layout, then copy c of lane l stores unit
+// 32 c + l of the 32-bin row — one contiguous 32*UB-byte run per store
+// instruction instead of a lane stride of I*sizeof(C) bytes, which writes
+// half sectors (2x the L2 store traffic of the image pass; ncu: 50% of the
+// image pass's global store sectors excessive).
+template <int I, typename R>
+struct ImageRowStore {
+  using Slot = RingSlot<I, R>;
+  using C = typename CplxOf<R>::type;
+  int64_t row0;              // byte offset of tile0's row at source 0, frame 0
+  int64_t corr[Slot::Q];     // per-copy correction of a tile across a mixture boundary
+  bool valid[Slot::Q];       // the copy's bin exists
+  int64_t NF, F;
+  int spos0, lane;
+  bool contiguous;
+
+  FFCA_DEV void init(int64_t tile0, int64_t G, int64_t N, int64_t F_, int lane_) {
+    lane = lane_;
+    F = F_;
+    NF = N * F_;
+    contiguous = (tile0 + 31 < G) && (tile0 / F_ == (tile0 + 31) / F_);
+    spos0 = Slot::pos(lane / Slot::Q, lane % Slot::Q);
+    const int64_t m0 = tile0 / F_, f0 = tile0 - m0 * F_;
+    row0 = (m0 * 2 * NF + f0) * Slot::YB;
+#pragma unroll
+    for (int c = 0; c < Slot::Q; ++c) {
+      const int u = 32 * c + lane, b = u / Slot::Q, a = u % Slot::Q;
+      int64_t gb = tile0 + b;
+      valid[c] = gb < G;
+      if (gb >= G) gb = G - 1;
+      const int64_t mb = gb / F_, fb = gb - mb * F_;
+      corr[c] = contiguous ? 0 : (mb * 2 * NF + fb) * Slot::YB + a * Slot::UB - row0 -
+                                     (int64_t)u * Slot::UB;
+    }
+  }
+  // o[j][a]: source j, channel a of this lane's bin at frame n; `slot` the
+  // consumed stage. Warp-synchronous (all lanes call it).
+  template <typename CC>
+  FFCA_DEV void store(void* mu_out, unsigned char* slot, int64_t n, const CC (&o)[2][I]) const {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      __syncwarp();  // (j = 0: every lane read the stage; j = 1: source 1 stored)
+#pragma unroll
+      for (int a = 0; a < Slot::Q; ++a) {
+        unsigned char* d = slot + Slot::pos(lane, a);
+        if constexpr (sizeof(C) == 16)
+          *(double2*)d = make_double2((double)o[j][a].x, (double)o[j][a].y);
+        else if constexpr (Slot::UB == 16)
+          *(float4*)d = make_float4((float)o[j][2 * a].x, (float)o[j][2 * a].y,
+                                    (float)o[j][2 * a + 1].x, (float)o[j][2 * a + 1].y);
+        else
+          *(float2*)d = make_float2((float)o[j][a].x, (float)o[j][a].y);
+      }
+      __syncwarp();
+      unsigned char* row = (unsigned char*)mu_out + row0 + (j * NF + n * F) * Slot::YB;
+#pragma unroll
+      for (int c = 0; c < Slot::Q; ++c) {
+        if (!valid[c]) continue;
+        unsigned char* dst = row + (32 * c + lane) * Slot::UB + (contiguous ? 0 : corr[c]);
+        const unsigned char* src = slot + spos0 + 32 * c * Slot::UB;
+        if constexpr (Slot::UB == 16)
+          *(uint4*)dst = *(const uint4*)src;
+        else
+          *(uint2*)dst = *(const uint2*)src;
+      }
+    }
   }
 };
 
@@ -542,26 +616,8 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
 
   R* vwrite = vb + nfirst * p.F;  // v of the frame being processed (advanced per frame)
   const unsigned char* cur_slot = wslots;  // ring stage of the frame being processed
-  // image rows (MU): byte offset of (mixture, bin) = tile0's row at source 0,
-  // frame 0, and per store copy c the correction of a tile across a mixture
-  // boundary (as ycorr) and whether its bin exists
-  int64_t mrow0 = 0;
-  int64_t mcorr[MU ? Slot::Q : 1];
-  bool mvalid[MU ? Slot::Q : 1];
-  if constexpr (MU) {
-    const int64_t m0 = tile0 / p.F, f0 = tile0 - m0 * p.F;
-    mrow0 = (m0 * 2 * NF + f0) * Slot::YB;
-#pragma unroll
-    for (int c = 0; c < Slot::Q; ++c) {
-      const int u = 32 * c + lane, b = u / Slot::Q, a = u % Slot::Q;
-      int64_t gb = tile0 + b;
-      mvalid[c] = gb < G;
-      if (gb >= G) gb = G - 1;
-      const int64_t mb = gb / p.F, fb = gb - mb * p.F;
-      mcorr[c] = contiguous ? 0 : (mb * 2 * NF + fb) * Slot::YB + a * Slot::UB - mrow0 -
-                                      (int64_t)u * Slot::UB;
-    }
-  }
+  ImageRowStore<I, R> img;  // image rows (MU pass)
+  if constexpr (MU) img.init(tile0, G, p.N, p.F, lane);
   // per-frame E+M body once z = P^H y is known
   auto frame = [&](int k, int64_t n, const T2 (&yv)[I], T v1, T v2, const T2 (&z)[I]) {
     T g1[I], g2[I], t1[I], t2[I];
@@ -727,40 +783,7 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
           o[1][a].y = z[a].y * g2[a];
         }
       }
-      // Write through the consumed ring stage (free until the next
-      // iteration's issue refills it): every lane puts its bin's row in the
-      // ring's swizzled slot layout, then copy c of lane l stores unit
-      // 32 c + l of the warp's 32-bin row — one contiguous 32*UB-byte run per
-      // store instruction instead of a 64-B lane stride (which wrote half
-      // sectors: 2x the L2 store traffic of the image pass).
-      unsigned char* sl = (unsigned char*)cur_slot;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        __syncwarp();  // (j = 0: all lanes read their y; j = 1: source 1 stored)
-#pragma unroll
-        for (int a = 0; a < Slot::Q; ++a) {
-          unsigned char* d = sl + Slot::pos(lane, a);
-          if constexpr (sizeof(C) == 16)
-            *(double2*)d = *(const double2*)&o[j][a];
-          else if constexpr (Slot::UB == 16)
-            *(float4*)d = make_float4(o[j][2 * a].x, o[j][2 * a].y, o[j][2 * a + 1].x,
-                                      o[j][2 * a + 1].y);
-          else
-            *(C*)d = o[j][a];
-        }
-        __syncwarp();
-        unsigned char* row = (unsigned char*)p.mu_out + mrow0 + (j * NF + n * p.F) * Slot::YB;
-#pragma unroll
-        for (int c = 0; c < Slot::Q; ++c) {
-          if (!mvalid[c]) continue;
-          unsigned char* dst = row + (32 * c + lane) * Slot::UB + (contiguous ? 0 : mcorr[c]);
-          const unsigned char* src = sl + spos0 + 32 * c * Slot::UB;
-          if constexpr (Slot::UB == 16)
-            *(uint4*)dst = *(const uint4*)src;
-          else
-            *(uint2*)dst = *(const uint2*)src;
-        }
-      }
+      img.store(p.mu_out, (unsigned char*)cur_slot, n, o);
     }
     if (bad && bad_n == 0) bad_n = n + 1;
   };

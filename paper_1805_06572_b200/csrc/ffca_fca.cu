@@ -33,7 +33,11 @@ namespace ffca {
 #define FFCA_FCA_MINB 1  // CTAs per SM the I <= 4 pass is register-budgeted for
 #endif
 
-template <int I, typename R, int WARPS>
+// UPDATE / LL / MU (power + covariance update, likelihood, posterior-mean
+// write) are compile-time variants, so the hot update-only pass carries
+// neither the image nor the likelihood code (register pressure: the fused
+// runtime-branch kernel spilled ~550 B per thread at I = 4).
+template <int I, typename R, int WARPS, bool UPDATE, bool LL, bool MU>
 __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const FcaIterParams p) {
   using C = typename CplxOf<R>::type;
   constexpr int NP = I * I;
@@ -91,7 +95,7 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
 #pragma unroll
     for (int e = 0; e < NP; ++e) acc[j][e] = 0.0;
   double llacc = 0.0;
-  const bool do_ll = p.llbin != nullptr;
+  constexpr bool do_ll = LL;
   int64_t bad_n = 0;
 
   for (int k = 0; k < K; ++k) {
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
       }
       x[a] = s;
     }
-    if (do_ll) {
+    if constexpr (LL) {
       // log det R + y^H R^{-1} y = 2 sum log L_ii + Re(y^H x)
       double prod = 1.0, quad = 0.0;
 #pragma unroll
@@ -164,24 +168,29 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
       }
       llacc += 2.0 * log(prod) + quad;
     }
-    if (p.mu_out != nullptr && active) {
-      // mu_j = v_j S_j x (the posterior means; written by the image pass only)
-      C* mo = (C*)p.mu_out;
-      C* d1 = mo + (((m * 2 + 0) * p.N + n) * p.F + f) * I;
-      C* d2 = mo + (((m * 2 + 1) * p.N + n) * p.F + f) * I;
+    if constexpr (MU) {
+      // mu_j = v_j S_j x (the posterior means; written by the image pass
+      // only). Direct lane-strided stores: at 255 registers the staged
+      // warp-cooperative store (ImageRowStore, as K3) spilled its addressing
+      // and made this pass slower (config 3: 7.0 -> 9.2 ms).
+      if (active) {
+        C* mo = (C*)p.mu_out;
+        C* d1 = mo + (((m * 2 + 0) * p.N + n) * p.F + f) * I;
+        C* d2 = mo + (((m * 2 + 1) * p.N + n) * p.F + f) * I;
 #pragma unroll
-      for (int a = 0; a < I; ++a) {
-        double2 s1 = cmk(0.0, 0.0), s2 = cmk(0.0, 0.0);
+        for (int a = 0; a < I; ++a) {
+          double2 s1 = cmk(0.0, 0.0), s2 = cmk(0.0, 0.0);
 #pragma unroll
-        for (int b = 0; b < I; ++b) {
-          s1 = cmac(s1, Sget(0, a, b), x[b]);
-          s2 = cmac(s2, Sget(1, a, b), x[b]);
+          for (int b = 0; b < I; ++b) {
+            s1 = cmac(s1, Sget(0, a, b), x[b]);
+            s2 = cmac(s2, Sget(1, a, b), x[b]);
+          }
+          d1[a] = from_c128<R>(cscale(s1, v1));
+          d2[a] = from_c128<R>(cscale(s2, v2));
         }
-        d1[a] = from_c128<R>(cscale(s1, v1));
-        d2[a] = from_c128<R>(cscale(s2, v2));
       }
     }
-    if (!p.update) continue;
+    if constexpr (!UPDATE) continue;
     // Phi_j = mu_j mu_j^H + v1 v2 S1 Rinv S2 with mu_j = v_j S_j x, so
     //   sum_n Phi_j / w_j = S_j (sum v_j^2/w_j x x^H) S_j + S1 (sum v1 v2/w_j Rinv) S2:
     // the per-point I x I products of the reference (_kernels_numba.py:290-314)
@@ -241,7 +250,7 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
                  (unsigned long long)((m * p.N + (bad_n - 1)) * p.F + f));
 
   cp_async_wait_all();
-  if (!p.update && !do_ll) return;
+  if constexpr (!UPDATE && !LL) return;
   if (WARPS > 1) {
     __syncthreads();  // ring and sS are dead: the reduction buffer reuses them
     if (warp > 0) {
@@ -266,14 +275,14 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
   }
   if (!active) return;
   const int64_t c = blockIdx.y;
-  if (p.update) {
+  if constexpr (UPDATE) {
     double* sp = p.Spart + (size_t)c * kFcaParts * NP * G + g;
 #pragma unroll
     for (int j = 0; j < kFcaParts; ++j)
 #pragma unroll
       for (int e = 0; e < NP; ++e) sp[(size_t)(j * NP + e) * G] = acc[j][e];
   }
-  if (do_ll) p.llbin[(size_t)c * G + g] = llacc;
+  if constexpr (LL) p.llbin[(size_t)c * G + g] = llacc;
 }
 
 template <int I, typename R>
@@ -284,22 +293,35 @@ constexpr size_t fca_smem_bytes() {
   return ss > red ? ss : red;
 }
 
-template <int I, typename R>
-static cudaError_t launch_fca_em_t(const FcaIterParams& p, cudaStream_t s) {
-  constexpr int NP = I * I;
+template <int I, typename R, bool UPDATE, bool LL, bool MU>
+static cudaError_t launch_fca_em_v(const FcaIterParams& p, cudaStream_t s) {
   const size_t smem = fca_smem_bytes<I, R>();
-  auto kern = fca_em_kernel<I, R, kWarps>;
-  if (cudaError_t e = ensure_smem<fca_em_kernel<I, R, kWarps>>(smem)) return e;
+  auto kern = fca_em_kernel<I, R, kWarps, UPDATE, LL, MU>;
+  if (cudaError_t e = ensure_smem<fca_em_kernel<I, R, kWarps, UPDATE, LL, MU>>(smem)) return e;
   dim3 grid((unsigned)((p.G + 31) / 32), (unsigned)p.nchunk);
   kern<<<grid, kWarps * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 
 template <int I, typename R>
+static cudaError_t launch_fca_em_t(const FcaIterParams& p, cudaStream_t s) {
+  const bool ll = p.llbin != nullptr, mu = p.mu_out != nullptr;
+  if (p.update) {
+    if (!ll && !mu) return launch_fca_em_v<I, R, true, false, false>(p, s);
+    if (ll && !mu) return launch_fca_em_v<I, R, true, true, false>(p, s);
+    if (!ll && mu) return launch_fca_em_v<I, R, true, false, true>(p, s);
+    return launch_fca_em_v<I, R, true, true, true>(p, s);
+  }
+  if (ll && !mu) return launch_fca_em_v<I, R, false, true, false>(p, s);
+  if (!ll && mu) return launch_fca_em_v<I, R, false, false, true>(p, s);
+  if (ll && mu) return launch_fca_em_v<I, R, false, true, true>(p, s);
+  return cudaSuccess;
+}
+
+template <int I, typename R>
 static int fca_bpsm_t() {
-  constexpr int NP = I * I;
   const size_t smem = fca_smem_bytes<I, R>();
-  auto kern = fca_em_kernel<I, R, kWarps>;
+  auto kern = fca_em_kernel<I, R, kWarps, true, false, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int n = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kWarps * 32, smem);

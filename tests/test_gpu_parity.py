@@ -598,3 +598,29 @@ def test_sharded_runs_bitwise_equal_at_every_world_size(M):
             if M == 1:  # bin shards: likelihood partials add up to the full trace
                 tot = sum(p["loglik"] for p in parts)
                 assert torch.allclose(tot, one["loglik"], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("I,dtype", [(2, "c128"), (3, "c128"), (4, "c128"), (4, "c64"), (8, "c128"),
+                                     (8, "c64")])
+def test_runs_are_bitwise_deterministic(I, dtype):
+    """Repeated runs give bitwise identical images, v, S and likelihood
+    (reference acceptance criterion, pkg/tests/test_acceptance.py:263-296).
+    compute-sanitizer is closed on the GPU pool, so this also stands in for
+    racecheck over the shared-memory frame rings, the cross-warp reductions
+    and the staged image stores: a race would show up as run-to-run
+    differences. Sizes give many CTAs, several frame chunks per bin, tiles
+    across mixture boundaries and a partial last tile."""
+    P = _pkg()
+    gen = np.random.default_rng(100 + I)
+    M, N, F = 3, 400, 45
+    y = random_complex(gen, (M, N, F, I))
+    inits = [P.init_random(y[m], 30 + m) for m in range(M)]
+    init = P.SpatialModel(v=np.stack([i.v for i in inits]), S=np.stack([i.S for i in inits]),
+                          v_floor=np.stack([i.v_floor for i in inits]))
+    for run in (P.fastfca_run, P.fca_run):
+        outs = [run(y, init, 3, dtype=dtype) for _ in range(3)]
+        for o in outs[1:]:
+            assert np.array_equal(o.images, outs[0].images), run.__name__
+            assert np.array_equal(o.model.v, outs[0].model.v), run.__name__
+            assert np.array_equal(o.model.S, outs[0].model.S), run.__name__
+            assert np.array_equal(np.asarray(o.loglik_trace), np.asarray(outs[0].loglik_trace))
