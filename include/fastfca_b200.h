@@ -240,6 +240,18 @@ int ffca_stft_analyze(const double* x, double* spec, int64_t batch, int channels
 int ffca_stft_synthesize(const double* spec, double* out, int64_t batch, int channels,
                          int64_t frames, int frame_length, int64_t length, void* stream);
 
+/* ---- separation quality (reference metrics.py) ---------------------------
+ * sdr (metrics.py:27-60, _channel_sdr): for each signal pair p of est, ref
+ * (pairs, length) f64 (device), the least-squares projection of est onto ref
+ * delayed by 0..max_shift samples (max_shift <= 63); sdr_db[p] =
+ * 10 log10(target / max(noise, 1e-30 target)), -300 for a zero projection.
+ * flags[p]: bit 0 = silent reference (MetricError), bit 1 = numerically
+ * rank-deficient delay basis (dependent delays dropped). pairs <= 65535.
+ * Deterministic (fixed-order reductions). */
+size_t ffca_sdr_workspace_size(int64_t pairs, int64_t length, int max_shift);
+int ffca_sdr(const double* est, const double* ref, int64_t pairs, int64_t length, int max_shift,
+             double* sdr_db, int* flags, void* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

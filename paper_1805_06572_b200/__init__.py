@@ -10,17 +10,20 @@ signatures, layouts, return types and exceptions follow the reference
 the STFT front / back end (``stft_analyze`` / ``stft_synthesize``, also on
 the GPU); ``separate`` chains analysis -> init -> EM -> synthesis in HBM.
 ``init_from_masks`` (the direction-clustering initial model) runs on the
-GPU as well. The simulator, metrics, WAV I/O and CLI are out of scope (see
-DESIGN.md).
+GPU as well, and so is the SDR metric (``sdr`` / ``sdr_pairing``) and the
+benchmark sweep's compute (``benchmark_sweep``). The simulator, WAV I/O and
+CLI are out of scope.
 """
 
 from .conventional import e_step, fca_run, log_likelihood, m_step
 from .errors import (BackendUnavailableError, ConfigurationError, DefinitenessError,
-                     FastFcaError, NonHermitianError, PipelineError, SingularMatrixError,
+                     FastFcaError, MetricError, NonHermitianError, PipelineError, SingularMatrixError,
                      SingularMixtureError)
 from .fast import (fast_e_step, fast_m_step_S, fast_m_step_v, fastfca_run, propagate_pencil,
                    transform_observations)
+from .benchmark import benchmark_sweep
 from .initializers import init_from_masks, init_from_masks_batch, init_random, init_random_batch
+from .metrics import measure_rtf, sdr, sdr_pairing, sdr_pairing_device, sdr_pairs_device
 from .pencil import PencilDecomposition, gevd_hpd, hermitian_eig, solve_hermitian_system
 from .pipeline import separate, separate_device
 from .sharding import fastfca_run_sharded, fca_run_sharded
@@ -57,7 +60,14 @@ __all__ = [
     "hermitian_eig",
     "fastfca_run_sharded",
     "fca_run_sharded",
+    "benchmark_sweep",
     "init_from_masks",
+    "measure_rtf",
+    "sdr",
+    "sdr_pairing",
+    "sdr_pairing_device",
+    "sdr_pairs_device",
+    "MetricError",
     "init_from_masks_batch",
     "init_random",
     "init_random_batch",

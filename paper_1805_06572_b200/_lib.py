@@ -110,6 +110,8 @@ SIGNATURES = [
     ("ffca_stft_frames", c_i64, [c_i64, c_int]),
     ("ffca_stft_analyze", c_int, [c_vp, c_vp, c_i64, c_int, c_i64, c_int, c_vp]),
     ("ffca_stft_synthesize", c_int, [c_vp, c_vp, c_i64, c_int, c_i64, c_int, c_i64, c_vp]),
+    ("ffca_sdr_workspace_size", c_sz, [c_i64, c_i64, c_int]),
+    ("ffca_sdr", c_int, [c_vp, c_vp, c_i64, c_i64, c_int, c_vp, c_vp, c_vp, c_vp]),
 ]
 
 _lib = None

@@ -15,7 +15,7 @@ from . import _device as D
 from .conventional import fca_run
 from .errors import ConfigurationError, PipelineError
 from .fast import fastfca_run
-from .initializers import init_random, init_random_batch
+from .initializers import init_from_masks, init_from_masks_batch, init_random, init_random_batch
 from .stft import _validate_params, stft_analyze_device, stft_synthesize_device
 from .types import AudioBuffer
 
@@ -28,8 +28,10 @@ def _check_finite(t, stage):
 
 
 def separate_device(samples, iterations=20, frame_length=1024, algorithm="fastfca", seed=0,
-                    seeds=None, compute_likelihood=False, dtype="c128"):
+                    seeds=None, compute_likelihood=False, dtype="c128", init="random"):
     """samples (C, length) or (M, C, length) float64 (CUDA tensor or array).
+    ``init``: "random" (seeded ``init_random``) or "masks" (``init_from_masks``,
+    the reference CLI's two choices, cli.py:93-98).
 
     Returns ``(result, images_time)``: the engine's :class:`SeparationResult`
     (device tensors) and the separated source images in the time domain,
@@ -46,14 +48,18 @@ def separate_device(samples, iterations=20, frame_length=1024, algorithm="fastfc
     length = int(x.shape[-1])
     spec = stft_analyze_device(x, frame_length)  # (..., N, F, C)
     _check_finite(spec, "stft")
-    if batched:
+    if init not in ("random", "masks"):
+        raise ConfigurationError(f"unknown init {init!r}; expected 'random' or 'masks'")
+    if init == "masks":
+        model = init_from_masks_batch(spec) if batched else init_from_masks(spec)
+    elif batched:
         M = int(spec.shape[0])
-        init = init_random_batch(spec, list(seeds) if seeds is not None
-                                 else [seed + m for m in range(M)], dtype=dtype)
+        model = init_random_batch(spec, list(seeds) if seeds is not None
+                                  else [seed + m for m in range(M)], dtype=dtype)
     else:
-        init = init_random(spec, seed, dtype=dtype)
+        model = init_random(spec, seed, dtype=dtype)
     _, run = ENGINES[algorithm]
-    result = run(spec, init, iterations, compute_likelihood=compute_likelihood, dtype=dtype,
+    result = run(spec, model, iterations, compute_likelihood=compute_likelihood, dtype=dtype,
                  device_output=True)
     images = result.images  # (..., 2, N, F, C)
     _check_finite(images, f"separation ({ENGINES[algorithm][0]})")
