@@ -20,6 +20,7 @@ from torch.profiler import ProfilerActivity, profile  # noqa: E402
 from bench import make_inputs, shard  # noqa: E402
 from paper_1805_06572_b200._engine import (plan_chunks, run_device, run_device_streams,  # noqa: E402
                                            status_of)
+from paper_1805_06572_b200.sharding import shard_chunk_frames  # noqa: E402
 from paper_1805_06572_b200.synth import CONFIGS  # noqa: E402
 
 
@@ -34,7 +35,7 @@ def main():
     Y, V, S, FL = make_inputs(cfg, shard(cfg, 0, 1))
     y, v, s, fl = (torch.from_numpy(x).cuda() for x in (Y, V, S, FL))
     M, N, F, I = Y.shape
-    cf, nc = plan_chunks(M * F, N, I, "c128", a.engine)
+    cf = shard_chunk_frames(cfg.M, cfg.N, cfg.F, cfg.I, "c128", a.engine, max_world=cfg.max_world)
     bufs = {"images": torch.empty((M, 2, N, F, I), dtype=torch.complex128, device="cuda"),
             "S": torch.empty((M, 2, F, I, I), dtype=torch.complex128, device="cuda"),
             "v": torch.empty_like(v)}
