@@ -97,6 +97,41 @@ FFCA_DEV void cp_async_wait() {
 }
 FFCA_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
+// ---- TMA bulk copies + mbarrier (sm_90+; the frame ring of the update pass) ----
+FFCA_DEV unsigned smem_u32(const void* ptr) { return (unsigned)__cvta_generic_to_shared(ptr); }
+FFCA_DEV void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+FFCA_DEV void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+FFCA_DEV void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+FFCA_DEV bool mbar_try_wait(unsigned bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+FFCA_DEV void mbar_wait(unsigned bar, unsigned parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// global -> shared bulk copy completing on `bar` (16-B aligned, size % 16 == 0)
+FFCA_DEV void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+// order this thread's earlier generic-proxy shared-memory accesses before
+// later async-proxy (bulk copy) writes to the same memory
+FFCA_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 // Compute precision follows the streaming precision: complex128 runs the
 // per-point math in FP64; complex64 runs it in FP32 (B200's 2x-wider FP32
 // pipe) with FP64 per-bin state and FP64 accumulators fed by FP32 partial
@@ -197,6 +232,23 @@ struct RingSlot {
   static FFCA_DEV constexpr int pos(int b, int a) { return (Q * b + (a ^ sw(b))) * UB; }
   static FFCA_DEV constexpr int rbase(int b) { return (Q * b + sw(b)) * UB; }
   static FFCA_DEV constexpr int rpos(int rb, int a) { return kXor ? (rb ^ (a * UB)) : rb + a * UB; }
+};
+
+// TMA ring stage of one warp (update pass, complex128): the frame's y row of
+// the warp's 32 bins copied by ONE elected lane with cp.async.bulk (one copy,
+// or two when the tile crosses into the next mixture) and v1, v2 as 16-B
+// aligned supersets of their runs (a frame row of v is only 8-B aligned when
+// F is odd). The row lands linearly (bin b at b*YB); lanes read their Q units
+// in the rotated order (k + sw(b)) mod Q — the RingSlot swizzle moved from the
+// write side to the read side, undone by storing P's rows in the same
+// rotation — so the reads stay bank-conflict free.
+template <int I, typename R>
+struct BulkSlot {
+  using RS = RingSlot<I, R>;
+  static constexpr int YB = RS::YB, VB = RS::VB, Q = RS::Q;
+  static constexpr int VA = ((32 * VB + 64) + 15) / 16 * 16;  // v run + alignment slack, 2 runs
+  static constexpr int WARP_BYTES = 32 * YB + 2 * VA;
+  static constexpr bool kOk = (YB % 16 == 0) && VB == 8;  // complex128
 };
 
 // The RingSlot scheme as a reusable object (used by the FCA pass, K4): a
@@ -370,15 +422,18 @@ struct SmemAcc {
   static constexpr bool value = std::is_same<R, float>::value && (I % 2 == 0) && UPDATE && !LL && !MU;
 };
 
-template <int I, typename R, int WARPS, int STAGES, bool MU = false, bool SACC = false>
+template <int I, typename R, int WARPS, int STAGES, bool MU = false, bool SACC = false,
+          bool BULK = false>
 struct Fast2Smem {
   static constexpr int NE = 2 * I * I + 1;
-  static constexpr size_t RING = (size_t)STAGES * WARPS * RingSlot<I, R>::WARP_BYTES;
+  static constexpr size_t RING =
+      (size_t)STAGES * WARPS * (BULK ? BulkSlot<I, R>::WARP_BYTES : RingSlot<I, R>::WARP_BYTES);
   static constexpr size_t RED = (size_t)(WARPS - 1) * NE * 32 * sizeof(double);
   static constexpr size_t PB = (size_t)I * I * 32 * sizeof(typename Math<R>::T2);  // P tile
   static constexpr size_t WB = MU ? PB : 0;                           // W tile, after P
   static constexpr size_t ACC = SACC ? (size_t)2 * I * I * WARPS * 32 * sizeof(double) : 0;
-  static constexpr size_t MAIN = RING + PB + WB + ACC;  // accumulators after the tiles
+  static constexpr size_t BARS = BULK ? (size_t)STAGES * WARPS * 8 : 0;  // one mbarrier per stage
+  static constexpr size_t MAIN = RING + PB + WB + ACC + BARS;  // accumulators after the tiles
   static constexpr size_t BYTES = MAIN > RED ? MAIN : RED;
 };
 
@@ -415,7 +470,8 @@ constexpr int fast2_minb() {
   return MU ? FAST2_MU_MINB : (SmemAcc<I, R, UPDATE, LL, MU>::value ? 4 : FAST2_MINB);
 }
 
-template <int I, typename R, int WARPS, int STAGES, bool UPDATE, bool LL, bool MU>
+template <int I, typename R, int WARPS, int STAGES, bool UPDATE, bool LL, bool MU,
+          bool BULK = false>
 __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>())) fast_em2_kernel(const FastIterParams p) {
   using C = typename CplxOf<R>::type;
   using Slot = RingSlot<I, R>;
@@ -441,7 +497,9 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
   R* vb = (R*)p.v + m * 2 * NF + f;  // no __restrict__: may alias vr (in place)
   const R* vr = (p.v_src ? (const R*)p.v_src : (const R*)p.v) + m * 2 * NF + f;
   constexpr bool kSacc = SmemAcc<I, R, UPDATE, LL, MU>::value;
-  using Sm = Fast2Smem<I, R, WARPS, STAGES, MU, kSacc>;
+  using Sm = Fast2Smem<I, R, WARPS, STAGES, MU, kSacc, BULK>;
+  using BS = BulkSlot<I, R>;
+  static_assert(!BULK || (BS::kOk && UPDATE && !LL && !MU), "bulk ring: complex128 update pass");
 
   double acc[2][kSacc ? 1 : NP];  // (kSacc: in shared memory, accS)
   // accS[(j NP + e) * WARPS * 32 + tid]: thread-minor, conflict-free
@@ -579,7 +637,7 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
   // W = P^{-H} for the image write (last pass only), same bin-minor tile layout
   T2* sW = sP + NP * 32;
   auto load_tile = [&]() {
-    if (FFCA_K3_PCOAL) {
+    if (FFCA_K3_PCOAL || BULK) {
       // the tile's P block (32 consecutive bins x NP entries) is one
       // contiguous run: thread t copies 16-B units t, t + 128, ... (bin
       // b = u / NP of the tile, clamped like g; entry e = u % NP)
@@ -587,7 +645,12 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
         const int b = u / NP, e = u - (u / NP) * NP;
         int64_t gb = tile0 + b;
         if (gb >= G) gb = G - 1;
-        sP[e * 32 + b] = Math<R>::c2(p.P[gb * NP + e]);
+        int es = e;
+        if constexpr (BULK) {  // row r of P where the lane's rotated unit order reads y_r
+          const int row = e / I;
+          es = ((row - Slot::sw(b) + Slot::Q) % Slot::Q) * I + (e - row * I);
+        }
+        sP[es * 32 + b] = Math<R>::c2(p.P[gb * NP + e]);
         if (MU && p.mu_back) sW[e * 32 + b] = Math<R>::c2(p.W[gb * NP + e]);
       }
     } else {
@@ -599,10 +662,90 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
   };
   if (!FFCA_K3_RING_FIRST) load_tile();
   constexpr int kAhead = STAGES - 1;  // frames issued ahead
+  // ---- TMA bulk ring (BULK): one elected lane per warp issues the copies ----
+  // the tile's valid bins and the split into two mixtures (F >= 32: at most
+  // two), per-segment source pointers at this warp's next frame, the 16-B
+  // aligned v supersets (their alignment is a per-warp constant: a warp's
+  // frames step by WARPS F v-elements = 32 F bytes), this lane's v offsets
+  [[maybe_unused]] int b_nval = 0, b_s = 0;
+  [[maybe_unused]] const unsigned char* b_y[2] = {nullptr, nullptr};
+  [[maybe_unused]] const unsigned char* b_v[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  [[maybe_unused]] unsigned b_len[2][2] = {{0u, 0u}, {0u, 0u}};
+  [[maybe_unused]] unsigned b_d2 = 0, b_bytes = 0, b_bar0 = 0;
+  [[maybe_unused]] int b_off[2] = {0, 0};
+  [[maybe_unused]] int b_rot = 0, b_ist = 0, b_rst = 0;
+  [[maybe_unused]] unsigned b_ph = 0;
+  auto b_stage = [&](int st) -> unsigned char* {
+    return smem_raw + ((size_t)st * WARPS + warp) * BS::WARP_BYTES;
+  };
+  if constexpr (BULK) {
+    b_nval = (int)min((int64_t)32, G - tile0);
+    const int64_t m0 = tile0 / p.F, f0 = tile0 - m0 * p.F;
+    b_s = (int)min((int64_t)b_nval, p.F - f0);
+    b_y[0] = (const unsigned char*)p.y + ((m0 * p.N + nfirst) * p.F + f0) * BS::YB;
+    b_y[1] = (const unsigned char*)p.y + (((m0 + 1) * p.N + nfirst) * p.F) * BS::YB;
+    const unsigned char* vbase = (const unsigned char*)(p.v_src ? p.v_src : p.v);
+    const int64_t va[2] = {(m0 * 2 * NF + nfirst * p.F + f0) * BS::VB,
+                           ((m0 + 1) * 2 * NF + nfirst * p.F) * BS::VB};
+    const int cnt[2] = {b_s, b_nval - b_s};
+    b_d2 = (unsigned)((16 + b_s * BS::VB + 15) / 16 * 16);
 #pragma unroll
-  for (int s = 0; s < kAhead; ++s) {
-    if (s < K) issue(s);
-    cp_async_commit();
+    for (int j = 0; j < 2; ++j)  // v1, v2
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {  // segments
+        const uintptr_t a = (uintptr_t)(vbase + va[q] + (int64_t)j * NF * BS::VB);
+        const uintptr_t lo = a & ~(uintptr_t)15;
+        const uintptr_t hi = (a + (uintptr_t)cnt[q] * BS::VB + 15) & ~(uintptr_t)15;
+        b_v[j][q] = (const unsigned char*)lo;
+        b_len[j][q] = cnt[q] > 0 ? (unsigned)(hi - lo) : 0u;
+        if ((lane < b_s) == (q == 0))
+          b_off[j] = (q == 0 ? 0 : (int)b_d2) + (int)(a - lo) +
+                     (q == 0 ? lane : lane - b_s) * BS::VB;
+      }
+    if (lane >= b_nval) b_off[0] = b_off[1] = 0;  // clamped bins read bin 0's slot
+    b_bytes = (unsigned)(b_nval * BS::YB) + b_len[0][0] + b_len[0][1] + b_len[1][0] + b_len[1][1];
+    b_rot = Slot::sw(lane);
+    b_bar0 = smem_u32(smem_raw + Sm::RING + Sm::PB + Sm::WB + Sm::ACC) + warp * 8;
+    if (lane == 0) {
+      for (int st = 0; st < STAGES; ++st) mbar_init(b_bar0 + st * WARPS * 8, 1);
+      mbar_init_fence();
+    }
+    __syncwarp();
+  }
+  auto bissue = [&]() {  // lane 0: this warp's next frame into stage b_ist
+    const unsigned bar = b_bar0 + b_ist * WARPS * 8;
+    unsigned char* dst = b_stage(b_ist);
+    b_ist = b_ist + 1 == STAGES ? 0 : b_ist + 1;
+    fence_proxy_async_smem();  // the stage's earlier generic reads before the async writes
+    mbar_expect_tx(bar, b_bytes);
+    bulk_g2s(smem_u32(dst), b_y[0], (unsigned)(b_s * BS::YB), bar);
+    if (b_nval > b_s)
+      bulk_g2s(smem_u32(dst + b_s * BS::YB), b_y[1], (unsigned)((b_nval - b_s) * BS::YB), bar);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      unsigned char* vd = dst + 32 * BS::YB + j * BS::VA;
+      bulk_g2s(smem_u32(vd), b_v[j][0], b_len[j][0], bar);
+      if (b_len[j][1]) bulk_g2s(smem_u32(vd + b_d2), b_v[j][1], b_len[j][1], bar);
+    }
+    const int64_t ys = (int64_t)WARPS * p.F * BS::YB, vs = (int64_t)WARPS * p.F * BS::VB;
+    b_y[0] += ys;
+    b_y[1] += ys;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      b_v[j][0] += vs;
+      b_v[j][1] += vs;
+    }
+  };
+  if constexpr (BULK) {
+    if (lane == 0)
+      for (int s = 0; s < kAhead; ++s)
+        if (s < K) bissue();
+  } else {
+#pragma unroll
+    for (int s = 0; s < kAhead; ++s) {
+      if (s < K) issue(s);
+      cp_async_commit();
+    }
   }
   if (FFCA_K3_RING_FIRST) load_tile();
   T lam[I], il[I];  // il = 1 / (I lam): the 1/I of v1 = tr1 / I folded in
@@ -808,19 +951,39 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
     v1 = ((const R*)vs)[lane];
     v2 = ((const R*)(vs + 32 * sizeof(R)))[lane];
   };
+  auto bload = [&](T2 (&yv)[I], T& v1, T& v2) {  // BULK: the stage of frame k
+    const unsigned bar = b_bar0 + b_rst * WARPS * 8;
+    mbar_wait(bar, b_ph);
+    const unsigned char* slot = b_stage(b_rst);
+    if (++b_rst == STAGES) {
+      b_rst = 0;
+      b_ph ^= 1u;
+    }
+    const unsigned char* row = slot + lane * BS::YB;
+#pragma unroll
+    for (int k = 0; k < Slot::Q; ++k)  // unit (k + rot) mod Q (P's rows stored to match)
+      yv[k] = *(const T2*)(row + 16 * ((k + b_rot) % Slot::Q));
+    v1 = *(const R*)(slot + 32 * BS::YB + b_off[0]);
+    v2 = *(const R*)(slot + 32 * BS::YB + BS::VA + b_off[1]);
+  };
 
   {
     constexpr int kUnroll = FAST2_UNROLL;
 #pragma unroll kUnroll
     for (int k = 0; k < K; ++k) {
       __syncwarp();  // every lane is done with the stage the next copy overwrites
-      if (k + STAGES - 1 < K) issue(k + STAGES - 1);
-      cp_async_commit();
-      cp_async_wait<STAGES - 1>();
-      __syncwarp();  // the other lanes' copies of this stage are visible
       T2 yv[I];
       T v1, v2;
-      load_frame(k, yv, v1, v2);
+      if constexpr (BULK) {
+        if (lane == 0 && k + STAGES - 1 < K) bissue();
+        bload(yv, v1, v2);
+      } else {
+        if (k + STAGES - 1 < K) issue(k + STAGES - 1);
+        cp_async_commit();
+        cp_async_wait<STAGES - 1>();
+        __syncwarp();  // the other lanes' copies of this stage are visible
+        load_frame(k, yv, v1, v2);
+      }
       T2 z[I];
       if constexpr (kF2) {
         // z_a = sum_b conj(P_ba) y_b: p.x (y.x, y.y) + p.y (y.y, -y.x), packed
@@ -917,17 +1080,46 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
   }
 }
 
+// TMA bulk-copy frame ring for the complex128 update pass (off: measured
+// slower). Correct (the whole GPU suite passes with it on), but at one warp
+// per 32-bin tile every warp-frame is 3-6 small bulk copies (a 2 KB y row,
+// two ~256 B v runs, doubled across a mixture boundary) issued by one lane:
+// the copies serialise on the SM's TMA unit, each needs its operands moved
+// to uniform registers (a waterfall loop in SASS) and the ring state costs
+// registers (spills at 168): config-3 update pass 2.09 ms vs 1.55 ms with the
+// cooperative cp.async ring, config 4 0.563 vs 0.412 ms (same session).
+#ifndef FFCA_K3_BULK
+#define FFCA_K3_BULK 0
+#endif
+// The bulk ring needs every tile within two mixtures (F >= 32) and 16-B
+// aligned y / v bases; other calls take the cp.async ring.
 template <int I, typename R, bool UPDATE, bool LL, bool MU>
-cudaError_t launch_fast2_variant(const FastIterParams& p, cudaStream_t s) {
+constexpr bool fast2_bulk_capable() {
+  return FFCA_K3_BULK && BulkSlot<I, R>::kOk && UPDATE && !LL && !MU &&
+         !SmemAcc<I, R, UPDATE, LL, MU>::value;
+}
+
+template <int I, typename R, bool UPDATE, bool LL, bool MU, bool BULK>
+cudaError_t launch_fast2_kern(const FastIterParams& p, cudaStream_t s) {
   constexpr int WARPS = kWarps;
   constexpr int STAGES = fast2_stages<I, R, UPDATE, LL, MU>();
-  using Sm = Fast2Smem<I, R, WARPS, STAGES, MU, SmemAcc<I, R, UPDATE, LL, MU>::value>;
-  auto kern = fast_em2_kernel<I, R, WARPS, STAGES, UPDATE, LL, MU>;
-  if (cudaError_t e = ensure_smem<fast_em2_kernel<I, R, WARPS, STAGES, UPDATE, LL, MU>>(Sm::BYTES))
+  using Sm = Fast2Smem<I, R, WARPS, STAGES, MU, SmemAcc<I, R, UPDATE, LL, MU>::value, BULK>;
+  auto kern = fast_em2_kernel<I, R, WARPS, STAGES, UPDATE, LL, MU, BULK>;
+  if (cudaError_t e = ensure_smem<fast_em2_kernel<I, R, WARPS, STAGES, UPDATE, LL, MU, BULK>>(Sm::BYTES))
     return e;
   dim3 grid((unsigned)((p.G + 31) / 32), (unsigned)p.nchunk);
   kern<<<grid, WARPS * 32, Sm::BYTES, s>>>(p);
   return cudaGetLastError();
+}
+
+template <int I, typename R, bool UPDATE, bool LL, bool MU>
+cudaError_t launch_fast2_variant(const FastIterParams& p, cudaStream_t s) {
+  if constexpr (fast2_bulk_capable<I, R, UPDATE, LL, MU>()) {
+    const void* vb = p.v_src ? p.v_src : p.v;
+    if (p.F >= 32 && ((uintptr_t)p.y % 16) == 0 && ((uintptr_t)vb % 16) == 0)
+      return launch_fast2_kern<I, R, UPDATE, LL, MU, true>(p, s);
+  }
+  return launch_fast2_kern<I, R, UPDATE, LL, MU, false>(p, s);
 }
 
 template <int I, typename R>

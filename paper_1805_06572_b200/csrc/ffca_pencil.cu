@@ -142,10 +142,17 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
 }
 
 #ifndef FFCA_K1_MINB
-#define FFCA_K1_MINB 1  // CTAs of 64 per SM the one-thread-per-bin refresh is budgeted for
+#define FFCA_K1_MINB 1  // CTAs per SM the one-thread-per-bin refresh is budgeted for
+#endif
+// Threads per CTA of the one-thread-per-bin refresh. Each thread runs ~5k
+// straight-line instructions once, so on the few-bin configs (513 bins:
+// 9 CTAs of 64) the pass is instruction-fetch bound (ncu stall_no_instruction
+// 4.2 per issue): larger CTAs put more warps behind every i-cache fill.
+#ifndef FFCA_K1_THREADS
+#define FFCA_K1_THREADS 64
 #endif
 template <int I>
-__global__ void __launch_bounds__(64, FFCA_K1_MINB) pencil_update_kernel(const PencilParams p) {
+__global__ void __launch_bounds__(FFCA_K1_THREADS, FFCA_K1_MINB) pencil_update_kernel(const PencilParams p) {
   constexpr int NP = I * I;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= p.G) return;
@@ -322,12 +329,13 @@ static bool use_par(int64_t G, int I) {
 cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s) {
   if (use_par(p.G, I)) return launch_pencil_par(p, I, s);
   if (I <= 4) {  // fused single kernel; only instantiated for I <= 4
-    const unsigned nb = nblk(p.G, 64);
+    constexpr int T = FFCA_K1_THREADS;
+    const unsigned nb = nblk(p.G, T);
     switch (I) {
-      case 1: pencil_update_kernel<1><<<nb, 64, 0, s>>>(p); break;
-      case 2: pencil_update_kernel<2><<<nb, 64, 0, s>>>(p); break;
-      case 3: pencil_update_kernel<3><<<nb, 64, 0, s>>>(p); break;
-      default: pencil_update_kernel<4><<<nb, 64, 0, s>>>(p); break;
+      case 1: pencil_update_kernel<1><<<nb, T, 0, s>>>(p); break;
+      case 2: pencil_update_kernel<2><<<nb, T, 0, s>>>(p); break;
+      case 3: pencil_update_kernel<3><<<nb, T, 0, s>>>(p); break;
+      default: pencil_update_kernel<4><<<nb, T, 0, s>>>(p); break;
     }
     return cudaGetLastError();
   }
