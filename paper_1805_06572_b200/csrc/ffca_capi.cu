@@ -306,8 +306,8 @@ int ffca_plan_grid(int64_t G, int64_t N, int I, int dtype, int algorithm, int64_
     bpsm = I >= 5 ? fca_par_blocks_per_sm(I, dtype) : fca_blocks_per_sm(I, dtype);
     tile = I >= 5 ? fca_par_bins_per_cta(I) : 32;
   } else {
-    bpsm = I >= 5 ? fast_par_blocks_per_sm(I, dtype) : fast_blocks_per_sm(I, dtype);
-    tile = I >= 5 ? fast_par_bins_per_cta() : 32;
+    bpsm = fast_update_blocks_per_sm(I, dtype);
+    tile = fast_tile_bins(I, dtype);
   }
   *ctas = (G + tile - 1) / tile * nc;
   *slots = (int64_t)sm_count() * bpsm;

@@ -16,7 +16,7 @@
 // per-bin sums are reduced across the CTA's warps in shared memory and
 // written as one partial per (frame chunk, bin). Reduction order is fixed, so
 // results are deterministic and independent of how bins are sharded.
-#include "ffca_internal.cuh"
+#include "ffca_fast2.cuh"  // FFCA_K3T
 
 namespace ffca {
 
@@ -58,13 +58,38 @@ int fast_blocks_per_sm(int I, int dtype) {
 }
 
 
+template <int I>
+int fast_tma_blocks_per_sm();  // ffca_fast_i<I>.cu
+
+// the update pass's CTA tile and residency: K3t (128-bin tiles, complex128,
+// I <= 4) when enabled, else the cp.async ring kernel (32-bin tiles) / K3p
+bool fast_tma_tiles(int I, int dtype) { return FFCA_K3T && dtype == FFCA_C128 && I >= 1 && I <= 4; }
+int fast_tile_bins(int I, int dtype) {
+  if (I >= 5) return fast_par_bins_per_cta();
+  return fast_tma_tiles(I, dtype) ? 128 : 32;
+}
+int fast_update_blocks_per_sm(int I, int dtype) {
+  if (!fast_tma_tiles(I, dtype)) return I >= 5 ? fast_par_blocks_per_sm(I, dtype) : fast_blocks_per_sm(I, dtype);
+  static int cache[5] = {};
+  if (!cache[I]) {
+    switch (I) {
+      case 1: cache[I] = fast_tma_blocks_per_sm<1>(); break;
+      case 2: cache[I] = fast_tma_blocks_per_sm<2>(); break;
+      case 3: cache[I] = fast_tma_blocks_per_sm<3>(); break;
+      default: cache[I] = fast_tma_blocks_per_sm<4>(); break;
+    }
+  }
+  return cache[I];
+}
+
 void plan_fast_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames,
                       int* nchunk) {
   if (I >= 5)
     plan_chunks(G, N, fast_par_blocks_per_sm(I, dtype), chunk_frames, nchunk,
                 fast_par_bins_per_cta(), 16);
   else
-    plan_chunks(G, N, fast_blocks_per_sm(I, dtype), chunk_frames, nchunk);
+    plan_chunks(G, N, fast_update_blocks_per_sm(I, dtype), chunk_frames, nchunk,
+                fast_tile_bins(I, dtype));
 }
 
 cudaError_t launch_fast_em(const FastIterParams& p, int I, int dtype, cudaStream_t s) {

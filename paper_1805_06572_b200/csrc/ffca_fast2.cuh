@@ -1133,10 +1133,35 @@ int fast2_blocks_per_sm() {
   return n > 0 ? n : 1;
 }
 
+// K3t (ffca_fast_tma.cuh): the complex128 update pass with a CTA-wide TMA
+// ring over 128-bin tiles; needs every tile within two mixtures (F >= 128)
+// and 16-B aligned y / v bases. Off by default: correct (GPU suite green with
+// it on) but slower than the cooperative cp.async ring — config-3 update pass
+// 1.68 ms vs 1.56 ms, config 4 0.488 vs 0.412 ms (same session): the 128-bin
+// P tile (32 KB) leaves room for only 4 ring stages at 3 CTAs/SM, i.e. ~90 KB
+// in flight per SM against ~150 KB for the per-warp 6-stage ring, and the 4
+// warps of a CTA run in lockstep on the shared stages.
+#ifndef FFCA_K3T
+#define FFCA_K3T 0
+#endif
+template <int I>
+cudaError_t launch_fast_tma(const FastIterParams& p, cudaStream_t s);
+template <int I, typename R>
+bool fast_tma_applies(const FastIterParams& p) {
+  if constexpr (!FFCA_K3T || !std::is_same<R, double>::value) {
+    return false;
+  } else {
+    const void* vb = p.v_src ? p.v_src : p.v;
+    return p.update && !p.llbin && !p.mu_out && p.F >= 128 && ((uintptr_t)p.y % 16) == 0 &&
+           ((uintptr_t)vb % 16) == 0;
+  }
+}
+
 template <int I, typename R>
 cudaError_t launch_fast2(const FastIterParams& p, cudaStream_t s) {
   const bool ll = p.llbin != nullptr;
   const bool mu = p.mu_out != nullptr;
+  if (fast_tma_applies<I, R>(p)) return launch_fast_tma<I>(p, s);
   if (p.update) {
     if (!ll && !mu) return launch_fast2_variant<I, R, true, false, false>(p, s);
     if (ll && !mu) return launch_fast2_variant<I, R, true, true, false>(p, s);

@@ -132,6 +132,9 @@ cudaError_t launch_ll_reduce(const double* llg, int64_t M, int64_t F, int64_t N,
 void plan_chunks(int64_t G, int64_t N, int blocks_per_sm, int64_t* chunk_frames, int* nchunk,
                  int tile_bins = 32, int64_t min_frames = 8 * kWarps);
 int fast_blocks_per_sm(int I, int dtype);
+// the FastFCA update pass's CTA tile (bins) and resident CTAs per SM
+int fast_tile_bins(int I, int dtype);
+int fast_update_blocks_per_sm(int I, int dtype);
 int fca_blocks_per_sm(int I, int dtype);
 // FCA plan: the lane-parallel kernel (I >= 5) tiles fewer bins per CTA and
 // streams every frame of a chunk in one lane group
