@@ -129,6 +129,8 @@ int check_args(const ffca_run_args* a) {
       !a->S_out || !a->workspace)
     return FFCA_ERR_INVALID;
   if (a->dtype != FFCA_C128 && a->dtype != FFCA_C64) return FFCA_ERR_INVALID;
+  // bin indices are split into (mixture, bin) with 32-bit divisions in the kernels
+  if (a->M * a->F >= 0x7fffffff || a->N * a->F >= ((int64_t)1 << 40)) return FFCA_ERR_INVALID;
   if ((a->flags & FFCA_FLAG_IMAGES) && !a->images) return FFCA_ERR_INVALID;
   if ((a->flags & FFCA_FLAG_LIKELIHOOD) && !a->loglik) return FFCA_ERR_INVALID;
   if (((size_t)a->workspace) % kAlign) return FFCA_ERR_INVALID;

@@ -273,14 +273,14 @@ struct FrameRing {
                      int64_t N, int64_t F, const void* y, const R* vrow, int64_t nfirst) {
     lane = lane_;
     wslots = base + (size_t)warp * Slot::WARP_BYTES;
-    contiguous = (tile0 + 31 < G) && (tile0 / F == (tile0 + 31) / F);
+    contiguous = (tile0 + 31 < G) && ((unsigned)tile0 / (unsigned)F == (unsigned)(tile0 + 31) / (unsigned)F);
     spos0 = Slot::pos(lane / Slot::Q, lane % Slot::Q);
     rb = Slot::rbase(lane);
     auto unit_off = [&](int c) -> int64_t {
       const int u = 32 * c + lane, b = u / Slot::Q, a = u % Slot::Q;
       int64_t gb = tile0 + b;
       if (gb >= G) gb = G - 1;
-      const int64_t mb = gb / F, fb = gb - mb * F;
+      const int64_t mb = (unsigned)gb / (unsigned)F, fb = gb - mb * F;
       return ((mb * N) * F + fb) * Slot::YB + a * Slot::UB;
     };
     const int64_t ybase = unit_off(0);
@@ -365,9 +365,9 @@ struct ImageRowStore {
     lane = lane_;
     F = F_;
     NF = N * F_;
-    contiguous = (tile0 + 31 < G) && (tile0 / F_ == (tile0 + 31) / F_);
+    contiguous = (tile0 + 31 < G) && ((unsigned)tile0 / (unsigned)F_ == (unsigned)(tile0 + 31) / (unsigned)F_);
     spos0 = Slot::pos(lane / Slot::Q, lane % Slot::Q);
-    const int64_t m0 = tile0 / F_, f0 = tile0 - m0 * F_;
+    const int64_t m0 = (unsigned)tile0 / (unsigned)F_, f0 = tile0 - m0 * F_;
     row0 = (m0 * 2 * NF + f0) * Slot::YB;
 #pragma unroll
     for (int c = 0; c < Slot::Q; ++c) {
@@ -375,7 +375,7 @@ struct ImageRowStore {
       int64_t gb = tile0 + b;
       valid[c] = gb < G;
       if (gb >= G) gb = G - 1;
-      const int64_t mb = gb / F_, fb = gb - mb * F_;
+      const int64_t mb = (unsigned)gb / (unsigned)F_, fb = gb - mb * F_;
       corr[c] = contiguous ? 0 : (mb * 2 * NF + fb) * Slot::YB + a * Slot::UB - row0 -
                                      (int64_t)u * Slot::UB;
     }
@@ -429,7 +429,9 @@ struct Fast2Smem {
   static constexpr size_t RING =
       (size_t)STAGES * WARPS * (BULK ? BulkSlot<I, R>::WARP_BYTES : RingSlot<I, R>::WARP_BYTES);
   static constexpr size_t RED = (size_t)(WARPS - 1) * NE * 32 * sizeof(double);
-  static constexpr size_t PB = (size_t)I * I * 32 * sizeof(typename Math<R>::T2);  // P tile
+  // P tile, rows of kTileStride (33) entries: the coalesced copy (consecutive
+  // threads = consecutive entries of one bin) then hits distinct banks
+  static constexpr size_t PB = (size_t)I * I * 33 * sizeof(typename Math<R>::T2);
   static constexpr size_t WB = MU ? PB : 0;                           // W tile, after P
   static constexpr size_t ACC = SACC ? (size_t)2 * I * I * WARPS * 32 * sizeof(double) : 0;
   static constexpr size_t BARS = BULK ? (size_t)STAGES * WARPS * 8 : 0;  // one mbarrier per stage
@@ -633,9 +635,10 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
   // P lives in shared memory (bin-minor SoA after the frame ring): the 4
   // warps of the CTA work on the same 32 bins, so one 16*I*I-byte column per
   // lane serves all of them and frees the registers for the accumulators.
+  constexpr int kTS = 33;  // P / W tile row stride (entries)
   T2* sP = (T2*)(smem_raw + Sm::RING);
   // W = P^{-H} for the image write (last pass only), same bin-minor tile layout
-  T2* sW = sP + NP * 32;
+  T2* sW = sP + NP * kTS;
   auto load_tile = [&]() {
     if (FFCA_K3_PCOAL || BULK) {
       // the tile's P block (32 consecutive bins x NP entries) is one
@@ -650,13 +653,13 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
           const int row = e / I;
           es = ((row - Slot::sw(b) + Slot::Q) % Slot::Q) * I + (e - row * I);
         }
-        sP[es * 32 + b] = Math<R>::c2(p.P[gb * NP + e]);
-        if (MU && p.mu_back) sW[e * 32 + b] = Math<R>::c2(p.W[gb * NP + e]);
+        sP[es * kTS + b] = Math<R>::c2(p.P[gb * NP + e]);
+        if (MU && p.mu_back) sW[e * kTS + b] = Math<R>::c2(p.W[gb * NP + e]);
       }
     } else {
-      for (int e = warp; e < NP; e += WARPS) sP[e * 32 + lane] = Math<R>::c2(p.P[g * NP + e]);
+      for (int e = warp; e < NP; e += WARPS) sP[e * kTS + lane] = Math<R>::c2(p.P[g * NP + e]);
       if (MU && p.mu_back)
-        for (int e = warp; e < NP; e += WARPS) sW[e * 32 + lane] = Math<R>::c2(p.W[g * NP + e]);
+        for (int e = warp; e < NP; e += WARPS) sW[e * kTS + lane] = Math<R>::c2(p.W[g * NP + e]);
     }
     __syncthreads();
   };
@@ -752,7 +755,7 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
 #pragma unroll
   for (int a = 0; a < I; ++a) {
     lam[a] = (T)p.lam[g * I + a];
-    il[a] = (T)(1.0 / ((double)I * p.lam[g * I + a]));
+    il[a] = (T)rcp_nr((double)I * p.lam[g * I + a]);  // (MUFU seed + 2 Newton: ~1 ulp; no IEEE division)
   }
   const T fl = (T)p.floor[g];
   constexpr T invI = T(1) / I;
@@ -907,7 +910,7 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
           T sx = 0, sy = 0;
 #pragma unroll
           for (int b = 0; b < I; ++b) {
-            const T2 w = sW[(a * I + b) * 32 + lane];
+            const T2 w = sW[(a * I + b) * kTS + lane];
             const T mx = g1[b] * z[b].x, my = g1[b] * z[b].y;
             sx = fma(w.x, mx, fma(-w.y, my, sx));
             sy = fma(w.x, my, fma(w.y, mx, sy));
@@ -989,12 +992,12 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
         // z_a = sum_b conj(P_ba) y_b: p.x (y.x, y.y) + p.y (y.y, -y.x), packed
 #pragma unroll
         for (int a = 0; a < I; ++a) {
-          const T2 p0 = sP[(0 * I + a) * 32 + lane];
+          const T2 p0 = sP[(0 * I + a) * kTS + lane];
           float2 za = f2::fma(f2::bc(p0.y), make_float2(yv[0].y, -yv[0].x),
                               f2::mul(f2::bc(p0.x), yv[0]));
 #pragma unroll
           for (int b = 1; b < I; ++b) {
-            const T2 pb = sP[(b * I + a) * 32 + lane];
+            const T2 pb = sP[(b * I + a) * kTS + lane];
             za = f2::fma(f2::bc(pb.x), yv[b], za);
             za = f2::fma(f2::bc(pb.y), make_float2(yv[b].y, -yv[b].x), za);
           }
@@ -1003,12 +1006,12 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
       } else
 #pragma unroll
       for (int a = 0; a < I; ++a) {
-        const T2 p0 = sP[(0 * I + a) * 32 + lane];
+        const T2 p0 = sP[(0 * I + a) * kTS + lane];
         T zr = p0.x * yv[0].x + p0.y * yv[0].y;
         T zi = p0.x * yv[0].y - p0.y * yv[0].x;
 #pragma unroll
         for (int b = 1; b < I; ++b) {
-          const T2 pb = sP[(b * I + a) * 32 + lane];
+          const T2 pb = sP[(b * I + a) * kTS + lane];
           zr = fma(pb.x, yv[b].x, fma(pb.y, yv[b].y, zr));
           zi = fma(pb.x, yv[b].y, fma(-pb.y, yv[b].x, zi));
         }

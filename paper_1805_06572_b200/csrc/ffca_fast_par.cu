@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, FAST_PAR_MINB) f
   if (!active) g = G - 1;
   const bool own = r < I;
   const int rr = own ? r : 0;  // clamped channel for idle lanes
-  const int64_t m = g / p.F, f = g - m * p.F;
+  const int64_t m = (unsigned)g / (unsigned)p.F, f = g - m * p.F;  // (32-bit division)
   double* base = sm + (size_t)grp * Lay::GROUP_DOUBLES;
   double2* sy = (double2*)base;      // y
   double2* sz = sy + I;              // z

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
   int64_t g = (int64_t)blockIdx.x * 32 + lane;
   const bool active = g < G;
   if (!active) g = G - 1;
-  const int64_t m = g / p.F;
+  const int64_t m = (unsigned)g / (unsigned)p.F;  // (32-bit division)
   const int64_t f = g - m * p.F;
   auto load_tile = [&]() {  // S1, S2 of the tile (packed, bin-minor)
     for (int e = warp; e < 2 * NP; e += WARPS) sS[e * 32 + lane] = p.Sp[(size_t)e * G + g];

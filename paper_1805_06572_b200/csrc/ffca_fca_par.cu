@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(FcaParLayout<I>::WARPS * 32, FCA_PAR_MINB) fca
   if (!active) g = G - 1;
   const bool own = r < I;
   const int rr = own ? r : 0;
-  const int64_t m = g / p.F, f = g - m * p.F;
+  const int64_t m = (unsigned)g / (unsigned)p.F, f = g - m * p.F;  // (32-bit division)
   double* base = sm + (size_t)grp * Lay::GROUP_DOUBLES;
   double2* SF = (double2*)base;             // [2][I][LD]: S1, S2 unpacked (row reads, no branches)
   double2* Lm = SF + 2 * I * Lay::LD;       // rows of Rinv
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(64)
   if (!active) g = G - 1;
   const bool own = r < I;
   const int rr = own ? r : 0;
-  const int64_t m = g / F, f = g - m * F;
+  const int64_t m = (unsigned)g / (unsigned)F, f = g - m * F;  // (32-bit division)
   double2* mS1 = (double2*)(sm + (size_t)grp * Lay::GROUP_DOUBLES);
   double2* mS2 = mS1 + I * LD;
   double2* mA = mS2 + I * LD;

@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kMT)
   __shared__ int ired[2 * kMW];
   const int tid = threadIdx.x;
   const int64_t g = blockIdx.x;
-  const int64_t m = g / F, f = g - m * F;
+  const int64_t m = (unsigned)g / (unsigned)F, f = g - m * F;  // (32-bit division)
   const double2* yb = y + (m * N * F + f) * I;
   const int64_t FI = F * I;
   extern __shared__ __align__(16) unsigned char zsm[];

@@ -20,7 +20,7 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
                           double2 (&S2)[I][I], double2 (&Pe)[I][I]) {
   constexpr int NP = I * I;
   const int64_t G = p.G;
-  const int64_t m = g / p.F, f = g - m * p.F;
+  const int64_t m = (unsigned)g / (unsigned)p.F, f = g - m * p.F;  // (32-bit division)
 
 
   // 1. reduce partials
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(64)
   constexpr int NP = I * I;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= G) return;
-  const int64_t m = g / F, f = g - m * F;
+  const int64_t m = (unsigned)g / (unsigned)F, f = g - m * F;  // (32-bit division)
   double2 A[I][I], B[I][I];
   const double2* s1 = S0 + ((m * 2 + 0) * F + f) * NP;
   const double2* s2 = S0 + ((m * 2 + 1) * F + f) * NP;

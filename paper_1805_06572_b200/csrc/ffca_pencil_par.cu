@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(ParLayout<I>::WARPS * 32) pencil_par_kernel(co
   const bool wr = own && active;  // may write global memory
   double* binb = sm + (size_t)bb * Lay::BIN_DOUBLES;
   const BinView<I> v{(double2*)binb, binb + Lay::NMAT * Lay::MAT * 2};
-  const int64_t m = g / p.F, f = g - m * p.F;
+  const int64_t m = (unsigned)g / (unsigned)p.F, f = g - m * p.F;  // (32-bit division)
 
   // 1. chunk partials -> S~1, S~2 (full Hermitian); entries split over lanes
   bool fin = true;
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(ParLayout<I>::WARPS * 32)
   const bool wr = own && active;
   double* binb = sm + (size_t)bb * Lay::BIN_DOUBLES;
   const BinView<I> v{(double2*)binb, binb + Lay::NMAT * Lay::MAT * 2};
-  const int64_t m = g / F, f = g - m * F;
+  const int64_t m = (unsigned)g / (unsigned)F, f = g - m * F;  // (32-bit division)
   const double2* s1 = S0 + ((m * 2 + 0) * F + f) * NP;
   const double2* s2 = S0 + ((m * 2 + 1) * F + f) * NP;
   if (own) {
