@@ -24,13 +24,14 @@
 namespace ffca {
 
 namespace {
-template <int I>
+template <int I, bool PAIR = false>
 struct FastParLayout {
   static constexpr int LB = 8;
   static constexpr int WARPS = 2;
   static constexpr int BPB = WARPS * 32 / LB;  // bins per CTA
-  // per group: y (2I), z (2I), (g1, g2) (2I) doubles; odd # of 16-B units
-  static constexpr int RAW = 6 * I;
+  // per group: y (2I), z (2I), (g1, g2) (2I) doubles (x2 frames when PAIR);
+  // odd # of 16-B units
+  static constexpr int RAW = 6 * I * (PAIR ? 2 : 1);
   static constexpr int U16 = (RAW + 1) / 2;
   static constexpr int GROUP_DOUBLES = 2 * ((U16 % 2) ? U16 : U16 + 1);
   static constexpr size_t RINGB = (size_t)8 * WARPS * 32 * 48;  // 8 stages x 64 lanes x 48 B
@@ -41,9 +42,16 @@ struct FastParLayout {
 #ifndef FAST_PAR_MINB
 #define FAST_PAR_MINB 8  // CTAs per SM the lane-parallel pass is register-budgeted for
 #endif
-template <int I, typename R, bool UPDATE, bool LL, bool MU>
-__global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, FAST_PAR_MINB) fast_par_kernel(const FastIterParams p) {
-  using Lay = FastParLayout<I>;
+#ifndef FAST_PAR_PAIR_MINB
+#define FAST_PAR_PAIR_MINB 6  // ... and its two-frames-per-trip update pass
+#endif
+#ifndef FFCA_K3P_PAIR
+#define FFCA_K3P_PAIR 1  // update pass: two frames per loop trip (ILP across the frame chains)
+#endif
+template <int I, typename R, bool UPDATE, bool LL, bool MU, bool PAIR = false>
+__global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, PAIR ? FAST_PAR_PAIR_MINB : FAST_PAR_MINB) fast_par_kernel(const FastIterParams p) {
+  static_assert(!PAIR || (UPDATE && !LL && !MU), "the paired loop is the update-only pass");
+  using Lay = FastParLayout<I, PAIR>;
   using C = typename CplxOf<R>::type;
   constexpr int NP = I * I;
   constexpr int LB = Lay::LB;
@@ -140,6 +148,120 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, FAST_PAR_MINB) f
     ynext += ystep;
     vnext += p.F;
   };
+  if constexpr (PAIR) {
+    // Two frames per trip: the per-frame chains (exchange -> z -> posterior
+    // -> group sums -> exchange -> accumulate) of frames k and k+1 run
+    // interleaved, with one set of warp barriers per pair. The per-lane ring
+    // runs a full kStages frames ahead: the two slots just read are refilled
+    // with frames k + kStages, k + kStages + 1 (no other lane reads them).
+    double2* syB = sgg + I;  // frame k+1's exchange buffers
+    double2* szB = syB + I;
+    double2* sggB = szB + I;
+#pragma unroll
+    for (int k = 0; k < kStages; ++k) {
+      if (k < K) issue(k);
+      cp_async_commit();
+    }
+#pragma unroll 1
+    for (int k = 0; k < K; k += 2) {
+      const bool two = k + 1 < K;  // (warp-uniform)
+      cp_async_wait<kStages - 2>();  // frames k and k+1 have landed
+      const unsigned char* slA = ring + (size_t)(k % kStages) * kStageStride;
+      const unsigned char* slB = ring + (size_t)((k + 1) % kStages) * kStageStride;
+      const double2 yA = to_c128(*(const C*)slA), yB = to_c128(*(const C*)slB);
+      const double v1A = (double)*(const R*)(slA + YB), v2A = (double)*(const R*)(slA + YB + VB);
+      const double v1B = (double)*(const R*)(slB + YB), v2B = (double)*(const R*)(slB + YB + VB);
+      if (k + kStages < K) issue(k + kStages);
+      cp_async_commit();
+      if (k + kStages + 1 < K) issue(k + kStages + 1);
+      cp_async_commit();
+      if (own) {
+        sy[r] = yA;
+        syB[r] = yB;
+      }
+      __syncwarp();
+      double zrA = 0.0, ziA = 0.0, zrB = 0.0, ziB = 0.0;
+#pragma unroll
+      for (int b = 0; b < I; ++b) {
+        const double2 a_ = sy[b], b_ = syB[b];
+        zrA = fma(pc[b].x, a_.x, fma(pc[b].y, a_.y, zrA));
+        ziA = fma(pc[b].x, a_.y, fma(-pc[b].y, a_.x, ziA));
+        zrB = fma(pc[b].x, b_.x, fma(pc[b].y, b_.y, zrB));
+        ziB = fma(pc[b].x, b_.y, fma(-pc[b].y, b_.x, ziB));
+      }
+      const double v1lA = v1A * lam, v1lB = v1B * lam;
+      const double rdA = rcp_nr(v1lA + v2A), rdB = rcp_nr(v1lB + v2B);
+      const double g1A = v1lA * rdA, g2A = v2A * rdA, g1B = v1lB * rdB, g2B = v2B * rdB;
+      const double cA = v2A * g1A, cB = v2B * g1B;
+      const double pzA = fma(zrA, zrA, ziA * ziA), pzB = fma(zrB, zrB, ziB * ziB);
+      const double t1A = fma(g1A * g1A, pzA, cA), t2A = fma(g2A * g2A, pzA, cA);
+      const double t1B = fma(g1B * g1B, pzB, cB), t2B = fma(g2B * g2B, pzB, cB);
+      if (own) {
+        sz[r] = cmk(zrA, ziA);
+        sgg[r] = cmk(g1A, g2A);
+        szB[r] = cmk(zrB, ziB);
+        sggB[r] = cmk(g1B, g2B);
+      }
+      double q1A = own ? t1A * il : 0.0, q2A = own ? t2A : 0.0;
+      double q1B = own ? t1B * il : 0.0, q2B = own ? t2B : 0.0;
+#pragma unroll
+      for (int o = LB / 2; o > 0; o >>= 1) {  // four group sums, interleaved
+        q1A += __shfl_xor_sync(0xffffffffu, q1A, o);
+        q2A += __shfl_xor_sync(0xffffffffu, q2A, o);
+        q1B += __shfl_xor_sync(0xffffffffu, q1B, o);
+        q2B += __shfl_xor_sync(0xffffffffu, q2B, o);
+      }
+      q1A /= I, q2A /= I, q1B /= I, q2B /= I;
+      const double w1A = (q1A < fl) ? fl : q1A, w2A = (q2A < fl) ? fl : q2A;
+      const double w1B = (q1B < fl) ? fl : q1B, w2B = (q2B < fl) ? fl : q2B;
+      if (r == 0) {
+        const int64_t nA = n0 + k;
+        if (active) {
+          vb[nA * p.F] = (R)w1A;
+          vb[NF + nA * p.F] = (R)w2A;
+          if (two) {
+            vb[(nA + 1) * p.F] = (R)w1B;
+            vb[NF + (nA + 1) * p.F] = (R)w2B;
+          }
+        }
+        auto badw = [](double w1, double w2) {
+          const long long b1 = __double_as_longlong(w1), b2 = __double_as_longlong(w2);
+          return (((b1 >> 52) & 0x7ff) == 0x7ff) | (((b2 >> 52) & 0x7ff) == 0x7ff) | (b1 <= 0) |
+                 (b2 <= 0);
+        };
+        if (badw(w1A, w2A) && bad_n == 0) bad_n = nA + 1;
+        if (two && badw(w1B, w2B) && bad_n == 0) bad_n = nA + 2;
+      }
+      __syncwarp();
+      if (own) {
+        const double iw1A = rcp_nr(w1A), iw2A = rcp_nr(w2A);
+        const double iw1B = rcp_nr(w1B), iw2B = rcp_nr(w2B);
+        const double h1A = g1A * iw1A, h2A = g2A * iw2A;
+        const double h1B = two ? g1B * iw1B : 0.0, h2B = two ? g2B * iw2B : 0.0;
+        accd1 = fma(t1A, iw1A, accd1);
+        accd2 = fma(t2A, iw2A, accd2);
+        if (two) {
+          accd1 = fma(t1B, iw1B, accd1);
+          accd2 = fma(t2B, iw2B, accd2);
+        }
+#pragma unroll
+        for (int so = 1; so <= NO; ++so) {
+          if (so == NO && (I % 2) == 0 && !ov[so]) continue;  // the half-filled last slot
+          const int cc = ob[so];
+          const double2 zcA = sz[cc], ggA = sgg[cc], zcB = szB[cc], ggB = sggB[cc];
+          const double xrA = fma(zrA, zcA.x, ziA * zcA.y), xiA = fma(ziA, zcA.x, -zrA * zcA.y);
+          const double xrB = fma(zrB, zcB.x, ziB * zcB.y), xiB = fma(ziB, zcB.x, -zrB * zcB.y);
+          const double k1A = h1A * ggA.x, k2A = h2A * ggA.y;
+          const double k1B = h1B * ggB.x, k2B = h2B * ggB.y;  // 0 for a missing frame
+          acc1[so] = fma(k1B, xrB, fma(k1A, xrA, acc1[so]));
+          acc1i[so] = fma(k1B, xiB, fma(k1A, xiA, acc1i[so]));
+          acc2[so] = fma(k2B, xrB, fma(k2A, xrA, acc2[so]));
+          acc2i[so] = fma(k2B, xiB, fma(k2A, xiA, acc2i[so]));
+        }
+      }
+      __syncwarp();  // the exchange buffers are rewritten by the next pair
+    }
+  } else {
 #pragma unroll
   for (int k = 0; k < kStages - 1; ++k) {
     if (k < K) issue(k);
@@ -245,6 +367,7 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, FAST_PAR_MINB) f
     }
     __syncwarp();  // sy / sz are rewritten by the next frame
   }
+  }
   cp_async_wait_all();
   if (bad_n && active && p.st)
     report_error(p.st, p.iter, FFCA_ERR_SINGULAR_MATRIX,
@@ -276,9 +399,10 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, FAST_PAR_MINB) f
 
 template <int I, typename R, bool UPDATE, bool LL, bool MU>
 static cudaError_t launch_fast_par_v(const FastIterParams& p, cudaStream_t s) {
-  using Lay = FastParLayout<I>;
+  constexpr bool PAIR = FFCA_K3P_PAIR && UPDATE && !LL && !MU;
+  using Lay = FastParLayout<I, PAIR>;
   dim3 grid((unsigned)((p.G + Lay::BPB - 1) / Lay::BPB), (unsigned)p.nchunk);
-  fast_par_kernel<I, R, UPDATE, LL, MU><<<grid, Lay::WARPS * 32, Lay::SMEM, s>>>(p);
+  fast_par_kernel<I, R, UPDATE, LL, MU, PAIR><<<grid, Lay::WARPS * 32, Lay::SMEM, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -317,12 +441,12 @@ int fast_par_blocks_per_sm(int I, int dtype) {
   case II:                                                                                      \
     if (f32)                                                                                    \
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                            \
-          &n, fast_par_kernel<II, float, true, false, false>, FastParLayout<II>::WARPS * 32,    \
-          FastParLayout<II>::SMEM);                                                              \
+          &n, fast_par_kernel<II, float, true, false, false, FFCA_K3P_PAIR>,                    \
+          FastParLayout<II>::WARPS * 32, FastParLayout<II, FFCA_K3P_PAIR>::SMEM);               \
     else                                                                                        \
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                            \
-          &n, fast_par_kernel<II, double, true, false, false>, FastParLayout<II>::WARPS * 32,   \
-          FastParLayout<II>::SMEM);                                                              \
+          &n, fast_par_kernel<II, double, true, false, false, FFCA_K3P_PAIR>,                   \
+          FastParLayout<II>::WARPS * 32, FastParLayout<II, FFCA_K3P_PAIR>::SMEM);               \
     break;
     FFCA_OCC(5)
     FFCA_OCC(6)
