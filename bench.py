@@ -377,8 +377,8 @@ def main():
     try:  # dram read+write per launch from the committed ncu --set full capture
         tj = json.loads((REPO / "profiles" / "traffic.json").read_text())
         for k, rec in tj.items():
-            if (args.engine == "fast" and args.dtype == "c128" and cfg.index == 3 and world == 1
-                    and "config 3" in k and "c128" in k):
+            if (args.engine == "fast" and args.dtype == "c128" and world == 1
+                    and f"config {cfg.index} " in k and "c128" in k):
                 traffic = rec["dram_bytes_per_launch"]
                 traffic_src = rec["source"]
     except Exception:
