@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pageable", action="store_true", help="skip the numpy-input e2e leg")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the extra resident lines (config 3 complex64, config 4)")
     ap.add_argument("--no-other", action="store_true", help="skip the second engine")
     ap.add_argument("--streams", type=int, default=2,
                     help="concurrent streams over independent mixtures (batched configs)")
@@ -187,6 +189,68 @@ def cpu_port_time(cfg, engine, sample, threads):
     from oracle import cpu_port
 
     return cpu_port.measure(cfg, engine, sample, threads)
+
+
+def resident_line(ecfg, dtype, engine, steps, inputs=None):
+    """One more resident-in-HBM measurement for the bench line's `extras`
+    (1 GPU, one stream, graph replays of the whole run): value, ms per run
+    and the update pass's roofline (CUDA events around each pass)."""
+    import torch
+
+    from paper_1805_06572_b200._engine import run_device, status_of, torch_types
+    from paper_1805_06572_b200.sharding import shard_chunk_frames
+
+    Y, V, S, FL = inputs if inputs is not None else make_inputs(ecfg, shard(ecfg, 0, 1))
+    ctype, rtype = torch_types(dtype)
+    y = torch.from_numpy(Y).cuda().to(ctype)
+    v = torch.from_numpy(V).cuda().to(rtype)
+    s0 = torch.from_numpy(S).cuda()
+    fl = torch.from_numpy(FL).cuda()
+    M, N, F, I = (int(x) for x in Y.shape)
+    cf = shard_chunk_frames(ecfg.M, ecfg.N, ecfg.F, ecfg.I, dtype, engine,
+                            max_world=ecfg.max_world)
+    bufs = {"images": torch.empty((M, 2, N, F, I), dtype=ctype, device="cuda"),
+            "S": torch.empty((M, 2, F, I, I), dtype=torch.complex128, device="cuda"),
+            "v": torch.empty_like(v)}
+
+    def run(graph=True, kernel_timing=False):
+        return run_device(engine, y, v, s0, fl, ecfg.L, likelihood=False, history=False,
+                          images=True, dtype=dtype, timing=False, check=False, out=bufs,
+                          chunk_frames=cf, graph=graph and not kernel_timing,
+                          kernel_timing=kernel_timing)
+
+    r = run(graph=False)
+    status_of(r, N, F)
+    bufs["workspace"] = r.workspace
+    for _ in range(2):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        r = run()
+    e1.record()
+    torch.cuda.synchronize()
+    status_of(r, N, F)
+    ms = e0.elapsed_time(e1) / steps
+    kr = run(kernel_timing=True)
+    status_of(kr, N, F)
+    hot = kr.kernel_ms[:-1] if len(kr.kernel_ms) > 1 else kr.kernel_ms
+    k_avg = statistics.mean(hot)
+    rb = 8 if dtype == "c128" else 4
+    alg = (2 * I + 4) * rb * M * F * N
+    peak, peak_kind = peaks()
+    ach = alg / (k_avg / 1e3) / 1e9
+    out = {"workload": ecfg.description, "engine": engine, "dtype": dtype,
+           "value": M * F * N * ecfg.L / (ms / 1e3), "unit": "TF-bin*it/s",
+           "ms_per_step": round(ms, 4), "steps": steps, "chunk_frames": cf,
+           "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                        "frac": round(ach / peak, 4), "algorithmic_bytes_per_launch": alg,
+                        "kernel_ms_avg": round(k_avg, 4), "launches_averaged": len(hot),
+                        "peak_source": peak_kind}}
+    del y, v, s0, fl, bufs, r, kr
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_reference(args, cfg):
@@ -514,6 +578,18 @@ def main():
                       "unit": "TF-bin*it/s", "ms_per_step": oms, "steps": osteps}
         del obufs
 
+    # the other headline lines on this GPU: config 3 complex64 (same draw, cast)
+    # and config 4 complex128, each with its own roofline block
+    extras = None
+    if (world == 1 and not args.no_extras and cfg.index == 3 and args.dtype == "c128"
+            and args.engine == "fast"):
+        del y_d, v_d, S_d, fl_d, bufs
+        torch.cuda.empty_cache()
+        extras = {"config3_c64": resident_line(cfg, "c64", "fast", max(2, args.steps // 2),
+                                               inputs=(Y, V, S, FL)),
+                  "config4_c128": resident_line(CONFIGS[4], "c128", "fast",
+                                                max(2, args.steps // 2))}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         # the unmodified reference (numba, baseline/_ref) on all host cores and
@@ -545,6 +621,7 @@ def main():
             "layout": {"streams_per_gpu": nstreams, "shard": list(sh), "grid": grid},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, **e2e_more,
             ("fca" if other == "fca" else "fastfca"): other_line,
+            "extras": extras,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
         }
