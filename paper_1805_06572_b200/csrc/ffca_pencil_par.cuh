@@ -160,7 +160,14 @@ FFCA_DEV bool par_jacobi(const BinView<I>& v, int M, int V, int r, bool act) {
     rotated = false;
 #pragma unroll 1
     for (int k = 0; k < n_rounds; ++k) {
-      if (r < Lay::NPAIR) rot[6 * r + 5] = 0.0;
+      if (r < Lay::NPAIR) {  // identity unless this lane's pair rotates
+        rot[6 * r + 0] = 1.0;
+        rot[6 * r + 1] = 0.0;
+        rot[6 * r + 2] = 1.0;
+        rot[6 * r + 3] = 0.0;
+        rot[6 * r + 5] = 0.0;
+      }
+      bool did = false;  // this lane's pair rotates this round
       if (act && r < Lay::NPAIR) {
         int p, q;
         rr_pair<I>(k, r, p, q);
@@ -187,19 +194,24 @@ FFCA_DEV bool par_jacobi(const BinView<I>& v, int M, int V, int r, bool act) {
             rp[2] = apq.x * rmag;
             rp[3] = -apq.y * rmag;
             rp[5] = 1.0;
+            did = true;
           }
         }
       }
       __syncwarp();
+      // a round in which no pair of any bin of the warp rotates (most rounds
+      // of the late sweeps, all of the final checking sweep) skips both
+      // update phases and their barriers
+      if (!__any_sync(0xffffffffu, did)) continue;
       bool any = false;
       if (act) {  // column update by row owner r: M[r][p], M[r][q], V[r][p], V[r][q]
 #pragma unroll
-        for (int i = 0; i < Lay::NPAIR; ++i) {
+        for (int i = 0; i < Lay::NPAIR; ++i) {  // branch-free: a still pair applies the identity
           const double* rp = rot + 6 * i;
-          if (rp[5] == 0.0) continue;
-          any = true;
+          any = any || rp[5] != 0.0;
           int p, q;
           rr_pair<I>(k, i, p, q);
+          if ((I % 2) && q >= I) continue;  // the odd order's resting player
           const double c = rp[0], sn = rp[1];
           const double2 emi = cmk(rp[2], rp[3]);
 #pragma unroll
@@ -217,9 +229,10 @@ FFCA_DEV bool par_jacobi(const BinView<I>& v, int M, int V, int r, bool act) {
 #pragma unroll
         for (int i = 0; i < Lay::NPAIR; ++i) {
           const double* rp = rot + 6 * i;
-          if (rp[5] == 0.0) continue;
+          const bool pin = rp[5] != 0.0;
           int p, q;
           rr_pair<I>(k, i, p, q);
+          if ((I % 2) && q >= I) continue;  // the odd order's resting player
           const double c = rp[0], sn = rp[1];
           const double2 epi = cmk(rp[2], -rp[3]);  // conj(emi)
           const double2 xp = v.at(M, p, r);
@@ -228,10 +241,10 @@ FFCA_DEV bool par_jacobi(const BinView<I>& v, int M, int V, int r, bool act) {
           double2 nq_ = cmk(sn * xp.x + c * xq.x, sn * xp.y + c * xq.y);
           // pin the rotated 2x2 block here (its column owners are p and q):
           // off-diagonal exactly zero, diagonal exactly real
-          if (r == p) {
+          if (pin && r == p) {
             np_.y = 0.0;
             nq_ = cmk(0.0, 0.0);
-          } else if (r == q) {
+          } else if (pin && r == q) {
             np_ = cmk(0.0, 0.0);
             nq_.y = 0.0;
           }
