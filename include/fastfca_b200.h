@@ -107,6 +107,12 @@ typedef struct ffca_run_args {
   const void* v_in; /* optional (M,2,N,F) initial powers, read only: the first pass reads
                        them here and writes `v` (which then need not be initialised);
                        NULL = `v` holds the initial powers (in place) */
+  int bin_parts;    /* FastFCA split-phase schedule: the bins in this many windows; window
+                       i's per-bin pencil refresh runs on a second (per-thread, per-device)
+                       stream while window i+1 streams, the passes chained with
+                       programmatic serialisation. 0 = auto (ffca_plan_parts), 1 = one
+                       window (plain schedule; also forced with FFCA_FLAG_HISTORY).
+                       Results are bitwise independent of it. */
 } ffca_run_args;
 
 /* ---- library info ------------------------------------------------------ */
@@ -121,6 +127,9 @@ int ffca_plan_chunks(int64_t G, int64_t N, int I, int dtype, int algorithm,
 /* Grid of the streaming pass for that plan (chunk_frames 0 = the auto plan):
  * *ctas = bin tiles x frame chunks, *slots = resident CTAs on the whole device
  * (SM count x CTAs per SM); ctas / slots = waves. Needs a device. */
+/* Bin windows the FastFCA driver pipelines (bin_parts = 0): 1 = none.
+ * Needs a device. */
+int ffca_plan_parts(int64_t G, int64_t N, int I, int dtype, int algorithm);
 int ffca_plan_grid(int64_t G, int64_t N, int I, int dtype, int algorithm, int64_t chunk_frames,
                    int64_t* ctas, int64_t* slots);
 size_t ffca_fastfca_workspace_size(int64_t M, int64_t N, int64_t F, int I, int iterations,

@@ -47,7 +47,7 @@ class DeviceRun:
 
 def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, history=False,
                images=True, dtype="c128", timing=True, check=True, out=None, chunk_frames=0,
-               kernel_timing=False, graph=False):
+               kernel_timing=False, graph=False, bin_parts=0):
     """Run ``iterations`` EM passes of FastFCA (``algorithm='fast'``) or
     conventional FCA (``'fca'``) entirely on the current CUDA stream.
 
@@ -58,6 +58,8 @@ def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, hi
     cached CUDA graph of the whole run when the arguments (buffers, sizes,
     flags) repeat — for repeated runs on preallocated ``out`` buffers; it is
     ignored when ``timing`` / ``kernel_timing`` events are requested.
+    ``bin_parts`` (FastFCA): bin windows of the split-phase schedule (0 =
+    the driver's plan, 1 = none); results do not depend on it.
     """
     lib = D.require()
     torch = D.torch
@@ -146,7 +148,7 @@ def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, hi
         chunk_frames=int(chunk_frames),
         kernel_events=ctypes.cast(kev_arr, ctypes.c_void_p).value if kev_arr is not None
         else None,
-        v_in=D.ptr(v_in).value)
+        v_in=D.ptr(v_in).value, bin_parts=int(bin_parts))
     fn = lib.ffca_fastfca_run if fast else lib.ffca_fca_run
     D.check_rc(fn(ctypes.byref(args), D.stream_handle()), fn.__name__)
     run = DeviceRun("FastFCA" if fast else "FCA", img, v, S_out, ll, S_hist, v_hist, [], ws)

@@ -57,6 +57,7 @@ class RunArgs(ctypes.Structure):
         ("S_out", c_vp), ("loglik", c_vp), ("S_hist", c_vp), ("v_hist", c_vp),
         ("workspace", c_vp), ("workspace_bytes", c_sz), ("iter_events", c_vp),
         ("chunk_frames", c_i64), ("kernel_events", c_vp), ("v_in", c_vp),
+        ("bin_parts", c_int),
     ]
 
 
@@ -66,6 +67,7 @@ SIGNATURES = [
     ("ffca_device_arch", c_int, []),
     ("ffca_plan_chunks", c_int,
      [c_i64, c_i64, c_int, c_int, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_int)]),
+    ("ffca_plan_parts", c_int, [c_i64, c_i64, c_int, c_int, c_int]),
     ("ffca_plan_grid", c_int,
      [c_i64, c_i64, c_int, c_int, c_int, c_i64, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     ("ffca_fastfca_workspace_size", c_sz,

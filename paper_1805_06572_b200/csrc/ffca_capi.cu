@@ -267,6 +267,66 @@ struct NvtxIter {  // one EM iteration's launches
   ~NvtxIter() { nvtxRangePop(); }
 };
 
+// the stream the split-phase schedule runs the pencil refreshes on: one per
+// (host thread, device), high priority so the refresh CTAs are placed ahead
+// of the queued streaming-pass CTAs as SM slots free up
+cudaStream_t side_stream() {
+  thread_local cudaStream_t ss[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!ss[dev]) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&ss[dev], cudaStreamNonBlocking, hi) != cudaSuccess)
+      ss[dev] = nullptr;
+  }
+  return ss[dev];
+}
+
+// FFCA_PDL=0: split-phase passes launched without programmatic serialisation
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FFCA_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// bin windows of the split-phase FastFCA schedule. The per-bin pencil refresh
+// (K1 / K1p) is latency bound (one thread / lane group per bin, a serial GEVD)
+// and in the plain schedule the GPU idles behind it every iteration (config
+// 4: K1p 45 of 500 us). With k windows, window i's refresh runs on a second
+// stream while window i+1 streams (the next pass launched with programmatic
+// serialisation, so it also fills the previous pass's last wave).
+// Measured (profiles/r02_split_phase.txt): config 4 +6% at k = 3-4; config 3
+// +-1% (K1 holds the whole register file while it runs: a throughput cost,
+// not a latency one); configs 0-2 lose (their passes are latency bound per
+// CTA, so a window's pass takes as long as a full one). The auto plan splits
+// only large single-mixture problems at I <= 4. FFCA_PARTS=k overrides.
+int auto_parts(int64_t M, int64_t F, int64_t N, int I, int dtype) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("FFCA_PARTS");
+    env = e ? atoi(e) : -1;
+  }
+  const int64_t G = M * F;
+  int k = env > 0 ? env : ((M == 1 && I <= 4 && G * N >= ((int64_t)4 << 20)) ? 3 : 1);
+  const int64_t maxk = G / bin_window_granularity(I, dtype);  // windows of >= one tile
+  if (k > maxk) k = (int)(maxk > 1 ? maxk : 1);
+  return k < 1 ? 1 : k;
+}
+
+int plan_parts(const ffca_run_args* a) {
+  const int64_t G = a->M * a->F;
+  if (a->flags & FFCA_FLAG_HISTORY) return 1;  // per-iteration v snapshots need a join
+  if (!pencil_window_capable(G, a->I)) return 1;
+  int k = a->bin_parts > 0 ? a->bin_parts : auto_parts(a->M, a->F, a->N, a->I, a->dtype);
+  const int64_t maxk = G / bin_window_granularity(a->I, a->dtype);
+  if (k > maxk) k = (int)(maxk > 1 ? maxk : 1);
+  return k < 1 ? 1 : (k > 16 ? 16 : k);
+}
+
 bool graph_mode(const ffca_run_args* a) {
   return (a->flags & FFCA_FLAG_GRAPH) && !a->iter_events && !a->kernel_events && !debug_sync();
 }
@@ -288,6 +348,12 @@ int ffca_plan_chunks(int64_t G, int64_t N, int I, int dtype, int algorithm,
   else
     plan_fast_chunks(G, N, I, dtype, chunk_frames, nchunk);
   return FFCA_OK;
+}
+
+int ffca_plan_parts(int64_t G, int64_t N, int I, int dtype, int algorithm) {
+  if (G < 1 || N < 1 || I < 1 || I > kMaxOrder) return FFCA_ERR_INVALID;
+  if (algorithm || !pencil_window_capable(G, I)) return 1;
+  return auto_parts(1, G, N, I, dtype);
 }
 
 int ffca_plan_grid(int64_t G, int64_t N, int I, int dtype, int algorithm, int64_t chunk_frames,
@@ -356,6 +422,109 @@ size_t ffca_fca_workspace_size(int64_t M, int64_t N, int64_t F, int I, int itera
   return a > b ? a : b;
 }
 
+// Split-phase EM loop (L >= 1, no history): the bins in k windows [e_i, e_i+1)
+// with tile-aligned edges. Main stream: pass(0, l), pass(1, l), ..., each
+// after its window's previous refresh; side stream: refresh(i, l) after
+// pass(i, l). So refresh(i, l) overlaps pass(i+1, l) (and the next
+// iteration's first passes), and every per-bin quantity sees exactly the
+// plain schedule's sequence of kernels (bitwise-identical results: the
+// windows only restrict which bins a launch covers). On return the main
+// stream has joined the side stream.
+static int fastfca_split_loop(const ffca_run_args* a, const FastWs& w, FastIterParams p, int k,
+                              cudaStream_t s) {
+  const int64_t G = a->M * a->F;
+  const int I = a->I, L = a->iterations;
+  const unsigned fl = a->flags;
+  const bool ll = fl & FFCA_FLAG_LIKELIHOOD;
+  const bool vin = a->v_in && a->v_in != a->v;
+  cudaEvent_t* ev = (cudaEvent_t*)a->iter_events;
+  cudaEvent_t* kev = (cudaEvent_t*)a->kernel_events;
+  const int gran = bin_window_granularity(I, a->dtype);
+  int64_t edge[17];
+  const int64_t tiles = (G + gran - 1) / gran;
+  int nw = 0;
+  edge[0] = 0;
+  for (int i = 1; i <= k; ++i) {
+    int64_t e = (i == k) ? G : ((tiles * i + k / 2) / k) * gran;
+    if (e > G) e = G;
+    if (e > edge[nw]) edge[++nw] = e;
+  }
+  cudaStream_t side = side_stream();
+  if (!side) return FFCA_ERR_CUDA;
+  int lo_prio = 0, hi_prio = 0;  // the refreshes are dispatched ahead of queued pass CTAs
+  cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+  // events: fork, pass_done[i], ref_done[i] (re-recorded every iteration;
+  // each wait binds to the latest record enqueued before it)
+  cudaEvent_t evs[1 + 2 * 16];
+  int ne = 0;
+  int rc = FFCA_OK;
+  for (; ne < 1 + 2 * nw; ++ne)
+    if (cudaEventCreateWithFlags(&evs[ne], cudaEventDisableTiming) != cudaSuccess) {
+      rc = FFCA_ERR_CUDA;
+      break;
+    }
+  cudaEvent_t* pass_done = evs + 1;
+  cudaEvent_t* ref_done = evs + 1 + nw;
+#define FFCA_TRY_S(expr)                                  \
+  do {                                                    \
+    rc = cu(checked((expr), #expr, __LINE__));            \
+    if (rc != FFCA_OK) goto done;                         \
+  } while (0)
+  if (rc != FFCA_OK) goto done;
+  FFCA_TRY_S(cudaEventRecord(evs[0], s));
+  FFCA_TRY_S(cudaStreamWaitEvent(side, evs[0], 0));
+  for (int l = 0; l < L; ++l) {
+    const NvtxIter nvtx_it(l);
+    if (ev) FFCA_TRY_S(cudaEventRecord(ev[l], s));
+    const bool last = (l == L - 1);
+    for (int i = 0; i < nw; ++i) {
+      if (l > 0) FFCA_TRY_S(cudaStreamWaitEvent(s, ref_done[i], 0));
+      if (kev && i == 0) FFCA_TRY_S(cudaEventRecord(kev[2 * l], s));
+      p.update = 1;
+      p.mu_out = (last && (fl & FFCA_FLAG_IMAGES)) ? a->images : nullptr;
+      p.mu_back = 1;
+      p.iter = l + 1;
+      p.v_src = (vin && l == 0) ? a->v_in : nullptr;
+      p.g0 = edge[i];
+      p.g1 = edge[i + 1];
+      // passes over different windows are independent: each may start while
+      // the previous one (the last pass on the stream) drains
+      p.pdl = (l > 0 || i > 0) && pdl_enabled();
+      FFCA_TRY_S(launch_fast_em(p, I, a->dtype, s));
+      if (kev && i == nw - 1) FFCA_TRY_S(cudaEventRecord(kev[2 * l + 1], s));
+      FFCA_TRY_S(cudaEventRecord(pass_done[i], s));
+      FFCA_TRY_S(cudaStreamWaitEvent(side, pass_done[i], 0));
+      PencilParams q{};
+      q.Spart = w.Spart;
+      q.nchunk = w.nchunk;
+      q.N = a->N;
+      q.G = G;
+      q.F = a->F;
+      q.P = w.P;
+      q.W = w.W;
+      q.lam = w.lam;
+      q.logdet2 = w.logdet2;
+      q.S_model = last ? (double2*)a->S_out : nullptr;
+      q.S_hist = nullptr;
+      q.llbin = ll ? w.llbin : nullptr;
+      q.llg = ll ? w.llg + (size_t)l * G : nullptr;
+      q.st = w.st;
+      q.iter = l + 1;
+      q.St = w.St;
+      q.g0 = edge[i];
+      q.g1 = edge[i + 1];
+      q.prio = hi_prio;
+      FFCA_TRY_S(launch_pencil_update(q, I, side));
+      FFCA_TRY_S(cudaEventRecord(ref_done[i], side));
+    }
+  }
+  for (int i = 0; i < nw; ++i) FFCA_TRY_S(cudaStreamWaitEvent(s, ref_done[i], 0));
+#undef FFCA_TRY_S
+done:
+  for (int i = 0; i < ne; ++i) cudaEventDestroy(evs[i]);
+  return rc;
+}
+
 static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
   int rc = 0;
   const int64_t M = a->M, N = a->N, F = a->F, G = M * F;
@@ -405,6 +574,16 @@ static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
     if (ll) FFCA_TRY(launch_ll_collect(w.llbin, w.nchunk, w.logdet2, N, G, w.llg, s));
     FFCA_TRY(cudaMemcpyAsync(a->S_out, a->S0, Sslice * sizeof(double2),
                              cudaMemcpyDeviceToDevice, s));
+  } else if (plan_parts(a) > 1) {
+    if ((rc = fastfca_split_loop(a, w, p, plan_parts(a), s))) return rc;
+    if (ev) FFCA_TRY(cudaEventRecord(ev[L], s));
+    if (ll) {
+      p.update = 0;
+      p.mu_out = nullptr;
+      p.iter = L + 1;
+      FFCA_TRY(launch_fast_em(p, I, a->dtype, s));
+      FFCA_TRY(launch_ll_collect(w.llbin, w.nchunk, w.logdet2, N, G, w.llg + (size_t)L * G, s));
+    }
   } else {
     for (int l = 0; l < L; ++l) {
       const NvtxIter nvtx_it(l);

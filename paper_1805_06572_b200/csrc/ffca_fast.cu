@@ -82,6 +82,11 @@ int fast_update_blocks_per_sm(int I, int dtype) {
   return cache[I];
 }
 
+int bin_window_granularity(int I, int dtype) {
+  const int t = fast_tile_bins(I, dtype);  // K3 32 / K3t 128 / K3p 8; K1p 8-32
+  return t > 32 ? t : 32;
+}
+
 void plan_fast_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames,
                       int* nchunk) {
   if (I >= 5)

@@ -475,6 +475,7 @@ constexpr int fast2_minb() {
 template <int I, typename R, int WARPS, int STAGES, bool UPDATE, bool LL, bool MU,
           bool BULK = false>
 __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>())) fast_em2_kernel(const FastIterParams p) {
+  pdl_release_dependents();
   using C = typename CplxOf<R>::type;
   using Slot = RingSlot<I, R>;
   using T = typename Math<R>::T;    // per-point compute type
@@ -488,7 +489,8 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t G = p.G;
-  int64_t g = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t tile0 = p.g0 + (int64_t)blockIdx.x * 32;  // (window edges are tile edges)
+  int64_t g = tile0 + lane;
   const bool active = g < G;
   if (!active) g = G - 1;
   const int64_t m = g / p.F;
@@ -571,7 +573,6 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
   // tile's 32 bins lie in one mixture (and none is clamped) the row is one
   // contiguous run and copy c reads ybase + 32 c UB; a tile across a mixture
   // boundary (or the last, partial tile) adds a per-copy correction.
-  const int64_t tile0 = (int64_t)blockIdx.x * 32;
   const bool contiguous = (tile0 + 31 < G) && (tile0 / p.F == (tile0 + 31) / p.F);
   const int spos0 = Slot::pos(lane / Slot::Q, lane % Slot::Q);
   const int rb = Slot::rbase(lane);
@@ -1110,9 +1111,8 @@ cudaError_t launch_fast2_kern(const FastIterParams& p, cudaStream_t s) {
   auto kern = fast_em2_kernel<I, R, WARPS, STAGES, UPDATE, LL, MU, BULK>;
   if (cudaError_t e = ensure_smem<fast_em2_kernel<I, R, WARPS, STAGES, UPDATE, LL, MU, BULK>>(Sm::BYTES))
     return e;
-  dim3 grid((unsigned)((p.G + 31) / 32), (unsigned)p.nchunk);
-  kern<<<grid, WARPS * 32, Sm::BYTES, s>>>(p);
-  return cudaGetLastError();
+  dim3 grid((unsigned)((window_end(p.g1, p.G) - p.g0 + 31) / 32), (unsigned)p.nchunk);
+  return launch_ex(kern, grid, dim3(WARPS * 32), Sm::BYTES, s, p.pdl != 0, 0, p);
 }
 
 template <int I, typename R, bool UPDATE, bool LL, bool MU>

@@ -50,6 +50,7 @@ struct FastParLayout {
 #endif
 template <int I, typename R, bool UPDATE, bool LL, bool MU, bool PAIR = false>
 __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, PAIR ? FAST_PAR_PAIR_MINB : FAST_PAR_MINB) fast_par_kernel(const FastIterParams p) {
+  pdl_release_dependents();
   static_assert(!PAIR || (UPDATE && !LL && !MU), "the paired loop is the update-only pass");
   using Lay = FastParLayout<I, PAIR>;
   using C = typename CplxOf<R>::type;
@@ -60,7 +61,7 @@ __global__ void __launch_bounds__(FastParLayout<I>::WARPS * 32, PAIR ? FAST_PAR_
   const int r = lane % LB;
   const int grp = warp * (32 / LB) + lane / LB;
   const int64_t G = p.G;
-  int64_t g = (int64_t)blockIdx.x * Lay::BPB + grp;
+  int64_t g = p.g0 + (int64_t)blockIdx.x * Lay::BPB + grp;
   const bool active = g < G;
   if (!active) g = G - 1;
   const bool own = r < I;
@@ -401,9 +402,10 @@ template <int I, typename R, bool UPDATE, bool LL, bool MU>
 static cudaError_t launch_fast_par_v(const FastIterParams& p, cudaStream_t s) {
   constexpr bool PAIR = FFCA_K3P_PAIR && UPDATE && !LL && !MU;
   using Lay = FastParLayout<I, PAIR>;
-  dim3 grid((unsigned)((p.G + Lay::BPB - 1) / Lay::BPB), (unsigned)p.nchunk);
-  fast_par_kernel<I, R, UPDATE, LL, MU, PAIR><<<grid, Lay::WARPS * 32, Lay::SMEM, s>>>(p);
-  return cudaGetLastError();
+  dim3 grid((unsigned)((window_end(p.g1, p.G) - p.g0 + Lay::BPB - 1) / Lay::BPB),
+            (unsigned)p.nchunk);
+  return launch_ex(fast_par_kernel<I, R, UPDATE, LL, MU, PAIR>, grid, dim3(Lay::WARPS * 32),
+                   Lay::SMEM, s, p.pdl != 0, 0, p);
 }
 
 template <int I, typename R>

@@ -50,6 +50,7 @@ constexpr size_t tma_smem_bytes() {
 
 template <int I, int STAGES>
 __global__ void __launch_bounds__(TmaLayout<I>::TB, 3) fast_tma_kernel(const FastIterParams p) {
+  pdl_release_dependents();
   using Lay = TmaLayout<I>;
   using Slot = RingSlot<I, double>;
   constexpr int TB = Lay::TB, NP = Lay::NP, YB = Lay::YB, VB = Lay::VB;
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(TmaLayout<I>::TB, 3) fast_tma_kernel(const Fas
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = threadIdx.x;  // bin within the tile
   const int64_t G = p.G, F = p.F, N = p.N, NF = N * F;
-  const int64_t tile0 = (int64_t)blockIdx.x * TB;
+  const int64_t tile0 = p.g0 + (int64_t)blockIdx.x * TB;
   int64_t g = tile0 + b;
   const bool active = g < G;
   if (!active) g = G - 1;
@@ -266,8 +267,11 @@ template <int I>
 cudaError_t launch_fast_tma(const FastIterParams& p, cudaStream_t s) {
   constexpr size_t SM = tma_smem_bytes<I>();
   if (cudaError_t e = ensure_smem<fast_tma_kernel<I, FFCA_K3T_STAGES>>(SM)) return e;
-  dim3 grid((unsigned)((p.G + TmaLayout<I>::TB - 1) / TmaLayout<I>::TB), (unsigned)p.nchunk);
-  fast_tma_kernel<I, FFCA_K3T_STAGES><<<grid, TmaLayout<I>::TB, SM, s>>>(p);
+  dim3 grid((unsigned)((window_end(p.g1, p.G) - p.g0 + TmaLayout<I>::TB - 1) / TmaLayout<I>::TB),
+            (unsigned)p.nchunk);
+  if (cudaError_t e = launch_ex(fast_tma_kernel<I, FFCA_K3T_STAGES>, grid, dim3(TmaLayout<I>::TB),
+                                SM, s, p.pdl != 0, 0, p))
+    return e;
   return cudaGetLastError();
 }
 

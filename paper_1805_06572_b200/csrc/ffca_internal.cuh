@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <utility>
 
 #include "ffca_common.cuh"
 
@@ -51,7 +52,50 @@ struct FastIterParams {
   int nchunk;
   ffca_status_dev* st;
   int iter;
+  // bin window [g0, g1) of this launch (g1 = 0: to G). g0 is a multiple of
+  // the pass's bin tile and g1 is one too or G (bin_window_granularity)
+  int64_t g0, g1;
+  // launch with programmatic stream serialisation: this pass may start while
+  // the previous kernel on the stream (a pass over OTHER bins) drains
+  int pdl;
 };
+// every CTA of a streaming pass releases its programmatic dependents on entry:
+// a pass over other bins launched after it with FastIterParams::pdl fills
+// the SM slots of its last partial wave instead of waiting for its drain
+__device__ __forceinline__ void pdl_release_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// kernel launch with the optional programmatic-serialisation attribute
+// and an optional scheduling priority (0: the stream's; else a value in the
+// device's stream-priority range, lower = more urgent; kept in graph nodes)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t s, bool pdl, int prio, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (prio) {
+    attr[n].id = cudaLaunchAttributePriority;
+    attr[n].val.priority = prio;
+    ++n;
+  }
+  cfg.attrs = n ? attr : nullptr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+// bins per window step: every window edge is a tile edge of the update pass
+// (K3 / K3t / K3p) and of the pencil refresh (K1 / K1p)
+int bin_window_granularity(int I, int dtype);
+__host__ __device__ inline int64_t window_end(int64_t g1, int64_t G) { return g1 > 0 ? g1 : G; }
 cudaError_t launch_fast_em(const FastIterParams& p, int I, int dtype, cudaStream_t s);
 
 // ---- K4: fused conventional FCA iteration (+ likelihood, + mu) -------------
@@ -90,7 +134,12 @@ struct PencilParams {
   ffca_status_dev* st;
   int iter;
   double2* St;  // [2][G][I][I] scratch for the split path (I >= 5)
+  int64_t g0, g1;  // bin window (g1 = 0: to G), as FastIterParams
+  int prio;        // launch priority (0: the stream's), see launch_ex
 };
+// whether launch_pencil_update honours a bin window (the 3-kernel I >= 5
+// path, FFCA_K1=thread, does not)
+bool pencil_window_capable(int64_t G, int I);
 cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s);
 
 // initial pencil from S0 (M,2,F,I,I): P, W, lam, logdet2 (fast.py:127-130)

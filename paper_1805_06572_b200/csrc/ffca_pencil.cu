@@ -154,8 +154,8 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
 template <int I>
 __global__ void __launch_bounds__(FFCA_K1_THREADS, FFCA_K1_MINB) pencil_update_kernel(const PencilParams p) {
   constexpr int NP = I * I;
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= p.G) return;
+  const int64_t g = p.g0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= window_end(p.g1, p.G)) return;
   double2 S1[I][I], S2[I][I], Pe[I][I];
   pencil_prep<I>(p, g, S1, S2, Pe);
 
@@ -315,6 +315,8 @@ cudaError_t launch_initial_par(const double2* S0, double2* P, double2* W, double
 // config 4, 46 vs 65 us); the one-thread-per-bin kernel for I <= 3 at any
 // size (configs 0/1: 0.28 vs 0.34 ms and 2.25 vs 2.66 ms per run) and for
 // big I = 4 batches. FFCA_K1=par|thread overrides (experiments).
+static bool use_par(int64_t G, int I);
+bool pencil_window_capable(int64_t G, int I) { return use_par(G, I) || I <= 4; }
 static bool use_par(int64_t G, int I) {
   static int mode = -1;
   if (mode < 0) {
@@ -330,12 +332,12 @@ cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s) {
   if (use_par(p.G, I)) return launch_pencil_par(p, I, s);
   if (I <= 4) {  // fused single kernel; only instantiated for I <= 4
     constexpr int T = FFCA_K1_THREADS;
-    const unsigned nb = nblk(p.G, T);
+    const unsigned nb = nblk(window_end(p.g1, p.G) - p.g0, T);
     switch (I) {
-      case 1: pencil_update_kernel<1><<<nb, T, 0, s>>>(p); break;
-      case 2: pencil_update_kernel<2><<<nb, T, 0, s>>>(p); break;
-      case 3: pencil_update_kernel<3><<<nb, T, 0, s>>>(p); break;
-      default: pencil_update_kernel<4><<<nb, T, 0, s>>>(p); break;
+      case 1: return launch_ex(pencil_update_kernel<1>, dim3(nb), dim3(T), 0, s, false, p.prio, p);
+      case 2: return launch_ex(pencil_update_kernel<2>, dim3(nb), dim3(T), 0, s, false, p.prio, p);
+      case 3: return launch_ex(pencil_update_kernel<3>, dim3(nb), dim3(T), 0, s, false, p.prio, p);
+      default: return launch_ex(pencil_update_kernel<4>, dim3(nb), dim3(T), 0, s, false, p.prio, p);
     }
     return cudaGetLastError();
   }

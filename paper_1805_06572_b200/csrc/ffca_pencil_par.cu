@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(ParLayout<I>::WARPS * 32) pencil_par_kernel(co
   const int r = lane % Lay::LB;
   const int bb = warp * Lay::BPW + lane / Lay::LB;
   const int64_t G = p.G;
-  int64_t g = (int64_t)blockIdx.x * Lay::BPB + bb;
+  int64_t g = p.g0 + (int64_t)blockIdx.x * Lay::BPB + bb;
   const bool active = g < G;
   if (!active) g = G - 1;
   const bool own = r < I;
@@ -285,8 +285,10 @@ template <int I>
 static cudaError_t launch_par_t(const PencilParams& p, cudaStream_t s) {
   using Lay = ParLayout<I>;
   if (cudaError_t e = ensure_smem<pencil_par_kernel<I>>(Lay::SMEM)) return e;
-  const unsigned nb = (unsigned)((p.G + Lay::BPB - 1) / Lay::BPB);
-  pencil_par_kernel<I><<<nb, Lay::WARPS * 32, Lay::SMEM, s>>>(p);
+  const unsigned nb = (unsigned)((window_end(p.g1, p.G) - p.g0 + Lay::BPB - 1) / Lay::BPB);
+  if (cudaError_t e = launch_ex(pencil_par_kernel<I>, dim3(nb), dim3(Lay::WARPS * 32), Lay::SMEM,
+                                s, false, p.prio, p))
+    return e;
   return cudaGetLastError();
 }
 

@@ -57,7 +57,9 @@ def test_library_is_sm100a():
 
 def test_run_args_layout_matches_c():
     # 3 int64 + 4 int32 + 10 pointers + size_t + pointer + int64 + 2 pointers
-    assert ctypes.sizeof(_lib.RunArgs) == 24 + 16 + 8 * 10 + 8 + 8 + 8 + 8 + 8
+    # + int bin_parts (padded to 8)
+    assert ctypes.sizeof(_lib.RunArgs) == 24 + 16 + 8 * 10 + 8 + 8 + 8 + 8 + 8 + 8
+    assert _lib.RunArgs.bin_parts.offset == 160
 
 
 def test_workspace_size_query_needs_no_device():
