@@ -340,6 +340,29 @@ struct FrameRing {
     v1 = (double)((const R*)vs)[lane];
     v2 = (double)((const R*)(vs + 32 * sizeof(R)))[lane];
   }
+  // the same in two steps (K4: the observation is not needed, and not kept
+  // in registers, while R is inverted): powers first, y from `cur` later
+  FFCA_DEV void load_v(double& v1, double& v2) {
+    cur = wslots + read_stage;
+    read_stage = read_stage + kStride == STAGES * kStride ? 0 : read_stage + kStride;
+    const unsigned char* vs = cur + 32 * Slot::YB;
+    v1 = (double)((const R*)vs)[lane];
+    v2 = (double)((const R*)(vs + 32 * sizeof(R)))[lane];
+  }
+  FFCA_DEV void load_y(double2 (&yv)[I]) const {
+    constexpr int PER = Slot::UB / (int)sizeof(C);
+#pragma unroll
+    for (int a = 0; a < Slot::Q; ++a) {
+      const unsigned char* src = cur + Slot::rpos(rb, a);
+      if constexpr (PER == 2) {
+        const float4 q = *(const float4*)src;
+        yv[2 * a] = cmk(q.x, q.y);
+        yv[2 * a + 1] = cmk(q.z, q.w);
+      } else {
+        yv[a] = to_c128(*(const C*)src);
+      }
+    }
+  }
 };
 
 // Warp-cooperative store of one frame's posterior means (images) of the

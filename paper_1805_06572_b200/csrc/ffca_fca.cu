@@ -29,6 +29,12 @@ namespace ffca {
 #ifndef FFCA_K4_RING_FIRST
 #define FFCA_K4_RING_FIRST 0  // 1: issue the frame ring before loading S1, S2
 #endif
+#ifndef FFCA_K4_SWEEP
+#define FFCA_K4_SWEEP 1  // frame-wise inverse by the Hermitian sweep (0: Cholesky chain)
+#endif
+#ifndef FFCA_K4_XX_RECOMPUTE
+#define FFCA_K4_XX_RECOMPUTE 1  // form the x x^H entries twice instead of holding I^2 registers (config 3 FCA 22.2 -> 22.7 G)
+#endif
 #ifndef FFCA_FCA_MINB
 #define FFCA_FCA_MINB 1  // CTAs per SM the I <= 4 pass is register-budgeted for
 #endif
@@ -37,6 +43,14 @@ namespace ffca {
 // write) are compile-time variants, so the hot update-only pass carries
 // neither the image nor the likelihood code (register pressure: the fused
 // runtime-branch kernel spilled ~550 B per thread at I = 4).
+// shared-memory load the compiler may not merge with an earlier load of the
+// same address
+__device__ __forceinline__ double lds_reload(unsigned addr) {
+  double v;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 template <int I, typename R, int WARPS, bool UPDATE, bool LL, bool MU>
 __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const FcaIterParams p) {
   using C = typename CplxOf<R>::type;
@@ -81,6 +95,7 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
   }
   if (FFCA_K4_RING_FIRST) load_tile();  // (S1, S2 after the ring prologue)
 
+  const unsigned sS_addr = (unsigned)__cvta_generic_to_shared(sS + lane);
   auto Sget = [&](int which, int a, int b) -> double2 {
     // full entry (a, b) of packed Hermitian matrix `which`
     const double* base = sS + which * NP * 32 + lane;
@@ -107,7 +122,30 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
     __syncwarp();  // the other lanes' copies of this stage are visible
     double2 yv[I];
     double v1, v2;
+#if FFCA_K4_SWEEP
+    ring.load_v(v1, v2);
+#else
     ring.load(yv, v1, v2);
+#endif
+#if FFCA_K4_SWEEP
+    // R = v1 S1 + v2 S2 (packed Hermitian) inverted in place by the
+    // symmetric sweep (herm_sweep_inverse): Ri = R^-1, the pivots' product is
+    // det R, and R is singular / indefinite iff a pivot is <= 0
+    double Ri[NP];
+    double detR;
+    {
+      // (volatile loads: S1, S2 are loop invariant, and plain loads get hoisted
+      // out of the frame loop into 2 I^2 registers' worth of spills)
+#pragma unroll
+      for (int e = 0; e < NP; ++e)
+        Ri[e] = fma(v1, lds_reload(sS_addr + (unsigned)(e * 32) * 8u),
+                    v2 * lds_reload(sS_addr + (unsigned)((NP + e) * 32) * 8u));
+      const bool ok = herm_sweep_inverse<I>(Ri, detR);
+      if (!ok && bad_n == 0) bad_n = n + 1;
+    }
+    asm volatile("" ::: "memory");  // y is loaded after the inversion (register budget)
+    ring.load_y(yv);
+#else
     // R = v1 S1 + v2 S2 and its Cholesky factor
     double2 Lm[I][I];
     [[maybe_unused]] double ild[I];
@@ -145,6 +183,7 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
           Ri[Herm<I>::im(a, b)] = s.y;
         }
       }
+#endif
     double2 x[I];
 #pragma unroll
     for (int a = 0; a < I; ++a) {
@@ -160,13 +199,17 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
     }
     if constexpr (LL) {
       // log det R + y^H R^{-1} y = 2 sum log L_ii + Re(y^H x)
-      double prod = 1.0, quad = 0.0;
+      double quad = 0.0;
 #pragma unroll
-      for (int a = 0; a < I; ++a) {
-        prod *= Lm[a][a].x;
-        quad += yv[a].x * x[a].x + yv[a].y * x[a].y;
-      }
+      for (int a = 0; a < I; ++a) quad += yv[a].x * x[a].x + yv[a].y * x[a].y;
+#if FFCA_K4_SWEEP
+      llacc += log(detR) + quad;
+#else
+      double prod = 1.0;
+#pragma unroll
+      for (int a = 0; a < I; ++a) prod *= Lm[a][a].x;
       llacc += 2.0 * log(prod) + quad;
+#endif
     }
     if constexpr (MU) {
       // mu_j = v_j S_j x (the posterior means; written by the image pass
@@ -201,26 +244,41 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
     //   mu_j^H S_j^-1 mu_j = v_j^2 x^H S_j x = v_j^2 tr(S_j x x^H)
     //   tr(S_1^-1 v1 v2 S1 Rinv S2) = v1 v2 tr(Rinv S2), tr(S_2^-1 ...) = v1 v2 tr(Rinv S1)
     // every term is non-negative (no cancellation).
-    double xx[NP];  // x x^H, packed: |x_a|^2, x_a conj(x_b)
+    // x x^H, packed (|x_a|^2, x_a conj(x_b)); with FFCA_K4_XX_RECOMPUTE the
+    // entries are formed from x where they are used (twice: traces and sums)
+    // instead of held in I^2 registers across the power update
+    auto xx_entry = [&](int e) -> double {
+      if (e < I) return cabs2(x[e]);
+      int a = 0, b = 1;
 #pragma unroll
-    for (int a = 0; a < I; ++a) {
-      xx[a] = cabs2(x[a]);
+      for (int aa = 0; aa < I; ++aa)
 #pragma unroll
-      for (int b = a + 1; b < I; ++b) {
-        const double2 e = cmulc(x[a], x[b]);
-        xx[Herm<I>::re(a, b)] = e.x;
-        xx[Herm<I>::im(a, b)] = e.y;
-      }
-    }
-    const double* S1p = sS + lane;
-    const double* S2p = sS + NP * 32 + lane;
+        for (int bb = aa + 1; bb < I; ++bb)
+          if (Herm<I>::re(aa, bb) == e || Herm<I>::im(aa, bb) == e) {
+            a = aa;
+            b = bb;
+          }
+      return e == Herm<I>::re(a, b) ? fma(x[a].x, x[b].x, x[a].y * x[b].y)
+                                    : fma(x[a].y, x[b].x, -x[a].x * x[b].y);
+    };
+#if FFCA_K4_XX_RECOMPUTE
+#define FFCA_XX(e) xx_entry(e)
+#else
+    double xx[NP];
+#pragma unroll
+    for (int e = 0; e < NP; ++e) xx[e] = xx_entry(e);
+#define FFCA_XX(e) xx[e]
+#endif
+    // S1, S2 re-read from shared memory (volatile, as for R)
     double qf1 = 0.0, qf2 = 0.0, tR1 = 0.0, tR2 = 0.0;
 #pragma unroll
     for (int e = 0; e < NP; ++e) {
-      const double s1 = S1p[e * 32], s2 = S2p[e * 32];
+      const double s1 = lds_reload(sS_addr + (unsigned)(e * 32) * 8u);
+      const double s2 = lds_reload(sS_addr + (unsigned)((NP + e) * 32) * 8u);
       const double wgt = e < I ? 1.0 : 2.0;  // compile-time after unrolling
-      qf1 = fma(wgt * s1, xx[e], qf1);
-      qf2 = fma(wgt * s2, xx[e], qf2);
+      const double xe = FFCA_XX(e);
+      qf1 = fma(wgt * s1, xe, qf1);
+      qf2 = fma(wgt * s2, xe, qf2);
       tR1 = fma(wgt * s1, Ri[e], tR1);
       tR2 = fma(wgt * s2, Ri[e], tR2);
     }
@@ -233,14 +291,20 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
       vb[n * p.F] = (R)w1;
       vb[NF + n * p.F] = (R)w2;
     }
+#if FFCA_K4_XX_RECOMPUTE
+#pragma unroll
+    for (int a = 0; a < I; ++a)  // opaque: the x x^H entries below are formed again
+      asm volatile("" : "+d"(x[a].x), "+d"(x[a].y));
+#endif
     const double iw1 = kFastMath ? rcp_fast(w1) : 1.0 / w1;
     const double iw2 = kFastMath ? rcp_fast(w2) : 1.0 / w2;
     const double cb1 = v1 * v1 * iw1, cb2 = v2 * v2 * iw2;
     const double cx1 = vv * iw1, cx2 = vv * iw2;
 #pragma unroll
     for (int e = 0; e < NP; ++e) {
-      acc[0][e] = fma(cb1, xx[e], acc[0][e]);
-      acc[1][e] = fma(cb2, xx[e], acc[1][e]);
+      const double xe = FFCA_XX(e);
+      acc[0][e] = fma(cb1, xe, acc[0][e]);
+      acc[1][e] = fma(cb2, xe, acc[1][e]);
       acc[2][e] = fma(cx1, Ri[e], acc[2][e]);
       acc[3][e] = fma(cx2, Ri[e], acc[3][e]);
     }
