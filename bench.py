@@ -217,7 +217,10 @@ def resident_line(ecfg, dtype, engine, steps, inputs=None):
         return run_device(engine, y, v, s0, fl, ecfg.L, likelihood=False, history=False,
                           images=True, dtype=dtype, timing=False, check=False, out=bufs,
                           chunk_frames=cf, graph=graph and not kernel_timing,
-                          kernel_timing=kernel_timing)
+                          kernel_timing=kernel_timing,
+                          # kernel events bracket ONE whole-grid pass launch per iteration
+                          # (plain schedule), not the split-phase windows' stream waits
+                          bin_parts=1 if kernel_timing else 0)
 
     r = run(graph=False)
     status_of(r, N, F)
@@ -369,7 +372,8 @@ def main():
     def step(timing=False):  # untimed-event steps replay a cached CUDA graph of the run
         return run_device(args.engine, y_d, v_d, S_d, fl_d, L, likelihood=False, history=False,
                           images=True, dtype=args.dtype, timing=timing, check=False,
-                          chunk_frames=cf, kernel_timing=timing, out=bufs, graph=not timing)
+                          chunk_frames=cf, kernel_timing=timing, out=bufs, graph=not timing,
+                          bin_parts=1 if timing else 0)  # (kernel events: whole-grid passes)
 
     bufs["workspace"] = step().workspace
     nstreams = args.streams if M > 1 else 1

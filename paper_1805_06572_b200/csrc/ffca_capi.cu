@@ -65,6 +65,7 @@ struct FastWs {
   ffca_status_dev* st;
   double2 *P, *W, *St;
   double *lam, *logdet2, *Spart, *llbin, *llg;
+  int* sync;  // KP: 2 * tiles + 1 ints (arrival counters, tile generations, abort word)
   int64_t chunk_frames;
   int nchunk;
   size_t bytes;
@@ -81,8 +82,11 @@ FastWs carve_fast(void* base, int64_t M, int64_t N, int64_t F, int I, int L, uns
                   int64_t cf_req, int dtype) {
   FastWs w{};
   const int64_t G = M * F;
-  if (!chunk_override(N, cf_req, &w.chunk_frames, &w.nchunk))
-    plan_fast_chunks(G, N, I, dtype, &w.chunk_frames, &w.nchunk);
+  if (!chunk_override(N, cf_req, &w.chunk_frames, &w.nchunk)) {
+    const bool kp = (flags & FFCA_FLAG_PERSIST) && !(flags & (FFCA_FLAG_LIKELIHOOD | FFCA_FLAG_HISTORY));
+    if (!(kp && plan_persist_chunks(G, N, I, dtype, &w.chunk_frames, &w.nchunk)))
+      plan_fast_chunks(G, N, I, dtype, &w.chunk_frames, &w.nchunk);
+  }
   Carve c(base);
   w.st = c.take<ffca_status_dev>(1);
   w.P = c.take<double2>(G * I * I);
@@ -90,6 +94,7 @@ FastWs carve_fast(void* base, int64_t M, int64_t N, int64_t F, int I, int L, uns
   w.lam = c.take<double>(G * I);
   w.logdet2 = c.take<double>(G);
   w.Spart = c.take<double>((size_t)w.nchunk * 2 * I * I * G);
+  w.sync = c.take<int>(2 * ((G + 31) / 32) + 1);
   const bool ll = flags & FFCA_FLAG_LIKELIHOOD;
   w.llbin = ll ? c.take<double>((size_t)w.nchunk * G) : nullptr;
   w.llg = ll ? c.take<double>((size_t)(L + 1) * G) : nullptr;
@@ -585,7 +590,37 @@ static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
       FFCA_TRY(launch_ll_collect(w.llbin, w.nchunk, w.logdet2, N, G, w.llg + (size_t)L * G, s));
     }
   } else {
-    for (int l = 0; l < L; ++l) {
+    // KP: the first L - 1 iterations of a small problem in one persistent
+    // launch (the last pass writes the images: a stand-alone launch)
+    int l0 = 0;
+    const int64_t tiles = (G + 31) / 32;
+    if (L >= 3 && !ll && !hist && !ev && !kev &&
+        ((fl & FFCA_FLAG_PERSIST) || fast_persist_env()) &&
+        fast_persist_shape(G, N, I, a->dtype) &&
+        tiles * (w.nchunk + 1) <= fast_persist_slots(I)) {
+      FFCA_TRY(cudaMemsetAsync(w.sync, 0, (2 * tiles + 1) * sizeof(int), s));
+      p.update = 1;
+      p.mu_out = nullptr;
+      p.mu_back = 1;
+      p.v_src = vin ? a->v_in : nullptr;
+      PencilParams q{};
+      q.Spart = w.Spart;
+      q.nchunk = w.nchunk;
+      q.N = N;
+      q.G = G;
+      q.F = F;
+      q.P = w.P;
+      q.W = w.W;
+      q.lam = w.lam;
+      q.logdet2 = w.logdet2;
+      q.st = w.st;
+      q.St = w.St;
+      const NvtxIter nvtx_it(0);
+      FFCA_TRY(launch_fast_persist(p, q, w.sync, (int)tiles, L - 1, I, s));
+      p.v_src = nullptr;
+      l0 = L - 1;
+    }
+    for (int l = l0; l < L; ++l) {
       const NvtxIter nvtx_it(l);
       if (ev) FFCA_TRY(cudaEventRecord(ev[l], s));
       p.update = 1;

@@ -16,6 +16,8 @@
 // per-bin sums are reduced across the CTA's warps in shared memory and
 // written as one partial per (frame chunk, bin). Reduction order is fixed, so
 // results are deterministic and independent of how bins are sharded.
+#include <cstdlib>
+
 #include "ffca_fast2.cuh"  // FFCA_K3T
 
 namespace ffca {
@@ -87,8 +89,44 @@ int bin_window_granularity(int I, int dtype) {
   return t > 32 ? t : 32;
 }
 
+// KP (persistent EM kernel, opt-in: FFCA_FLAG_PERSIST or FFCA_PERSIST=1) applies
+// to complex128 I <= 4 problems of at most FFCA_PERSIST_MAXPTS (default 4 Mi)
+// TF-bins whose tiles * (nchunk + 1) CTAs are resident at once.
+static int64_t env_i64(const char* name, int64_t dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoll(e) : dflt;
+}
+bool fast_persist_env() {
+  static const int on = (int)env_i64("FFCA_PERSIST", 0);
+  return on != 0;
+}
+bool fast_persist_shape(int64_t G, int64_t N, int I, int dtype) {
+  static const int64_t maxpts = env_i64("FFCA_PERSIST_MAXPTS", (int64_t)4 << 20);
+  if (I < 1 || I > 4 || dtype != FFCA_C128 || G * N > maxpts) return false;
+  const int64_t tiles = (G + 31) / 32;
+  return tiles * 3 <= fast_persist_slots(I);
+}
+// KP's chunk plan: one resident wave with room for the tiles' refresher CTAs,
+// the finest chunking of >= FFCA_PERSIST_MINF frames (default 8 per warp)
+bool plan_persist_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames,
+                         int* nchunk) {
+  if (!fast_persist_shape(G, N, I, dtype)) return false;
+  static const int64_t minf = env_i64("FFCA_PERSIST_MINF", 8 * kWarps);
+  const int64_t tiles = (G + 31) / 32;
+  const int64_t ncmax = fast_persist_slots(I) / tiles - 1;
+  for (int64_t nc = ncmax; nc >= 1; --nc) {
+    const int64_t cf = (N + nc - 1) / nc;
+    if (cf < minf && nc > 1) continue;
+    *chunk_frames = cf;
+    *nchunk = (int)((N + cf - 1) / cf);
+    return true;
+  }
+  return false;
+}
+
 void plan_fast_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames,
                       int* nchunk) {
+  if (fast_persist_env() && plan_persist_chunks(G, N, I, dtype, chunk_frames, nchunk)) return;
   if (I >= 5)
     plan_chunks(G, N, fast_par_blocks_per_sm(I, dtype), chunk_frames, nchunk,
                 fast_par_bins_per_cta(), 16);
@@ -112,6 +150,39 @@ cudaError_t launch_fast_em(const FastIterParams& p, int I, int dtype, cudaStream
       return cudaErrorInvalidValue;
   }
 #undef FFCA_CASE2
+}
+
+// ---- KP dispatch (ffca_persist_i<I>.cu) ---------------------------------------
+template <int I>
+int persist_slots();
+template <int I>
+cudaError_t launch_persist(const FastIterParams& fp, const PencilParams& pp, const PersistCtl& ctl,
+                           cudaStream_t s);
+
+int fast_persist_slots(int I) {
+  static int cache[5] = {-1, -1, -1, -1, -1};
+  if (I < 1 || I > 4) return 0;
+  if (cache[I] < 0) {
+    switch (I) {
+      case 1: cache[I] = persist_slots<1>(); break;
+      case 2: cache[I] = persist_slots<2>(); break;
+      case 3: cache[I] = persist_slots<3>(); break;
+      default: cache[I] = persist_slots<4>(); break;
+    }
+  }
+  return cache[I];
+}
+
+cudaError_t launch_fast_persist(const FastIterParams& fp, const PencilParams& pp, int* sync,
+                                int tiles, int iters, int I, cudaStream_t s) {
+  PersistCtl ctl{sync, sync + tiles, sync + 2 * tiles, tiles, fp.nchunk, iters};
+  switch (I) {
+    case 1: return launch_persist<1>(fp, pp, ctl, s);
+    case 2: return launch_persist<2>(fp, pp, ctl, s);
+    case 3: return launch_persist<3>(fp, pp, ctl, s);
+    case 4: return launch_persist<4>(fp, pp, ctl, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 // ---- likelihood bookkeeping ------------------------------------------------

@@ -495,10 +495,18 @@ constexpr int fast2_minb() {
   return MU ? FAST2_MU_MINB : (SmemAcc<I, R, UPDATE, LL, MU>::value ? 4 : FAST2_MINB);
 }
 
+// 16-byte L2 (cache-global) load of a complex128
+__device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
+
+// The pass of one CTA: bin tile `bx` of the launch window, frame chunk `by`.
+// A device function so that the persistent EM kernel (ffca_persist.cuh) runs
+// the same code for every iteration of a resident (tile, chunk). The per-bin
+// state another CTA may have rewritten during the same kernel (P, W, lambda)
+// is read with L2 loads (__ldcg), never through L1.
 template <int I, typename R, int WARPS, int STAGES, bool UPDATE, bool LL, bool MU,
           bool BULK = false>
-__global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>())) fast_em2_kernel(const FastIterParams p) {
-  pdl_release_dependents();
+__device__ __forceinline__ void fast_em2_body(const FastIterParams& p, const unsigned bx,
+                                              const unsigned by) {
   using C = typename CplxOf<R>::type;
   using Slot = RingSlot<I, R>;
   using T = typename Math<R>::T;    // per-point compute type
@@ -512,13 +520,13 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t G = p.G;
-  const int64_t tile0 = p.g0 + (int64_t)blockIdx.x * 32;  // (window edges are tile edges)
+  const int64_t tile0 = p.g0 + (int64_t)bx * 32;  // (window edges are tile edges)
   int64_t g = tile0 + lane;
   const bool active = g < G;
   if (!active) g = G - 1;
   const int64_t m = g / p.F;
   const int64_t f = g - m * p.F;
-  const int64_t n0 = (int64_t)blockIdx.y * p.chunk_frames;
+  const int64_t n0 = (int64_t)by * p.chunk_frames;
   const int64_t n1 = min(p.N, n0 + p.chunk_frames);
   const int64_t NF = p.N * p.F;
   R* vb = (R*)p.v + m * 2 * NF + f;  // no __restrict__: may alias vr (in place)
@@ -677,13 +685,13 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
           const int row = e / I;
           es = ((row - Slot::sw(b) + Slot::Q) % Slot::Q) * I + (e - row * I);
         }
-        sP[es * kTS + b] = Math<R>::c2(p.P[gb * NP + e]);
-        if (MU && p.mu_back) sW[e * kTS + b] = Math<R>::c2(p.W[gb * NP + e]);
+        sP[es * kTS + b] = Math<R>::c2(ldcg2(p.P + gb * NP + e));
+        if (MU && p.mu_back) sW[e * kTS + b] = Math<R>::c2(ldcg2(p.W + gb * NP + e));
       }
     } else {
-      for (int e = warp; e < NP; e += WARPS) sP[e * kTS + lane] = Math<R>::c2(p.P[g * NP + e]);
+      for (int e = warp; e < NP; e += WARPS) sP[e * kTS + lane] = Math<R>::c2(ldcg2(p.P + g * NP + e));
       if (MU && p.mu_back)
-        for (int e = warp; e < NP; e += WARPS) sW[e * kTS + lane] = Math<R>::c2(p.W[g * NP + e]);
+        for (int e = warp; e < NP; e += WARPS) sW[e * kTS + lane] = Math<R>::c2(ldcg2(p.W + g * NP + e));
     }
     __syncthreads();
   };
@@ -778,8 +786,9 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
   T lam[I], il[I];  // il = 1 / (I lam): the 1/I of v1 = tr1 / I folded in
 #pragma unroll
   for (int a = 0; a < I; ++a) {
-    lam[a] = (T)p.lam[g * I + a];
-    il[a] = (T)rcp_nr((double)I * p.lam[g * I + a]);  // (MUFU seed + 2 Newton: ~1 ulp; no IEEE division)
+    const double lam_a = __ldcg(p.lam + g * I + a);
+    lam[a] = (T)lam_a;
+    il[a] = (T)rcp_nr((double)I * lam_a);  // (MUFU seed + 2 Newton: ~1 ulp; no IEEE division)
   }
   const T fl = (T)p.floor[g];
   constexpr T invI = T(1) / I;
@@ -1057,7 +1066,7 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
     // --- cross-warp reduction straight from the shared accumulators ---
     __syncthreads();
     if (warp != 0 || !active) return;
-    double* sp = p.Spart + (size_t)blockIdx.y * 2 * NP * G + g;
+    double* sp = p.Spart + (size_t)by * 2 * NP * G + g;
 #pragma unroll
     for (int e = 0; e < 2 * NP; ++e) {
       double t = accS[e * kAccStride];
@@ -1094,7 +1103,7 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
     }
   }
   if (!active) return;
-  const int64_t c = blockIdx.y;
+  const int64_t c = by;
   if (UPDATE) {
     double* sp = p.Spart + (size_t)c * 2 * NP * G + g;
 #pragma unroll
@@ -1105,6 +1114,13 @@ __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>(
   }
   if (LL) p.llbin[(size_t)c * G + g] = llacc;
   }
+}
+
+template <int I, typename R, int WARPS, int STAGES, bool UPDATE, bool LL, bool MU,
+          bool BULK = false>
+__global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>())) fast_em2_kernel(const FastIterParams p) {
+  pdl_release_dependents();
+  fast_em2_body<I, R, WARPS, STAGES, UPDATE, LL, MU, BULK>(p, blockIdx.x, blockIdx.y);
 }
 
 // TMA bulk-copy frame ring for the complex128 update pass (off: measured

@@ -35,6 +35,9 @@ namespace ffca {
 #ifndef FFCA_K4_XX_RECOMPUTE
 #define FFCA_K4_XX_RECOMPUTE 1  // form the x x^H entries twice instead of holding I^2 registers (config 3 FCA 22.2 -> 22.7 G)
 #endif
+#ifndef FFCA_K4_TR
+#define FFCA_K4_TR 2  // interleaved partial sums per power-update trace (1, 2 or 4; config 3 pass 3.49 / 3.42 / 3.46 ms)
+#endif
 #ifndef FFCA_FCA_MINB
 #define FFCA_FCA_MINB 1  // CTAs per SM the I <= 4 pass is register-budgeted for
 #endif
@@ -270,18 +273,28 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
 #define FFCA_XX(e) xx[e]
 #endif
     // S1, S2 re-read from shared memory (volatile, as for R)
-    double qf1 = 0.0, qf2 = 0.0, tR1 = 0.0, tR2 = 0.0;
+    // (kTr interleaved partial sums per trace: shorter dependent FMA chains)
+    constexpr int kTr = FFCA_K4_TR;
+    double qf1p[kTr], qf2p[kTr], tR1p[kTr], tR2p[kTr];
+#pragma unroll
+    for (int t = 0; t < kTr; ++t) qf1p[t] = qf2p[t] = tR1p[t] = tR2p[t] = 0.0;
 #pragma unroll
     for (int e = 0; e < NP; ++e) {
       const double s1 = lds_reload(sS_addr + (unsigned)(e * 32) * 8u);
       const double s2 = lds_reload(sS_addr + (unsigned)((NP + e) * 32) * 8u);
       const double wgt = e < I ? 1.0 : 2.0;  // compile-time after unrolling
       const double xe = FFCA_XX(e);
-      qf1 = fma(wgt * s1, xe, qf1);
-      qf2 = fma(wgt * s2, xe, qf2);
-      tR1 = fma(wgt * s1, Ri[e], tR1);
-      tR2 = fma(wgt * s2, Ri[e], tR2);
+      qf1p[e % kTr] = fma(wgt * s1, xe, qf1p[e % kTr]);
+      qf2p[e % kTr] = fma(wgt * s2, xe, qf2p[e % kTr]);
+      tR1p[e % kTr] = fma(wgt * s1, Ri[e], tR1p[e % kTr]);
+      tR2p[e % kTr] = fma(wgt * s2, Ri[e], tR2p[e % kTr]);
     }
+    auto fold = [](const double (&t)[kTr]) {
+      if constexpr (kTr == 4) return (t[0] + t[1]) + (t[2] + t[3]);
+      else if constexpr (kTr == 2) return t[0] + t[1];
+      else return t[0];
+    };
+    const double qf1 = fold(qf1p), qf2 = fold(qf2p), tR1 = fold(tR1p), tR2 = fold(tR2p);
     const double vv = v1 * v2;
     const double q1 = (v1 * v1 * qf1 + vv * tR2) * invI;
     const double q2 = (v2 * v2 * qf2 + vv * tR1) * invI;

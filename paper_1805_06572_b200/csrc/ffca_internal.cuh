@@ -142,6 +142,31 @@ struct PencilParams {
 bool pencil_window_capable(int64_t G, int I);
 cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s);
 
+// ---- KP: persistent FastFCA EM kernel (ffca_persist.cuh) ---------------------
+// One cooperative launch that runs `iters` whole iterations (pass + refresh)
+// of a complex128 I <= 4 problem whose tiles * (nchunk + 1) CTAs are resident
+// at once. `sync` = 2 * tiles + 1 zeroed ints (arrival counters, tile
+// generations, abort word). fast_persist_slots: CTAs resident at once (0:
+// not available for this order).
+struct PersistCtl {
+  int* arrive;  // [tiles] chunk CTAs that finished a pass of the tile (cumulative over iterations)
+  int* ready;   // [tiles] iterations whose refresh is complete
+  int* abort;   // [1] a wait timed out
+  int tiles, nchunk;
+  int iters;    // iterations run inside the kernel (numbered 1..iters as the plain loop's p.iter)
+};
+
+int fast_persist_slots(int I);
+// shape test of the KP path (order, dtype, size); a run also needs
+// tiles * (nchunk + 1) <= fast_persist_slots and no likelihood / history / events.
+// KP is opt-in: FFCA_FLAG_PERSIST per run, or FFCA_PERSIST=1 (fast_persist_env)
+bool fast_persist_shape(int64_t G, int64_t N, int I, int dtype);
+bool fast_persist_env();
+bool plan_persist_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames,
+                         int* nchunk);
+cudaError_t launch_fast_persist(const FastIterParams& fp, const PencilParams& pp, int* sync,
+                                int tiles, int iters, int I, cudaStream_t s);
+
 // initial pencil from S0 (M,2,F,I,I): P, W, lam, logdet2 (fast.py:127-130)
 cudaError_t launch_initial_pencil(const double2* S0, double2* P, double2* W, double* lam,
                                   double* logdet2, int64_t G, int64_t F, int I,

@@ -1,0 +1,160 @@
+// KP — persistent FastFCA EM kernel for problems whose whole update-pass grid
+// is resident at once (configs 0 / 1: a few hundred bins). The plain schedule
+// runs two launches per iteration (streaming pass K3, per-bin refresh K1) and
+// on these sizes each is a few microseconds of latency-bound work behind a
+// kernel boundary. Here ONE cooperative launch runs `iters` full iterations
+// (reference fast.py:200-223, the loop body of fastfca_run):
+//
+//   * streaming CTAs, one per (32-bin tile, frame chunk): every iteration
+//     they run K3's pass (fast_em2_body, the same code as the stand-alone
+//     kernel: same chunking, same arithmetic, same partial layout), then
+//     bump the tile's arrival counter;
+//   * one refresher CTA per tile (its warp 0, lane = bin): waits until all
+//     of the tile's chunk CTAs have arrived, runs K1's per-bin refresh
+//     (pencil_update_body) and publishes the tile's iteration number.
+//
+// Tiles never wait for each other: the only synchronisation is per tile,
+// through two words in global memory (release: __threadfence + atomic;
+// acquire: relaxed polling loads + one fence), and the per-bin state crossing CTAs (partials, P,
+// W, lambda) is read from L2 (__ldcg), never through L1. The launch is
+// cooperative only for its co-residency guarantee (a CTA that spins on a
+// tile's flag needs that tile's other CTAs to be running); the waits are
+// bounded (kSpinLimitNs) and report FFCA_ERR_CUDA instead of hanging.
+#pragma once
+
+#include "ffca_fast2.cuh"
+#include "ffca_pencil_body.cuh"
+
+namespace ffca {
+
+constexpr unsigned long long kSpinLimitNs = 4000000000ull;  // 4 s
+
+// Polling load: relaxed at gpu scope (served by L2, no L1 invalidation per
+// poll — an acquire load compiles to the load plus a CCTL.IVALL, which on an
+// SM shared with a refresher warp keeps flushing that warp's L1-resident
+// spill slots). The acquire fence is issued once, after the wait.
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acquire_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// spin until *flag >= target; false when the run was aborted / timed out
+__device__ __forceinline__ bool wait_ge(const int* flag, int target, int* abort) {
+  unsigned spins = 0;
+  unsigned long long t0 = 0;
+  while (ld_relaxed_gpu(flag) < target) {
+    if ((++spins & 255u) == 0) {
+      if (ld_relaxed_gpu(abort)) return false;
+      const unsigned long long t = global_ns();
+      if (t0 == 0) t0 = t;
+      if (t - t0 > kSpinLimitNs) {
+        atomicExch(abort, 1);
+        return false;
+      }
+    }
+  }
+  fence_acquire_gpu();
+  return true;
+}
+
+template <int I>
+struct PersistCfg {
+  static constexpr int WARPS = kWarps;
+  static constexpr int STAGES = fast2_stages<I, double, true, false, false>();
+  using Sm = Fast2Smem<I, double, WARPS, STAGES, false, false, false>;
+};
+
+#ifndef FFCA_PERSIST_MINB
+#define FFCA_PERSIST_MINB 2  // CTAs per SM: the refresher role (K1's per-bin code) needs the
+                             // full register budget (at 3 per SM it spills ~0.7-2.7 KB and
+                             // config 1 drops from 17.2 to 12.9 G)
+#endif
+
+template <int I>
+__global__ void __launch_bounds__(kWarps * 32, FFCA_PERSIST_MINB)
+    fast_persist_kernel(FastIterParams fp, PencilParams pp, const PersistCtl ctl) {
+  using Cfg = PersistCfg<I>;
+  const int nstream = ctl.tiles * ctl.nchunk;
+  if ((int)blockIdx.x < nstream) {
+    // ---- streaming role: tile-major so that a tile's chunks start together
+    const unsigned tile = blockIdx.x % (unsigned)ctl.tiles;
+    const unsigned chunk = blockIdx.x / (unsigned)ctl.tiles;
+    __shared__ int s_ok;
+    for (int l = 0; l < ctl.iters; ++l) {
+      if (l > 0) {
+        if (threadIdx.x < 32) {
+          const bool ok = wait_ge(ctl.ready + tile, l, ctl.abort);
+          if (threadIdx.x == 0) s_ok = ok;
+        }
+        __syncthreads();
+        if (!s_ok) return;
+        fp.v_src = nullptr;
+      }
+      fp.iter = l + 1;
+      fast_em2_body<I, double, Cfg::WARPS, Cfg::STAGES, true, false, false, false>(fp, tile, chunk);
+      __threadfence();   // this thread's v and partial stores, device-wide
+      __syncthreads();   // (also: the body's shared memory is free for the next iteration)
+      if (threadIdx.x == 0) atomicAdd(ctl.arrive + tile, 1);
+    }
+  } else {
+    // ---- refresher role: warp 0 of the CTA, lane = bin of the tile
+    if (threadIdx.x >= 32) return;
+    const int tile = (int)blockIdx.x - nstream;
+    const int64_t g = pp.g0 + (int64_t)tile * 32 + threadIdx.x;
+    const bool active = g < pp.G;
+    for (int l = 0; l < ctl.iters; ++l) {
+      const bool ok = wait_ge(ctl.arrive + tile, ctl.nchunk * (l + 1), ctl.abort);
+      if (!__all_sync(0xffffffffu, ok)) {
+        if (threadIdx.x == 0 && pp.st)
+          report_error(pp.st, l + 1, FFCA_ERR_CUDA, (unsigned long long)tile);
+        return;
+      }
+      pp.iter = l + 1;
+      if (active) pencil_update_body<I, true>(pp, g);
+      __threadfence();  // P, W, lambda, logdet2 of this bin, device-wide
+      __syncwarp();
+      if (threadIdx.x == 0) atomicExch(ctl.ready + tile, l + 1);
+    }
+  }
+}
+
+// CTAs of the persistent kernel that can be resident at once on this device
+template <int I>
+int persist_slots() {
+  using Cfg = PersistCfg<I>;
+  auto kern = fast_persist_kernel<I>;
+  if (ensure_smem<fast_persist_kernel<I>>(Cfg::Sm::BYTES) != cudaSuccess) return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kWarps * 32, Cfg::Sm::BYTES) !=
+      cudaSuccess)
+    return 0;
+  return n * sm_count();
+}
+
+template <int I>
+cudaError_t launch_persist(const FastIterParams& fp, const PencilParams& pp, const PersistCtl& ctl,
+                           cudaStream_t s) {
+  using Cfg = PersistCfg<I>;
+  if (cudaError_t e = ensure_smem<fast_persist_kernel<I>>(Cfg::Sm::BYTES)) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ctl.tiles * ctl.nchunk + ctl.tiles));
+  cfg.blockDim = dim3(kWarps * 32);
+  cfg.dynamicSmemBytes = Cfg::Sm::BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fast_persist_kernel<I>, fp, pp, ctl);
+}
+
+}  // namespace ffca

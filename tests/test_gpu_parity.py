@@ -664,3 +664,67 @@ def test_split_phase_windows_bitwise(I, dtype, M, F, graph):
     assert O.scale_dev(outs[3][1][0], ref.v) <= tol
     assert O.scale_dev(outs[3][2][0], ref.S) <= tol
     assert O.scale_dev(outs[3][0][0], ref.images) <= tol
+
+
+@pytest.mark.parametrize("shape,L", [((2, 90, 40, 2), 6), ((1, 150, 70, 3), 5), ((1, 120, 33, 4), 4),
+                                     ((3, 64, 11, 1), 3)])
+def test_persistent_em_kernel_equals_the_plain_schedule(shape, L):
+    """KP (opt-in): small complex128 runs without likelihood / history / events
+    do their first L - 1 iterations in ONE persistent cooperative launch
+    (streaming and refresher CTAs synchronised per tile through global
+    flags). With equal chunking the arithmetic is the plain schedule's:
+    bitwise equal results; also as a replayed graph, with a separate
+    initial-power buffer, and against the oracle."""
+    import torch
+
+    from paper_1805_06572_b200._engine import run_device
+
+    P = _pkg()
+    M, N, F, I = shape
+    gen = np.random.default_rng(41 + I)
+    Y = torch.from_numpy(random_complex(gen, shape)).cuda()
+    inits = [P.init_random(Y[m], 80 + m) for m in range(M)]
+    V = torch.stack([i.v for i in inits])
+    S = torch.stack([i.S for i in inits])
+    FL = torch.stack([i.v_floor for i in inits])
+    V0 = V.clone()
+    kw = dict(likelihood=False, timing=False, chunk_frames=32)  # (KP's own plan differs)
+    plain = run_device("fast", Y, V, S, FL, L, **kw)
+    kw["persist"] = True
+    kp = run_device("fast", Y, V, S, FL, L, **kw)
+    for k in ("images", "v", "S"):
+        if I == 4:  # the plain schedule refreshes few I = 4 bins with the lane-parallel K1p
+            a, b = getattr(kp, k).cpu().numpy(), getattr(plain, k).cpu().numpy()
+            assert O.scale_dev(a, b) <= 1e-12, k
+        else:
+            assert torch.equal(getattr(kp, k), getattr(plain, k)), k
+    out = {"images": torch.empty_like(plain.images), "S": torch.empty_like(plain.S),
+           "v": torch.empty_like(plain.v)}
+    for _ in range(3):  # captured graph, then replays
+        r = run_device("fast", Y, V, S, FL, L, out=out, graph=True, **kw)
+        out["workspace"] = r.workspace
+        for k in ("images", "v", "S"):
+            assert torch.equal(getattr(r, k), getattr(kp, k)), k
+    assert torch.equal(V, V0)
+    # the oracle on the first mixture
+    y0 = Y[0].cpu().numpy()
+    ref = O.fastfca_run(y0, inits[0].v.cpu().numpy(), inits[0].S.cpu().numpy(),
+                        inits[0].v_floor.cpu().numpy(), L)
+    auto = run_device("fast", Y, V, S, FL, L, likelihood=False, timing=False, persist=True)
+    for r in (kp, auto):  # (auto: KP's own chunk plan)
+        assert O.scale_dev(r.images[0].cpu().numpy(), ref.images) <= TOL
+        assert O.scale_dev(r.v[0].cpu().numpy(), ref.v) <= TOL
+        assert O.scale_dev(r.S[0].cpu().numpy(), ref.S) <= TOL
+
+
+def test_persistent_em_kernel_reports_collapsed_powers():
+    """A silent mixture under KP raises like the plain schedule."""
+    from paper_1805_06572_b200._engine import run_device
+
+    P = _pkg()
+    y = np.zeros((40, 20, 2), dtype=complex)
+    init = P.init_random(y, 1)
+    for persist in (False, True):
+        with pytest.raises(P.SingularMatrixError):
+            run_device("fast", y[None], init.v[None], init.S[None], init.v_floor[None], 4,
+                       likelihood=False, timing=False, persist=persist)
