@@ -35,9 +35,16 @@ namespace ffca {
 #ifndef FFCA_K4_XX_RECOMPUTE
 #define FFCA_K4_XX_RECOMPUTE 1  // form the x x^H entries twice instead of holding I^2 registers (config 3 FCA 22.2 -> 22.7 G)
 #endif
+#ifndef FFCA_K4_LAUNDER
+#define FFCA_K4_LAUNDER 0  // 1: plain shared loads through per-phase laundered addresses
+#endif
 #ifndef FFCA_K4_TR
 #define FFCA_K4_TR 2  // interleaved partial sums per power-update trace (1, 2 or 4; config 3 pass 3.49 / 3.42 / 3.46 ms)
 #endif
+#ifndef FFCA_FCA_WARPS
+#define FFCA_FCA_WARPS 4  // warps per CTA of the I <= 4 FCA pass
+#endif
+constexpr int kFcaWarps = FFCA_FCA_WARPS;
 #ifndef FFCA_FCA_MINB
 #define FFCA_FCA_MINB 1  // CTAs per SM the I <= 4 pass is register-budgeted for
 #endif
@@ -50,8 +57,21 @@ namespace ffca {
 // same address
 __device__ __forceinline__ double lds_reload(unsigned addr) {
   double v;
+#if FFCA_K4_LAUNDER
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));  // (address laundered per phase)
+#else
   asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+#endif
   return v;
+}
+// an address the compiler must treat as new: loads through it are neither
+// hoisted out of the frame loop nor merged with another phase's loads, but
+// stay freely schedulable within their phase
+__device__ __forceinline__ unsigned launder(unsigned a) {
+#if FFCA_K4_LAUNDER
+  asm volatile("" : "+r"(a));
+#endif
+  return a;
 }
 
 template <int I, typename R, int WARPS, bool UPDATE, bool LL, bool MU>
@@ -139,10 +159,11 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
     {
       // (volatile loads: S1, S2 are loop invariant, and plain loads get hoisted
       // out of the frame loop into 2 I^2 registers' worth of spills)
+      const unsigned aR = launder(sS_addr);
 #pragma unroll
       for (int e = 0; e < NP; ++e)
-        Ri[e] = fma(v1, lds_reload(sS_addr + (unsigned)(e * 32) * 8u),
-                    v2 * lds_reload(sS_addr + (unsigned)((NP + e) * 32) * 8u));
+        Ri[e] = fma(v1, lds_reload(aR + (unsigned)(e * 32) * 8u),
+                    v2 * lds_reload(aR + (unsigned)((NP + e) * 32) * 8u));
       const bool ok = herm_sweep_inverse<I>(Ri, detR);
       if (!ok && bad_n == 0) bad_n = n + 1;
     }
@@ -274,14 +295,15 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
 #endif
     // S1, S2 re-read from shared memory (volatile, as for R)
     // (kTr interleaved partial sums per trace: shorter dependent FMA chains)
+    const unsigned aT = launder(sS_addr);
     constexpr int kTr = FFCA_K4_TR;
     double qf1p[kTr], qf2p[kTr], tR1p[kTr], tR2p[kTr];
 #pragma unroll
     for (int t = 0; t < kTr; ++t) qf1p[t] = qf2p[t] = tR1p[t] = tR2p[t] = 0.0;
 #pragma unroll
     for (int e = 0; e < NP; ++e) {
-      const double s1 = lds_reload(sS_addr + (unsigned)(e * 32) * 8u);
-      const double s2 = lds_reload(sS_addr + (unsigned)((NP + e) * 32) * 8u);
+      const double s1 = lds_reload(aT + (unsigned)(e * 32) * 8u);
+      const double s2 = lds_reload(aT + (unsigned)((NP + e) * 32) * 8u);
       const double wgt = e < I ? 1.0 : 2.0;  // compile-time after unrolling
       const double xe = FFCA_XX(e);
       qf1p[e % kTr] = fma(wgt * s1, xe, qf1p[e % kTr]);
@@ -365,18 +387,18 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
 template <int I, typename R>
 constexpr size_t fca_smem_bytes() {
   constexpr size_t NP = (size_t)I * I;
-  constexpr size_t ss = FrameRing<I, R, kWarps, FFCA_FCA_STAGES>::BYTES + 2 * NP * 32 * sizeof(double);
-  constexpr size_t red = (size_t)(kWarps - 1) * (kFcaParts * NP + 1) * 32 * sizeof(double);
+  constexpr size_t ss = FrameRing<I, R, kFcaWarps, FFCA_FCA_STAGES>::BYTES + 2 * NP * 32 * sizeof(double);
+  constexpr size_t red = (size_t)(kFcaWarps - 1) * (kFcaParts * NP + 1) * 32 * sizeof(double);
   return ss > red ? ss : red;
 }
 
 template <int I, typename R, bool UPDATE, bool LL, bool MU>
 static cudaError_t launch_fca_em_v(const FcaIterParams& p, cudaStream_t s) {
   const size_t smem = fca_smem_bytes<I, R>();
-  auto kern = fca_em_kernel<I, R, kWarps, UPDATE, LL, MU>;
-  if (cudaError_t e = ensure_smem<fca_em_kernel<I, R, kWarps, UPDATE, LL, MU>>(smem)) return e;
+  auto kern = fca_em_kernel<I, R, kFcaWarps, UPDATE, LL, MU>;
+  if (cudaError_t e = ensure_smem<fca_em_kernel<I, R, kFcaWarps, UPDATE, LL, MU>>(smem)) return e;
   dim3 grid((unsigned)((p.G + 31) / 32), (unsigned)p.nchunk);
-  kern<<<grid, kWarps * 32, smem, s>>>(p);
+  kern<<<grid, kFcaWarps * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -398,10 +420,10 @@ static cudaError_t launch_fca_em_t(const FcaIterParams& p, cudaStream_t s) {
 template <int I, typename R>
 static int fca_bpsm_t() {
   const size_t smem = fca_smem_bytes<I, R>();
-  auto kern = fca_em_kernel<I, R, kWarps, true, false, false>;
+  auto kern = fca_em_kernel<I, R, kFcaWarps, true, false, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kWarps * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kFcaWarps * 32, smem);
   return n > 0 ? n : 1;
 }
 
