@@ -64,10 +64,13 @@ extern "C" {
                                  * first call with these exact arguments and replay it on
                                  * later identical calls (repeated runs on fixed buffers);
                                  * ignored when iter_events / kernel_events are given */
-#define FFCA_FLAG_PERSIST 16u   /* FastFCA, opt-in: small complex128 runs (no likelihood /
-                                 * history / events) do their first L-1 iterations in ONE
-                                 * persistent cooperative launch (streaming + refresher CTAs,
-                                 * per-tile flags); same arithmetic as the plain schedule */
+#define FFCA_FLAG_PERSIST 16u   /* FastFCA: use the persistent EM kernel whenever the run fits it
+                                 * (complex128, I <= 4, no likelihood / history / events, the
+                                 * whole pass grid resident): the first L-1 iterations in ONE
+                                 * cooperative launch (streaming + refresher CTAs, per-tile
+                                 * flags). Without the flag it is used on the shapes where it
+                                 * measured faster; same arithmetic as the plain schedule */
+#define FFCA_FLAG_NO_PERSIST 32u /* never use the persistent EM kernel */
 
 /* Device-side status word (lives in the run workspace, or caller-allocated
  * for the stage entry points). Zero-initialise with ffca_status_reset. */

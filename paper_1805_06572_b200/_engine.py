@@ -47,7 +47,7 @@ class DeviceRun:
 
 def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, history=False,
                images=True, dtype="c128", timing=True, check=True, out=None, chunk_frames=0,
-               kernel_timing=False, graph=False, bin_parts=0, persist=False):
+               kernel_timing=False, graph=False, bin_parts=0, persist=None):
     """Run ``iterations`` EM passes of FastFCA (``algorithm='fast'``) or
     conventional FCA (``'fca'``) entirely on the current CUDA stream.
 
@@ -60,10 +60,11 @@ def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, hi
     ignored when ``timing`` / ``kernel_timing`` events are requested.
     ``bin_parts`` (FastFCA): bin windows of the split-phase schedule (0 =
     the driver's plan, 1 = none); results do not depend on it.
-    ``persist`` (FastFCA, opt-in): the persistent EM kernel — small complex128
-    runs without likelihood / history / timing events do their first L - 1
+    ``persist`` (FastFCA): the persistent EM kernel — small complex128 runs
+    without likelihood / history / timing events do their first L - 1
     iterations in one cooperative launch (the plain schedule's arithmetic;
-    its own frame chunking unless ``chunk_frames`` is given).
+    its own frame chunking unless ``chunk_frames`` is given). None: on the
+    shapes where it measured faster; True: whenever the run fits; False: never.
     """
     lib = D.require()
     torch = D.torch
@@ -114,8 +115,8 @@ def run_device(algorithm, y, v0, S0, v_floor, iterations, *, likelihood=True, hi
         flags |= _lib.FLAG_IMAGES
     if graph:
         flags |= _lib.FLAG_GRAPH
-    if persist:
-        flags |= _lib.FLAG_PERSIST
+    if persist is not None:
+        flags |= _lib.FLAG_PERSIST if persist else _lib.FLAG_NO_PERSIST
     fast = algorithm == "fast"
     wsz = (lib.ffca_fastfca_workspace_size if fast else lib.ffca_fca_workspace_size)(
         M, N, F, I, L, flags, int(chunk_frames))

@@ -34,6 +34,7 @@ FLAG_HISTORY = 2
 FLAG_IMAGES = 4
 FLAG_GRAPH = 8
 FLAG_PERSIST = 16
+FLAG_NO_PERSIST = 32
 
 c_i64 = ctypes.c_int64
 c_int = ctypes.c_int

@@ -83,8 +83,8 @@ FastWs carve_fast(void* base, int64_t M, int64_t N, int64_t F, int I, int L, uns
   FastWs w{};
   const int64_t G = M * F;
   if (!chunk_override(N, cf_req, &w.chunk_frames, &w.nchunk)) {
-    const bool kp = (flags & FFCA_FLAG_PERSIST) && !(flags & (FFCA_FLAG_LIKELIHOOD | FFCA_FLAG_HISTORY));
-    if (!(kp && plan_persist_chunks(G, N, I, dtype, &w.chunk_frames, &w.nchunk)))
+    if (!(fast_persist_wanted(flags, G, N, I, dtype) &&
+          plan_persist_chunks(G, N, I, dtype, &w.chunk_frames, &w.nchunk)))
       plan_fast_chunks(G, N, I, dtype, &w.chunk_frames, &w.nchunk);
   }
   Carve c(base);
@@ -594,10 +594,9 @@ static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
     // launch (the last pass writes the images: a stand-alone launch)
     int l0 = 0;
     const int64_t tiles = (G + 31) / 32;
-    if (L >= 3 && !ll && !hist && !ev && !kev &&
-        ((fl & FFCA_FLAG_PERSIST) || fast_persist_env()) &&
-        fast_persist_shape(G, N, I, a->dtype) &&
-        tiles * (w.nchunk + 1) <= fast_persist_slots(I)) {
+    if (L >= 3 && !ev && !kev && fast_persist_wanted(fl, G, N, I, a->dtype) &&
+        tiles * (w.nchunk + 1) <= fast_persist_slots(I) &&
+        w.nchunk <= fast_persist_max_chunks(I)) {
       FFCA_TRY(cudaMemsetAsync(w.sync, 0, (2 * tiles + 1) * sizeof(int), s));
       p.update = 1;
       p.mu_out = nullptr;

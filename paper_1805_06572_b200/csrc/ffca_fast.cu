@@ -89,22 +89,41 @@ int bin_window_granularity(int I, int dtype) {
   return t > 32 ? t : 32;
 }
 
-// KP (persistent EM kernel, opt-in: FFCA_FLAG_PERSIST or FFCA_PERSIST=1) applies
+// KP (persistent EM kernel) applies
 // to complex128 I <= 4 problems of at most FFCA_PERSIST_MAXPTS (default 4 Mi)
 // TF-bins whose tiles * (nchunk + 1) CTAs are resident at once.
 static int64_t env_i64(const char* name, int64_t dflt) {
   const char* e = getenv(name);
   return e && *e ? atoll(e) : dflt;
 }
-bool fast_persist_env() {
-  static const int on = (int)env_i64("FFCA_PERSIST", 0);
-  return on != 0;
+// FFCA_PERSIST: 0 never, 1 whenever the shape fits, unset: the measured-win
+// region (fast_persist_auto)
+int fast_persist_env() {
+  static const int v = (int)env_i64("FFCA_PERSIST", -1);
+  return v;
 }
 bool fast_persist_shape(int64_t G, int64_t N, int I, int dtype) {
   static const int64_t maxpts = env_i64("FFCA_PERSIST_MAXPTS", (int64_t)4 << 20);
   if (I < 1 || I > 4 || dtype != FFCA_C128 || G * N > maxpts) return false;
   const int64_t tiles = (G + 31) / 32;
   return tiles * 3 <= fast_persist_slots(I);
+}
+// Shapes on which KP measured faster than the plain schedule
+// (profiles/r02_persist_sweep.jsonl: +2..36%): I <= 3 (at I = 4 the plain
+// schedule's lane-parallel K1p beats the one-thread-per-bin refresher), at
+// most 17 tiles (more leave too few chunks per tile among the 296 resident
+// CTAs) and at least 250k TF-bins (below, the two launches are as cheap).
+bool fast_persist_auto(int64_t G, int64_t N, int I, int dtype) {
+  if (!fast_persist_shape(G, N, I, dtype)) return false;
+  return I <= 3 && (G + 31) / 32 <= 17 && G * N >= 250000;
+}
+// whether a run with these flags takes the KP path (given that its chunking fits)
+bool fast_persist_wanted(unsigned flags, int64_t G, int64_t N, int I, int dtype) {
+  if (flags & (FFCA_FLAG_NO_PERSIST | FFCA_FLAG_LIKELIHOOD | FFCA_FLAG_HISTORY)) return false;
+  const int env = fast_persist_env();
+  if (env == 0) return false;
+  if ((flags & FFCA_FLAG_PERSIST) || env > 0) return fast_persist_shape(G, N, I, dtype);
+  return fast_persist_auto(G, N, I, dtype);
 }
 // KP's chunk plan: one resident wave with room for the tiles' refresher CTAs,
 // the finest chunking of >= FFCA_PERSIST_MINF frames (default 8 per warp)
@@ -113,7 +132,8 @@ bool plan_persist_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_
   if (!fast_persist_shape(G, N, I, dtype)) return false;
   static const int64_t minf = env_i64("FFCA_PERSIST_MINF", 8 * kWarps);
   const int64_t tiles = (G + 31) / 32;
-  const int64_t ncmax = fast_persist_slots(I) / tiles - 1;
+  int64_t ncmax = fast_persist_slots(I) / tiles - 1;
+  if (ncmax > fast_persist_max_chunks(I)) ncmax = fast_persist_max_chunks(I);
   for (int64_t nc = ncmax; nc >= 1; --nc) {
     const int64_t cf = (N + nc - 1) / nc;
     if (cf < minf && nc > 1) continue;
@@ -126,7 +146,9 @@ bool plan_persist_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_
 
 void plan_fast_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames,
                       int* nchunk) {
-  if (fast_persist_env() && plan_persist_chunks(G, N, I, dtype, chunk_frames, nchunk)) return;
+  if (fast_persist_wanted(0, G, N, I, dtype) &&
+      plan_persist_chunks(G, N, I, dtype, chunk_frames, nchunk))
+    return;
   if (I >= 5)
     plan_chunks(G, N, fast_par_blocks_per_sm(I, dtype), chunk_frames, nchunk,
                 fast_par_bins_per_cta(), 16);
@@ -155,6 +177,17 @@ cudaError_t launch_fast_em(const FastIterParams& p, int I, int dtype, cudaStream
 // ---- KP dispatch (ffca_persist_i<I>.cu) ---------------------------------------
 template <int I>
 int persist_slots();
+template <int I>
+int persist_max_chunks();
+int fast_persist_max_chunks(int I) {
+  switch (I) {
+    case 1: return persist_max_chunks<1>();
+    case 2: return persist_max_chunks<2>();
+    case 3: return persist_max_chunks<3>();
+    case 4: return persist_max_chunks<4>();
+    default: return 0;
+  }
+}
 template <int I>
 cudaError_t launch_persist(const FastIterParams& fp, const PencilParams& pp, const PersistCtl& ctl,
                            cudaStream_t s);

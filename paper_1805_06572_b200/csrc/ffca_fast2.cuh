@@ -503,10 +503,18 @@ __device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
 // the same code for every iteration of a resident (tile, chunk). The per-bin
 // state another CTA may have rewritten during the same kernel (P, W, lambda)
 // is read with L2 loads (__ldcg), never through L1.
+struct NoPreTile {  // (stand-alone pass: nothing to wait for)
+  __device__ __forceinline__ bool operator()() const { return true; }
+};
+// `pre` (persistent kernel): called once the frame ring's first stages are in
+// flight and before any per-bin state (P, W, lambda) is read — the wait for
+// the tile's pencil refresh, overlapped with the y / v prefetch; false = the
+// run was aborted (the CTA drains its copies and returns).
 template <int I, typename R, int WARPS, int STAGES, bool UPDATE, bool LL, bool MU,
-          bool BULK = false>
+          bool BULK = false, class PreTile = NoPreTile>
 __device__ __forceinline__ void fast_em2_body(const FastIterParams& p, const unsigned bx,
-                                              const unsigned by) {
+                                              const unsigned by, PreTile pre = PreTile()) {
+  constexpr bool kRingFirst = FFCA_K3_RING_FIRST || !std::is_same<PreTile, NoPreTile>::value;
   using C = typename CplxOf<R>::type;
   using Slot = RingSlot<I, R>;
   using T = typename Math<R>::T;    // per-point compute type
@@ -695,7 +703,19 @@ __device__ __forceinline__ void fast_em2_body(const FastIterParams& p, const uns
     }
     __syncthreads();
   };
-  if (!FFCA_K3_RING_FIRST) load_tile();
+  // lambda (and the floor) are requested before the P tile's copy, so that
+  // the two L2 round trips overlap
+  double lam_g[I];
+  double fl_g = 0.0;
+  auto load_lam = [&]() {
+#pragma unroll
+    for (int a = 0; a < I; ++a) lam_g[a] = __ldcg(p.lam + g * I + a);
+    fl_g = p.floor[g];
+  };
+  if (!kRingFirst) {
+    load_lam();
+    load_tile();
+  }
   constexpr int kAhead = STAGES - 1;  // frames issued ahead
   // ---- TMA bulk ring (BULK): one elected lane per warp issues the copies ----
   // the tile's valid bins and the split into two mixtures (F >= 32: at most
@@ -782,15 +802,21 @@ __device__ __forceinline__ void fast_em2_body(const FastIterParams& p, const uns
       cp_async_commit();
     }
   }
-  if (FFCA_K3_RING_FIRST) load_tile();
+  if (kRingFirst) {
+    if (!pre()) {
+      cp_async_wait_all();
+      return;
+    }
+    load_lam();
+    load_tile();
+  }
   T lam[I], il[I];  // il = 1 / (I lam): the 1/I of v1 = tr1 / I folded in
 #pragma unroll
   for (int a = 0; a < I; ++a) {
-    const double lam_a = __ldcg(p.lam + g * I + a);
-    lam[a] = (T)lam_a;
-    il[a] = (T)rcp_nr((double)I * lam_a);  // (MUFU seed + 2 Newton: ~1 ulp; no IEEE division)
+    lam[a] = (T)lam_g[a];
+    il[a] = (T)rcp_nr((double)I * lam_g[a]);  // (MUFU seed + 2 Newton: ~1 ulp; no IEEE division)
   }
-  const T fl = (T)p.floor[g];
+  const T fl = (T)fl_g;
   constexpr T invI = T(1) / I;
 
   R* vwrite = vb + nfirst * p.F;  // v of the frame being processed (advanced per frame)

@@ -157,11 +157,13 @@ struct PersistCtl {
 };
 
 int fast_persist_slots(int I);
+int fast_persist_max_chunks(int I);  // (the refresher stages the tile's partials in shared memory)
 // shape test of the KP path (order, dtype, size); a run also needs
 // tiles * (nchunk + 1) <= fast_persist_slots and no likelihood / history / events.
-// KP is opt-in: FFCA_FLAG_PERSIST per run, or FFCA_PERSIST=1 (fast_persist_env)
+// fast_persist_wanted: the run's flags (FFCA_FLAG_PERSIST / _NO_PERSIST), the
+// FFCA_PERSIST environment override and the measured-win region decide
 bool fast_persist_shape(int64_t G, int64_t N, int I, int dtype);
-bool fast_persist_env();
+bool fast_persist_wanted(unsigned flags, int64_t G, int64_t N, int I, int dtype);
 bool plan_persist_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames,
                          int* nchunk);
 cudaError_t launch_fast_persist(const FastIterParams& fp, const PencilParams& pp, int* sync,

@@ -3,6 +3,8 @@
 // kernel (ffca_persist.cuh).
 #pragma once
 
+#include <type_traits>
+
 #include "ffca_internal.cuh"
 
 namespace ffca {
@@ -10,12 +12,38 @@ namespace ffca {
 // Steps shared by the fused (I <= 4) and split (I >= 5) pencil updates:
 // chunk partials -> S~ (/N), ridge with eps*gram, model / history covariances,
 // likelihood collect. Leaves S_t in S1/S2 and P_e in Pe.
-template <int I, bool COH = false>
+struct NoPreSum {
+  FFCA_DEV const double* operator()() const { return nullptr; }
+};
+// `pre` (persistent kernel): called after this bin's P and W loads are issued
+// and before the chunk partials are read — the wait for the tile's chunk CTAs.
+// It may return a shared-memory copy of the tile's partials,
+// [chunk][entry][32 bins] (the CTA's warps fetch it in one round trip), which
+// the ordered sums then read instead of global memory.
+template <int I, bool COH = false, class PreSum = NoPreSum>
 FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
-                          double2 (&S2)[I][I], double2 (&Pe)[I][I]) {
+                          double2 (&S2)[I][I], double2 (&Pe)[I][I], PreSum pre = PreSum()) {
   constexpr int NP = I * I;
   const int64_t G = p.G;
   const int64_t m = (unsigned)g / (unsigned)p.F, f = g - m * p.F;  // (32-bit division)
+
+  // the basis of the pass being finished (this bin's P_e, W_e): requested
+  // first, so that their latency overlaps the partials' (or the wait)
+  // (stand-alone the 2 I^2 complex registers are not affordable during the
+  // partial sums: loaded after them)
+  constexpr bool kEarly = !std::is_same<PreSum, NoPreSum>::value;
+  double2 We[I][I];
+  auto load_basis = [&]() {
+#pragma unroll
+    for (int a = 0; a < I; ++a)
+#pragma unroll
+      for (int b = 0; b < I; ++b) {
+        Pe[a][b] = p.P[g * NP + a * I + b];
+        We[a][b] = p.W[g * NP + a * I + b];
+      }
+  };
+  if (kEarly) load_basis();
+  const double* staged = pre();
 
 
   // 1. reduce partials
@@ -26,7 +54,9 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
     // CB chunks per batch: all their loads are issued before the adds, which
     // keep the chunk order (bitwise identical sums)
     // loads in flight per batch: ~64 (I = 4: register bound), ~108 at I = 3
-    constexpr int CB = I == 3 ? 6 : (2 * NP >= 64 ? 1 : (64 / (2 * NP) > 8 ? 8 : 64 / (2 * NP)));
+    // (with the basis already in registers, half the batch at I = 3)
+    constexpr int CB = I == 3 ? (std::is_same<PreSum, NoPreSum>::value ? 6 : 3)
+                              : (2 * NP >= 64 ? 1 : (64 / (2 * NP) > 8 ? 8 : 64 / (2 * NP)));
 #pragma unroll 1
     for (int c0 = 0; c0 < p.nchunk; c0 += CB) {
       double ld[CB][2 * NP];
@@ -36,7 +66,8 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
         const double* sp = p.Spart + (size_t)(c0 + cb) * 2 * NP * G + g;
 #pragma unroll
         for (int e = 0; e < 2 * NP; ++e)
-          ld[cb][e] = COH ? __ldcg(sp + (size_t)e * G) : sp[(size_t)e * G];
+          ld[cb][e] = staged ? staged[((c0 + cb) * 2 * NP + e) * 32 + (threadIdx.x & 31)]
+                             : (COH ? __ldcg(sp + (size_t)e * G) : sp[(size_t)e * G]);
       }
 #pragma unroll
       for (int cb = 0; cb < CB; ++cb) {
@@ -66,14 +97,7 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
     p.llg[g] = (double)p.N * p.logdet2[g] - s;
   }
 
-  double2 We[I][I];
-#pragma unroll
-  for (int a = 0; a < I; ++a)
-#pragma unroll
-    for (int b = 0; b < I; ++b) {
-      Pe[a][b] = p.P[g * NP + a * I + b];
-      We[a][b] = p.W[g * NP + a * I + b];
-    }
+  if (!kEarly) load_basis();
 
   // 2. ridge eps_j = 1e-9 tr(gram^{-1} S~_j)/I with gram^{-1} = W^H W
   //    (W = P^{-H}), then S_t = S~ + eps_j gram (fast.py:80-90).
@@ -141,11 +165,11 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
 // pencil, P <- P Q, W = P^-H, log|det P|^2. COH: the chunk partials were
 // written by other CTAs of the SAME kernel (persistent EM kernel) and are
 // read with L2 loads.
-template <int I, bool COH = false>
-FFCA_DEV void pencil_update_body(const PencilParams& p, const int64_t g) {
+template <int I, bool COH = false, class PreSum = NoPreSum>
+FFCA_DEV void pencil_update_body(const PencilParams& p, const int64_t g, PreSum pre = PreSum()) {
   constexpr int NP = I * I;
   double2 S1[I][I], S2[I][I], Pe[I][I];
-  pencil_prep<I, COH>(p, g, S1, S2, Pe);
+  pencil_prep<I, COH, PreSum>(p, g, S1, S2, Pe, pre);
 
   // 3. GEVD of the transformed pencil, P <- P Q
   double lam[I];

@@ -89,36 +89,53 @@ __global__ void __launch_bounds__(kWarps * 32, FFCA_PERSIST_MINB)
     const unsigned chunk = blockIdx.x / (unsigned)ctl.tiles;
     __shared__ int s_ok;
     for (int l = 0; l < ctl.iters; ++l) {
-      if (l > 0) {
+      fp.iter = l + 1;
+      if (l > 0) fp.v_src = nullptr;
+      // the wait for the tile's refresh of iteration l - 1 runs inside the
+      // pass, after its y / v prefetch is in flight and before P / lambda
+      auto pre = [&]() -> bool {
+        if (l == 0) return true;
         if (threadIdx.x < 32) {
           const bool ok = wait_ge(ctl.ready + tile, l, ctl.abort);
           if (threadIdx.x == 0) s_ok = ok;
         }
         __syncthreads();
-        if (!s_ok) return;
-        fp.v_src = nullptr;
-      }
-      fp.iter = l + 1;
-      fast_em2_body<I, double, Cfg::WARPS, Cfg::STAGES, true, false, false, false>(fp, tile, chunk);
+        return s_ok != 0;
+      };
+      fast_em2_body<I, double, Cfg::WARPS, Cfg::STAGES, true, false, false, false>(fp, tile, chunk,
+                                                                                  pre);
+      if (l > 0 && !s_ok) return;  // aborted inside the pass (CTA-uniform)
       __threadfence();   // this thread's v and partial stores, device-wide
       __syncthreads();   // (also: the body's shared memory is free for the next iteration)
       if (threadIdx.x == 0) atomicAdd(ctl.arrive + tile, 1);
     }
   } else {
-    // ---- refresher role: warp 0 of the CTA, lane = bin of the tile
+    // ---- refresher role: warp 0 of the CTA, lane = bin of the tile.
+    // (Staging the tile's partials in shared memory with all four warps —
+    // every load in flight at once — measured slower: config 1 15.9-17.2 G
+    // against 19.3 G for the one-warp refresher below.)
     if (threadIdx.x >= 32) return;
     const int tile = (int)blockIdx.x - nstream;
     const int64_t g = pp.g0 + (int64_t)tile * 32 + threadIdx.x;
     const bool active = g < pp.G;
     for (int l = 0; l < ctl.iters; ++l) {
-      const bool ok = wait_ge(ctl.arrive + tile, ctl.nchunk * (l + 1), ctl.abort);
+      pp.iter = l + 1;
+      bool ok = true;
+      // the wait for the tile's chunk CTAs runs inside the per-bin code, after
+      // the bin's P / W loads are issued
+      auto pre = [&]() -> const double* {
+        ok = wait_ge(ctl.arrive + tile, ctl.nchunk * (l + 1), ctl.abort);
+        return nullptr;
+      };
+      if (active)
+        pencil_update_body<I, true>(pp, g, pre);
+      else
+        pre();
       if (!__all_sync(0xffffffffu, ok)) {
         if (threadIdx.x == 0 && pp.st)
           report_error(pp.st, l + 1, FFCA_ERR_CUDA, (unsigned long long)tile);
         return;
       }
-      pp.iter = l + 1;
-      if (active) pencil_update_body<I, true>(pp, g);
       __threadfence();  // P, W, lambda, logdet2 of this bin, device-wide
       __syncwarp();
       if (threadIdx.x == 0) atomicExch(ctl.ready + tile, l + 1);
@@ -126,28 +143,41 @@ __global__ void __launch_bounds__(kWarps * 32, FFCA_PERSIST_MINB)
   }
 }
 
+// Dynamic shared memory: the streaming role's ring + tile
+template <int I>
+size_t persist_smem(int) {
+  return PersistCfg<I>::Sm::BYTES;
+}
+template <int I>
+cudaError_t persist_attr() {
+  return ensure_smem<fast_persist_kernel<I>>(PersistCfg<I>::Sm::BYTES);
+}
+
 // CTAs of the persistent kernel that can be resident at once on this device
 template <int I>
 int persist_slots() {
-  using Cfg = PersistCfg<I>;
   auto kern = fast_persist_kernel<I>;
-  if (ensure_smem<fast_persist_kernel<I>>(Cfg::Sm::BYTES) != cudaSuccess) return 0;
+  if (persist_attr<I>() != cudaSuccess) return 0;
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kWarps * 32, Cfg::Sm::BYTES) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kWarps * 32, PersistCfg<I>::Sm::BYTES) !=
       cudaSuccess)
     return 0;
   return n * sm_count();
+}
+template <int I>
+int persist_max_chunks() {
+  return 1 << 20;  // (no per-chunk resource in the kernel)
 }
 
 template <int I>
 cudaError_t launch_persist(const FastIterParams& fp, const PencilParams& pp, const PersistCtl& ctl,
                            cudaStream_t s) {
-  using Cfg = PersistCfg<I>;
-  if (cudaError_t e = ensure_smem<fast_persist_kernel<I>>(Cfg::Sm::BYTES)) return e;
+  if (cudaError_t e = persist_attr<I>()) return e;
+  if (ctl.nchunk > persist_max_chunks<I>()) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(ctl.tiles * ctl.nchunk + ctl.tiles));
   cfg.blockDim = dim3(kWarps * 32);
-  cfg.dynamicSmemBytes = Cfg::Sm::BYTES;
+  cfg.dynamicSmemBytes = persist_smem<I>(ctl.nchunk);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;

@@ -3,6 +3,7 @@
 
 namespace ffca {
 template int persist_slots<1>();
+template int persist_max_chunks<1>();
 template cudaError_t launch_persist<1>(const FastIterParams&, const PencilParams&,
                                        const PersistCtl&, cudaStream_t);
 }  // namespace ffca

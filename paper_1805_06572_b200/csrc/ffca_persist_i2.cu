@@ -3,6 +3,7 @@
 
 namespace ffca {
 template int persist_slots<2>();
+template int persist_max_chunks<2>();
 template cudaError_t launch_persist<2>(const FastIterParams&, const PencilParams&,
                                        const PersistCtl&, cudaStream_t);
 }  // namespace ffca

@@ -689,7 +689,7 @@ def test_persistent_em_kernel_equals_the_plain_schedule(shape, L):
     FL = torch.stack([i.v_floor for i in inits])
     V0 = V.clone()
     kw = dict(likelihood=False, timing=False, chunk_frames=32)  # (KP's own plan differs)
-    plain = run_device("fast", Y, V, S, FL, L, **kw)
+    plain = run_device("fast", Y, V, S, FL, L, persist=False, **kw)
     kw["persist"] = True
     kp = run_device("fast", Y, V, S, FL, L, **kw)
     for k in ("images", "v", "S"):
