@@ -165,8 +165,16 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
 // pencil, P <- P Q, W = P^-H, log|det P|^2. COH: the chunk partials were
 // written by other CTAs of the SAME kernel (persistent EM kernel) and are
 // read with L2 loads.
-template <int I, bool COH = false, class PreSum = NoPreSum>
-FFCA_DEV void pencil_update_body(const PencilParams& p, const int64_t g, PreSum pre = PreSum()) {
+struct NoPublish {
+  FFCA_DEV void operator()() const {}
+};
+// `publish` (persistent kernel): called as soon as the bin's P_next and lambda
+// are stored — all the next update pass reads — so that W = P_next^-H and
+// log|det P|^2 (needed by the NEXT refresh's ridge, the image pass and the
+// likelihood only) are computed while that pass is already streaming.
+template <int I, bool COH = false, class PreSum = NoPreSum, class Publish = NoPublish>
+FFCA_DEV void pencil_update_body(const PencilParams& p, const int64_t g, PreSum pre = PreSum(),
+                                 Publish publish = Publish()) {
   constexpr int NP = I * I;
   double2 S1[I][I], S2[I][I], Pe[I][I];
   pencil_prep<I, COH, PreSum>(p, g, S1, S2, Pe, pre);
@@ -182,18 +190,20 @@ FFCA_DEV void pencil_update_body(const PencilParams& p, const int64_t g, PreSum 
   }
   double2 Pn[I][I];
   matmul<I>(Pe, Q, Pn);
-  double2 Inv[I][I];
-  double lad = 0.0;
-  lu_inverse<I>(Pn, Inv, &lad);
 #pragma unroll
   for (int a = 0; a < I; ++a) {
     p.lam[g * I + a] = lam[a];
 #pragma unroll
-    for (int b = 0; b < I; ++b) {
-      p.P[g * NP + a * I + b] = Pn[a][b];
-      p.W[g * NP + a * I + b] = cconj(Inv[b][a]);
-    }
+    for (int b = 0; b < I; ++b) p.P[g * NP + a * I + b] = Pn[a][b];
   }
+  publish();
+  double2 Inv[I][I];
+  double lad = 0.0;
+  lu_inverse<I>(Pn, Inv, &lad);
+#pragma unroll
+  for (int a = 0; a < I; ++a)
+#pragma unroll
+    for (int b = 0; b < I; ++b) p.W[g * NP + a * I + b] = cconj(Inv[b][a]);
   p.logdet2[g] = 2.0 * lad;
 }
 

@@ -127,18 +127,26 @@ __global__ void __launch_bounds__(kWarps * 32, FFCA_PERSIST_MINB)
         ok = wait_ge(ctl.arrive + tile, ctl.nchunk * (l + 1), ctl.abort);
         return nullptr;
       };
+      // the tile's generation is published once every lane has stored P and
+      // lambda; W and log|det P|^2 follow while the next pass streams (a lane's
+      // own loads of them in the next refresh are in program order; the image
+      // pass reads them after the kernel)
+      auto publish = [&]() {
+        __threadfence();  // P, lambda of this bin, device-wide
+        asm volatile("barrier.sync 2, 32;" ::: "memory");  // (per-thread: inactive lanes arrive below)
+        if (threadIdx.x == 0 && ok) atomicExch(ctl.ready + tile, l + 1);
+      };
       if (active)
-        pencil_update_body<I, true>(pp, g, pre);
-      else
+        pencil_update_body<I, true>(pp, g, pre, publish);
+      else {
         pre();
+        publish();
+      }
       if (!__all_sync(0xffffffffu, ok)) {
         if (threadIdx.x == 0 && pp.st)
           report_error(pp.st, l + 1, FFCA_ERR_CUDA, (unsigned long long)tile);
         return;
       }
-      __threadfence();  // P, W, lambda, logdet2 of this bin, device-wide
-      __syncwarp();
-      if (threadIdx.x == 0) atomicExch(ctl.ready + tile, l + 1);
     }
   }
 }
