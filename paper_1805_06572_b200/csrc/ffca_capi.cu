@@ -595,7 +595,7 @@ static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
     int l0 = 0;
     const int64_t tiles = (G + 31) / 32;
     if (L >= 3 && !ev && !kev && fast_persist_wanted(fl, G, N, I, a->dtype) &&
-        tiles * (w.nchunk + 1) <= fast_persist_slots(I) &&
+        tiles * w.nchunk + persist_refreshers(tiles) <= fast_persist_slots(I) &&
         w.nchunk <= fast_persist_max_chunks(I)) {
       FFCA_TRY(cudaMemsetAsync(w.sync, 0, (2 * tiles + 1) * sizeof(int), s));
       p.update = 1;

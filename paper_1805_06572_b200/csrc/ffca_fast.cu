@@ -132,7 +132,7 @@ bool plan_persist_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_
   if (!fast_persist_shape(G, N, I, dtype)) return false;
   static const int64_t minf = env_i64("FFCA_PERSIST_MINF", 8 * kWarps);
   const int64_t tiles = (G + 31) / 32;
-  int64_t ncmax = fast_persist_slots(I) / tiles - 1;
+  int64_t ncmax = (fast_persist_slots(I) - persist_refreshers(tiles)) / tiles;
   if (ncmax > fast_persist_max_chunks(I)) ncmax = fast_persist_max_chunks(I);
   for (int64_t nc = ncmax; nc >= 1; --nc) {
     const int64_t cf = (N + nc - 1) / nc;

@@ -156,6 +156,12 @@ struct PersistCtl {
   int iters;    // iterations run inside the kernel (numbered 1..iters as the plain loop's p.iter)
 };
 
+#ifndef FFCA_PERSIST_RTILES
+#define FFCA_PERSIST_RTILES 4  // tiles (warps) per refresher CTA of KP, 1..4
+#endif
+inline int64_t persist_refreshers(int64_t tiles) {
+  return (tiles + FFCA_PERSIST_RTILES - 1) / FFCA_PERSIST_RTILES;
+}
 int fast_persist_slots(int I);
 int fast_persist_max_chunks(int I);  // (the refresher stages the tile's partials in shared memory)
 // shape test of the KP path (order, dtype, size); a run also needs

@@ -9,8 +9,8 @@
 //     they run K3's pass (fast_em2_body, the same code as the stand-alone
 //     kernel: same chunking, same arithmetic, same partial layout), then
 //     bump the tile's arrival counter;
-//   * one refresher CTA per tile (its warp 0, lane = bin): waits until all
-//     of the tile's chunk CTAs have arrived, runs K1's per-bin refresh
+//   * one refresher warp per tile (lane = bin; four to a CTA): waits until
+//     all of the tile's chunk CTAs have arrived, runs K1's per-bin refresh
 //     (pencil_update_body) and publishes the tile's iteration number.
 //
 // Tiles never wait for each other: the only synchronisation is per tile,
@@ -114,9 +114,14 @@ __global__ void __launch_bounds__(kWarps * 32, FFCA_PERSIST_MINB)
     // (Staging the tile's partials in shared memory with all four warps —
     // every load in flight at once — measured slower: config 1 15.9-17.2 G
     // against 19.3 G for the one-warp refresher below.)
-    if (threadIdx.x >= 32) return;
-    const int tile = (int)blockIdx.x - nstream;
-    const int64_t g = pp.g0 + (int64_t)tile * 32 + threadIdx.x;
+    // FFCA_PERSIST_RTILES tiles per refresher CTA (one per warp): warps that
+    // run the same ~64 KB of straight-line per-bin code on one SM share its
+    // instruction-cache fills (the stand-alone K1 is instruction-fetch bound)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp >= FFCA_PERSIST_RTILES) return;
+    const int tile = ((int)blockIdx.x - nstream) * FFCA_PERSIST_RTILES + warp;
+    if (tile >= ctl.tiles) return;
+    const int64_t g = pp.g0 + (int64_t)tile * 32 + lane;
     const bool active = g < pp.G;
     for (int l = 0; l < ctl.iters; ++l) {
       pp.iter = l + 1;
@@ -133,8 +138,9 @@ __global__ void __launch_bounds__(kWarps * 32, FFCA_PERSIST_MINB)
       // pass reads them after the kernel)
       auto publish = [&]() {
         __threadfence();  // P, lambda of this bin, device-wide
-        asm volatile("barrier.sync 2, 32;" ::: "memory");  // (per-thread: inactive lanes arrive below)
-        if (threadIdx.x == 0 && ok) atomicExch(ctl.ready + tile, l + 1);
+        // (per-thread barrier of this warp's 32 lanes: inactive lanes arrive below)
+        asm volatile("barrier.sync %0, 32;" ::"r"(2 + warp) : "memory");
+        if (lane == 0 && ok) atomicExch(ctl.ready + tile, l + 1);
       };
       if (active)
         pencil_update_body<I, true>(pp, g, pre, publish);
@@ -143,7 +149,7 @@ __global__ void __launch_bounds__(kWarps * 32, FFCA_PERSIST_MINB)
         publish();
       }
       if (!__all_sync(0xffffffffu, ok)) {
-        if (threadIdx.x == 0 && pp.st)
+        if (lane == 0 && pp.st)
           report_error(pp.st, l + 1, FFCA_ERR_CUDA, (unsigned long long)tile);
         return;
       }
@@ -183,7 +189,7 @@ cudaError_t launch_persist(const FastIterParams& fp, const PencilParams& pp, con
   if (cudaError_t e = persist_attr<I>()) return e;
   if (ctl.nchunk > persist_max_chunks<I>()) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(ctl.tiles * ctl.nchunk + ctl.tiles));
+  cfg.gridDim = dim3((unsigned)(ctl.tiles * ctl.nchunk + (int)persist_refreshers(ctl.tiles)));
   cfg.blockDim = dim3(kWarps * 32);
   cfg.dynamicSmemBytes = persist_smem<I>(ctl.nchunk);
   cfg.stream = s;
