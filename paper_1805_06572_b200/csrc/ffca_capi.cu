@@ -317,6 +317,7 @@ int auto_parts(int64_t M, int64_t F, int64_t N, int I, int dtype) {
   }
   const int64_t G = M * F;
   int k = env > 0 ? env : ((M == 1 && I <= 4 && G * N >= ((int64_t)4 << 20)) ? 3 : 1);
+  if (env <= 0 && fast_par_split_shape(G, N, I)) k = 2;
   const int64_t maxk = G / bin_window_granularity(I, dtype);  // windows of >= one tile
   if (k > maxk) k = (int)(maxk > 1 ? maxk : 1);
   return k < 1 ? 1 : k;
@@ -494,7 +495,9 @@ static int fastfca_split_loop(const ffca_run_args* a, const FastWs& w, FastIterP
       p.g1 = edge[i + 1];
       // passes over different windows are independent: each may start while
       // the previous one (the last pass on the stream) drains
-      p.pdl = (l > 0 || i > 0) && pdl_enabled();
+      // (I >= 5: programmatic launch of the lane-parallel pass over the other
+      // window's tail measured slower, 3.6 vs 5.0 G at config 2)
+      p.pdl = (l > 0 || i > 0) && pdl_enabled() && I <= 4;
       FFCA_TRY_S(launch_fast_em(p, I, a->dtype, s));
       if (kev && i == nw - 1) FFCA_TRY_S(cudaEventRecord(kev[2 * l + 1], s));
       FFCA_TRY_S(cudaEventRecord(pass_done[i], s));

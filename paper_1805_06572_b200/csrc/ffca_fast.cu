@@ -144,11 +144,29 @@ bool plan_persist_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_
   return false;
 }
 
+// I >= 5 problems of a few hundred to a few thousand bins: the lane-parallel
+// refresh K1p is one short latency-bound wave (config 2: 79 of 221 us per
+// iteration), so the driver runs two bin windows, window B's pass overlapping
+// window A's refresh (config 2 FastFCA 4.64 -> 5.3 G; three windows lose).
+// FFCA_PAR_SPLIT=0 turns the rule off.
+bool fast_par_split_shape(int64_t G, int64_t N, int I) {
+  static const int on = (int)env_i64("FFCA_PAR_SPLIT", 1);
+  return on && I >= 5 && G >= 256 && G <= 4096 && G * N >= ((int64_t)1 << 19);
+}
+
 void plan_fast_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames,
                       int* nchunk) {
   if (fast_persist_wanted(0, G, N, I, dtype) &&
       plan_persist_chunks(G, N, I, dtype, chunk_frames, nchunk))
     return;
+  if (I >= 5 && fast_par_split_shape(G, N, I)) {
+    // two bin windows (split-phase schedule): each window's pass should fill
+    // the GPU by itself, with chunks of >= 48 frames (config 2: 41 chunks of
+    // 49 frames; sweep in profiles/r02_split_phase.txt)
+    plan_chunks((G + 1) / 2, N, fast_par_blocks_per_sm(I, dtype), chunk_frames, nchunk,
+                fast_par_bins_per_cta(), 48);
+    return;
+  }
   if (I >= 5)
     plan_chunks(G, N, fast_par_blocks_per_sm(I, dtype), chunk_frames, nchunk,
                 fast_par_bins_per_cta(), 16);

@@ -222,6 +222,8 @@ int fca_blocks_per_sm(int I, int dtype);
 // streams every frame of a chunk in one lane group
 void plan_fca_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames, int* nchunk);
 void plan_fast_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames, int* nchunk);
+// I >= 5: shapes the driver runs as two bin windows (split-phase, no PDL)
+bool fast_par_split_shape(int64_t G, int64_t N, int I);
 
 int sm_count();
 

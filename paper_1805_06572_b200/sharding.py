@@ -132,9 +132,20 @@ MAX_WORLD = 8  # one node of B200s
 def _plan_cost(G, N, I, cf, dtype, algorithm):
     """The drivers' modelled makespan of one streaming pass (ffca_fast.cu
     plan_chunks): waves x (frames per chunk + per-CTA overhead)."""
-    gm = grid_model(G, N, I, cf, dtype, algorithm)
+    k = plan_parts(G, N, I, dtype, algorithm)  # bin windows of the split-phase schedule
+    gm = grid_model(-(-G // k), N, I, cf, dtype, algorithm)
     waves = -(-gm["ctas"] // max(gm["slots"], 1))
-    return waves * (min(cf, N) + 24)
+    return k * waves * (min(cf, N) + 24)
+
+
+def plan_parts(G, N, I, dtype="c128", algorithm="fast"):
+    """Bin windows the FastFCA driver pipelines for G bins (1 = plain schedule)."""
+    from . import _device as D
+    from ._engine import DTYPES
+
+    lib = D.require()
+    return max(1, int(lib.ffca_plan_parts(int(G), int(N), int(I), DTYPES[dtype],
+                                          0 if algorithm == "fast" else 1)))
 
 
 def shard_chunk_frames(M, N, F, I, dtype="c128", algorithm="fast", max_world=MAX_WORLD):
