@@ -132,7 +132,10 @@ MAX_WORLD = 8  # one node of B200s
 def _plan_cost(G, N, I, cf, dtype, algorithm):
     """The drivers' modelled makespan of one streaming pass (ffca_fast.cu
     plan_chunks): waves x (frames per chunk + per-CTA overhead)."""
-    k = plan_parts(G, N, I, dtype, algorithm)  # bin windows of the split-phase schedule
+    # bin windows of the split-phase schedule at I >= 5 (each window's pass has to
+    # fill the GPU by itself; at I <= 4 the windows' passes are chained with
+    # programmatic launch and fill one another's tails: whole-grid model)
+    k = plan_parts(G, N, I, dtype, algorithm) if I >= 5 else 1
     gm = grid_model(-(-G // k), N, I, cf, dtype, algorithm)
     waves = -(-gm["ctas"] // max(gm["slots"], 1))
     return k * waves * (min(cf, N) + 24)
