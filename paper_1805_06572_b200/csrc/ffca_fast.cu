@@ -98,6 +98,10 @@ static int64_t env_i64(const char* name, int64_t dflt) {
 }
 // FFCA_PERSIST: 0 never, 1 whenever the shape fits, unset: the measured-win
 // region (fast_persist_auto)
+bool fast_persist_lar() {
+  static const int v = (int)env_i64("FFCA_PERSIST_LAR", 1);
+  return v != 0;
+}
 int fast_persist_env() {
   static const int v = (int)env_i64("FFCA_PERSIST", -1);
   return v;
@@ -109,13 +113,14 @@ bool fast_persist_shape(int64_t G, int64_t N, int I, int dtype) {
   return tiles * 3 <= fast_persist_slots(I);
 }
 // Shapes on which KP measured faster than the plain schedule
-// (profiles/r02_persist_sweep.jsonl: +2..36%): I <= 3 (at I = 4 the plain
-// schedule's lane-parallel K1p beats the one-thread-per-bin refresher), at
-// most 17 tiles (more leave too few chunks per tile among the 296 resident
-// CTAs) and at least 250k TF-bins (below, the two launches are as cheap).
+// (profiles/r02_persist_sweep_lar.jsonl, 48 shapes): I = 3 up to 33 tiles
+// (+2..31%), I = 2 up to 9 tiles with >= 1000 frames (+6..18%; shorter or
+// wider I = 2 problems tie within 4%). At I = 4 the plain schedule's
+// lane-parallel K1p beats the one-thread-per-bin refresh (KP 0.67-0.92x).
 bool fast_persist_auto(int64_t G, int64_t N, int I, int dtype) {
-  if (!fast_persist_shape(G, N, I, dtype)) return false;
-  return I <= 3 && (G + 31) / 32 <= 17 && G * N >= 250000;
+  if (!fast_persist_shape(G, N, I, dtype) || G * N < 32768) return false;
+  const int64_t tiles = (G + 31) / 32;
+  return (I == 3 && tiles <= 33) || (I == 2 && tiles <= 9 && N >= 1000);
 }
 // whether a run with these flags takes the KP path (given that its chunking fits)
 bool fast_persist_wanted(unsigned flags, int64_t G, int64_t N, int I, int dtype) {
@@ -226,7 +231,8 @@ int fast_persist_slots(int I) {
 
 cudaError_t launch_fast_persist(const FastIterParams& fp, const PencilParams& pp, int* sync,
                                 int tiles, int iters, int I, cudaStream_t s) {
-  PersistCtl ctl{sync, sync + tiles, sync + 2 * tiles, tiles, fp.nchunk, iters};
+  PersistCtl ctl{sync, sync + tiles, sync + 2 * tiles, tiles, fp.nchunk, iters,
+                 fast_persist_lar() ? 1 : 0};
   switch (I) {
     case 1: return launch_persist<1>(fp, pp, ctl, s);
     case 2: return launch_persist<2>(fp, pp, ctl, s);

@@ -38,6 +38,9 @@ namespace ffca {
 #ifndef FFCA_K4_LAUNDER
 #define FFCA_K4_LAUNDER 0  // 1: plain shared loads through per-phase laundered addresses
 #endif
+#ifndef FFCA_K4_STAGED_MU
+#define FFCA_K4_STAGED_MU 0  // 1: image rows stored through the consumed ring stage
+#endif
 #ifndef FFCA_K4_TR
 #define FFCA_K4_TR 2  // interleaved partial sums per power-update trace (1, 2 or 4; config 3 pass 3.49 / 3.42 / 3.46 ms)
 #endif
@@ -127,6 +130,10 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
     return cmk(base[Herm<I>::re(b, a) * 32], -base[Herm<I>::im(b, a) * 32]);
   };
 
+#if FFCA_K4_STAGED_MU
+  ImageRowStore<I, R> img;
+  if constexpr (MU) img.init((int64_t)blockIdx.x * 32, G, p.N, p.F, lane);
+#endif
   double acc[kFcaParts][NP];  // packed Hermitian B1, B2, X1, X2 (see the update block)
 #pragma unroll
   for (int j = 0; j < kFcaParts; ++j)
@@ -240,6 +247,23 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
       // only). Direct lane-strided stores: at 255 registers the staged
       // warp-cooperative store (ImageRowStore, as K3) spilled its addressing
       // and made this pass slower (config 3: 7.0 -> 9.2 ms).
+#if FFCA_K4_STAGED_MU
+      {  // warp-cooperative row stores through the consumed ring stage (as K3)
+        double2 o[2][I];
+#pragma unroll
+        for (int a = 0; a < I; ++a) {
+          double2 s1 = cmk(0.0, 0.0), s2 = cmk(0.0, 0.0);
+#pragma unroll
+          for (int b = 0; b < I; ++b) {
+            s1 = cmac(s1, Sget(0, a, b), x[b]);
+            s2 = cmac(s2, Sget(1, a, b), x[b]);
+          }
+          o[0][a] = cscale(s1, v1);
+          o[1][a] = cscale(s2, v2);
+        }
+        img.store(p.mu_out, ring.cur, n, o);
+      }
+#else
       if (active) {
         C* mo = (C*)p.mu_out;
         C* d1 = mo + (((m * 2 + 0) * p.N + n) * p.F + f) * I;
@@ -256,6 +280,7 @@ __global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const
           d2[a] = from_c128<R>(cscale(s2, v2));
         }
       }
+#endif
     }
     if constexpr (!UPDATE) continue;
     // Phi_j = mu_j mu_j^H + v1 v2 S1 Rinv S2 with mu_j = v_j S_j x, so

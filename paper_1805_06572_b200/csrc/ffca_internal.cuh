@@ -154,13 +154,15 @@ struct PersistCtl {
   int* abort;   // [1] a wait timed out
   int tiles, nchunk;
   int iters;    // iterations run inside the kernel (numbered 1..iters as the plain loop's p.iter)
+  int lar;      // 1: the last chunk CTA of a tile to arrive refreshes it (no refresher CTAs)
 };
 
 #ifndef FFCA_PERSIST_RTILES
 #define FFCA_PERSIST_RTILES 4  // tiles (warps) per refresher CTA of KP, 1..4
 #endif
+bool fast_persist_lar();  // FFCA_PERSIST_LAR (default 1)
 inline int64_t persist_refreshers(int64_t tiles) {
-  return (tiles + FFCA_PERSIST_RTILES - 1) / FFCA_PERSIST_RTILES;
+  return fast_persist_lar() ? 0 : (tiles + FFCA_PERSIST_RTILES - 1) / FFCA_PERSIST_RTILES;
 }
 int fast_persist_slots(int I);
 int fast_persist_max_chunks(int I);  // (the refresher stages the tile's partials in shared memory)

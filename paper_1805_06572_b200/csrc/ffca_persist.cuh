@@ -5,18 +5,21 @@
 // kernel boundary. Here ONE cooperative launch runs `iters` full iterations
 // (reference fast.py:200-223, the loop body of fastfca_run):
 //
-//   * streaming CTAs, one per (32-bin tile, frame chunk): every iteration
-//     they run K3's pass (fast_em2_body, the same code as the stand-alone
+//   * one CTA per (32-bin tile, frame chunk) stays resident: every iteration
+//     it runs K3's pass (fast_em2_body, the same code as the stand-alone
 //     kernel: same chunking, same arithmetic, same partial layout), then
-//     bump the tile's arrival counter;
-//   * one refresher warp per tile (lane = bin; four to a CTA): waits until
-//     all of the tile's chunk CTAs have arrived, runs K1's per-bin refresh
-//     (pencil_update_body) and publishes the tile's iteration number.
+//     takes a ticket on the tile's arrival counter;
+//   * the LAST chunk CTA of a tile to arrive refreshes the tile (LAR): warps
+//     1-3 sum the tile's partials in chunk order into shared memory, warp 0
+//     (lane = bin) runs K1's per-bin refresh (pencil_update_body) on the sums
+//     and publishes the tile's iteration number; the others wait for it.
+//     (FFCA_PERSIST_LAR=0: dedicated refresher warps, one per tile, poll the
+//     arrival counter instead — slower, kept for comparison.)
 //
 // Tiles never wait for each other: the only synchronisation is per tile,
 // through two words in global memory (release: __threadfence + atomic;
-// acquire: relaxed polling loads + one fence), and the per-bin state crossing CTAs (partials, P,
-// W, lambda) is read from L2 (__ldcg), never through L1. The launch is
+// acquire: relaxed polling loads + one fence), and the per-bin state crossing
+// CTAs (partials, P, lambda) is read from L2 (__ldcg), never through L1. The launch is
 // cooperative only for its co-residency guarantee (a CTA that spins on a
 // tile's flag needs that tile's other CTAs to be running); the waits are
 // bounded (kSpinLimitNs) and report FFCA_ERR_CUDA instead of hanging.
@@ -87,7 +90,15 @@ __global__ void __launch_bounds__(kWarps * 32, FFCA_PERSIST_MINB)
     // ---- streaming role: tile-major so that a tile's chunks start together
     const unsigned tile = blockIdx.x % (unsigned)ctl.tiles;
     const unsigned chunk = blockIdx.x / (unsigned)ctl.tiles;
-    __shared__ int s_ok;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ int s_ok, s_ticket;
+    // (LAR) the tile's summed partials, [2 I^2][32 bins], beyond the pass's shared memory
+    extern __shared__ __align__(16) unsigned char kp_smem[];
+    double* stage = (double*)(kp_smem + Cfg::Sm::BYTES);
+    constexpr int NE2 = 2 * I * I;
+    const int64_t g = pp.g0 + (int64_t)tile * 32 + lane;
+    const bool active = g < pp.G;
+    auto cta_barrier = []() { asm volatile("barrier.sync 1, %0;" ::"n"(kWarps * 32) : "memory"); };
     for (int l = 0; l < ctl.iters; ++l) {
       fp.iter = l + 1;
       if (l > 0) fp.v_src = nullptr;
@@ -107,7 +118,79 @@ __global__ void __launch_bounds__(kWarps * 32, FFCA_PERSIST_MINB)
       if (l > 0 && !s_ok) return;  // aborted inside the pass (CTA-uniform)
       __threadfence();   // this thread's v and partial stores, device-wide
       __syncthreads();   // (also: the body's shared memory is free for the next iteration)
-      if (threadIdx.x == 0) atomicAdd(ctl.arrive + tile, 1);
+      if (!ctl.lar) {
+        if (threadIdx.x == 0) atomicAdd(ctl.arrive + tile, 1);
+        continue;
+      }
+      // ---- LAR: the LAST chunk CTA of the tile to arrive refreshes the tile.
+      // Its four warps sum the tile's chunk partials (fixed chunk order, every
+      // load in flight at once) into shared memory, warp 0 runs K1's per-bin
+      // code on the sums and publishes the tile; warps 1-3 go on to the next
+      // pass's prefetch. No refresher CTAs, one flag hop per iteration.
+      if (threadIdx.x == 0) s_ticket = atomicAdd(ctl.arrive + tile, 1);
+      __syncthreads();
+      if (s_ticket != ctl.nchunk * (l + 1) - 1) continue;  // (CTA-uniform)
+      fence_acquire_gpu();  // the other chunk CTAs' partials (released before their arrival)
+      // (warps 1-3 reduce; warp 0 already holds its bins' P / W in registers and only waits)
+      constexpr int RT = (kWarps - 1) * 32;  // reducing threads
+      auto staged = [&]() -> const double* {
+        cta_barrier();  // (per-thread: warp 0's lanes arrive from inside the per-bin code)
+        return stage;
+      };
+      auto reduce = [&]() {
+        const int rt = (int)threadIdx.x - 32;
+        constexpr int PPT = (NE2 * 32 + RT - 1) / RT;  // (entry, bin) pairs per thread
+        constexpr int CB = NE2 >= 18 ? 8 : 16;  // chunks per batch (register budget)
+        double sum[PPT];
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) sum[j] = 0.0;
+#pragma unroll 1
+        for (int c0 = 0; c0 < ctl.nchunk; c0 += CB) {
+          double buf[PPT][CB];
+#pragma unroll
+          for (int j = 0; j < PPT; ++j) {
+            const int idx = rt + RT * j;
+            const int e = idx >> 5, b = idx & 31;
+            int64_t gb = pp.g0 + (int64_t)tile * 32 + b;
+            if (gb >= pp.G) gb = pp.G - 1;
+            const double* sp = pp.Spart + (size_t)e * pp.G + gb;
+#pragma unroll
+            for (int k = 0; k < CB; ++k)
+              buf[j][k] = (idx < NE2 * 32 && c0 + k < ctl.nchunk)
+                              ? __ldcg(sp + (size_t)(c0 + k) * NE2 * pp.G)
+                              : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < PPT; ++j)
+#pragma unroll
+            for (int k = 0; k < CB; ++k)
+              if (c0 + k < ctl.nchunk) sum[j] += buf[j][k];
+        }
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          const int idx = rt + RT * j;
+          if (idx < NE2 * 32) stage[idx] = sum[j];
+        }
+        cta_barrier();
+      };
+      if (warp != 0) {
+        reduce();
+        continue;
+      }
+      PencilParams q = pp;
+      q.iter = l + 1;
+      q.nchunk = 1;  // (the staged sums are one "chunk")
+      auto publish = [&]() {
+        __threadfence();  // P, lambda of this bin, device-wide
+        asm volatile("barrier.sync 2, 32;" ::: "memory");
+        if (lane == 0) atomicExch(ctl.ready + tile, l + 1);
+      };
+      if (active)
+        pencil_update_body<I, true>(q, g, staged, publish);
+      else {
+        staged();
+        publish();
+      }
     }
   } else {
     // ---- refresher role: warp 0 of the CTA, lane = bin of the tile.
@@ -159,12 +242,12 @@ __global__ void __launch_bounds__(kWarps * 32, FFCA_PERSIST_MINB)
 
 // Dynamic shared memory: the streaming role's ring + tile
 template <int I>
-size_t persist_smem(int) {
-  return PersistCfg<I>::Sm::BYTES;
+size_t persist_smem(int) {  // the pass's ring + tile, then LAR's staged sums [2 I^2][32]
+  return PersistCfg<I>::Sm::BYTES + (size_t)2 * I * I * 32 * sizeof(double);
 }
 template <int I>
 cudaError_t persist_attr() {
-  return ensure_smem<fast_persist_kernel<I>>(PersistCfg<I>::Sm::BYTES);
+  return ensure_smem<fast_persist_kernel<I>>(persist_smem<I>(0));
 }
 
 // CTAs of the persistent kernel that can be resident at once on this device
@@ -173,7 +256,7 @@ int persist_slots() {
   auto kern = fast_persist_kernel<I>;
   if (persist_attr<I>() != cudaSuccess) return 0;
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kWarps * 32, PersistCfg<I>::Sm::BYTES) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kWarps * 32, persist_smem<I>(0)) !=
       cudaSuccess)
     return 0;
   return n * sm_count();
@@ -189,7 +272,7 @@ cudaError_t launch_persist(const FastIterParams& fp, const PencilParams& pp, con
   if (cudaError_t e = persist_attr<I>()) return e;
   if (ctl.nchunk > persist_max_chunks<I>()) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(ctl.tiles * ctl.nchunk + (int)persist_refreshers(ctl.tiles)));
+  cfg.gridDim = dim3((unsigned)(ctl.tiles * ctl.nchunk + (ctl.lar ? 0 : (int)persist_refreshers(ctl.tiles))));
   cfg.blockDim = dim3(kWarps * 32);
   cfg.dynamicSmemBytes = persist_smem<I>(ctl.nchunk);
   cfg.stream = s;
