@@ -618,9 +618,17 @@ static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
       q.st = w.st;
       q.St = w.St;
       const NvtxIter nvtx_it(0);
-      FFCA_TRY(launch_fast_persist(p, q, w.sync, (int)tiles, L - 1, I, s));
-      p.v_src = nullptr;
-      l0 = L - 1;
+      // a cooperative launch the device cannot place at once (SMs taken by
+      // another context) is refused up front: fall back to the plain schedule
+      const cudaError_t ke = launch_fast_persist(p, q, w.sync, (int)tiles, L - 1, I, s);
+      if (ke == cudaSuccess) {
+        p.v_src = nullptr;
+        l0 = L - 1;
+      } else if (ke == cudaErrorCooperativeLaunchTooLarge || ke == cudaErrorLaunchOutOfResources) {
+        cudaGetLastError();
+      } else {
+        FFCA_TRY(ke);
+      }
     }
     for (int l = l0; l < L; ++l) {
       const NvtxIter nvtx_it(l);

@@ -44,6 +44,10 @@ namespace ffca {
 #ifndef FFCA_K4_TR
 #define FFCA_K4_TR 2  // interleaved partial sums per power-update trace (1, 2 or 4; config 3 pass 3.49 / 3.42 / 3.46 ms)
 #endif
+#ifndef FFCA_FCA_MINB3_MAXI
+#define FFCA_FCA_MINB3_MAXI 0  // orders up to which the pass is budgeted for 3 CTAs / SM (I <= 3 fits 168
+                               // registers, but config 1 FCA measured 16.6 vs 18.6 G: off)
+#endif
 #ifndef FFCA_FCA_WARPS
 #define FFCA_FCA_WARPS 4  // warps per CTA of the I <= 4 FCA pass
 #endif
@@ -77,8 +81,16 @@ __device__ __forceinline__ unsigned launder(unsigned a) {
   return a;
 }
 
+// CTAs per SM the pass is register-budgeted for (FFCA_FCA_MINB3_MAXI: orders
+// budgeted for 3 CTAs / SM instead; at I = 4 the four packed accumulators need
+// all 255 registers)
+template <int I>
+constexpr int fca_minb() {
+  return I <= FFCA_FCA_MINB3_MAXI ? 3 : FFCA_FCA_MINB;
+}
+
 template <int I, typename R, int WARPS, bool UPDATE, bool LL, bool MU>
-__global__ void __launch_bounds__(WARPS * 32, FFCA_FCA_MINB) fca_em_kernel(const FcaIterParams p) {
+__global__ void __launch_bounds__(WARPS * 32, (fca_minb<I>())) fca_em_kernel(const FcaIterParams p) {
   using C = typename CplxOf<R>::type;
   constexpr int NP = I * I;
   constexpr int NE = kFcaParts * NP + 1;
