@@ -65,7 +65,7 @@ struct FastWs {
   ffca_status_dev* st;
   double2 *P, *W, *St;
   double *lam, *logdet2, *Spart, *llbin, *llg;
-  int* sync;  // KP: 2 * tiles + 1 ints (arrival counters, tile generations, abort word)
+  int* sync;  // KP: 3 * tiles + 1 ints (arrival counters, tile / W generations, abort word)
   int64_t chunk_frames;
   int nchunk;
   size_t bytes;
@@ -94,7 +94,7 @@ FastWs carve_fast(void* base, int64_t M, int64_t N, int64_t F, int I, int L, uns
   w.lam = c.take<double>(G * I);
   w.logdet2 = c.take<double>(G);
   w.Spart = c.take<double>((size_t)w.nchunk * 2 * I * I * G);
-  w.sync = c.take<int>(2 * ((G + 31) / 32) + 1);
+  w.sync = c.take<int>(3 * ((G + 31) / 32) + 1);
   const bool ll = flags & FFCA_FLAG_LIKELIHOOD;
   w.llbin = ll ? c.take<double>((size_t)w.nchunk * G) : nullptr;
   w.llg = ll ? c.take<double>((size_t)(L + 1) * G) : nullptr;
@@ -600,7 +600,7 @@ static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
     if (L >= 3 && !ev && !kev && fast_persist_wanted(fl, G, N, I, a->dtype) &&
         tiles * w.nchunk + persist_refreshers(tiles) <= fast_persist_slots(I) &&
         w.nchunk <= fast_persist_max_chunks(I)) {
-      FFCA_TRY(cudaMemsetAsync(w.sync, 0, (2 * tiles + 1) * sizeof(int), s));
+      FFCA_TRY(cudaMemsetAsync(w.sync, 0, (3 * tiles + 1) * sizeof(int), s));
       p.update = 1;
       p.mu_out = nullptr;
       p.mu_back = 1;

@@ -231,7 +231,7 @@ int fast_persist_slots(int I) {
 
 cudaError_t launch_fast_persist(const FastIterParams& fp, const PencilParams& pp, int* sync,
                                 int tiles, int iters, int I, cudaStream_t s) {
-  PersistCtl ctl{sync, sync + tiles, sync + 2 * tiles, tiles, fp.nchunk, iters,
+  PersistCtl ctl{sync, sync + tiles, sync + 2 * tiles, sync + 3 * tiles, tiles, fp.nchunk, iters,
                  fast_persist_lar() ? 1 : 0};
   switch (I) {
     case 1: return launch_persist<1>(fp, pp, ctl, s);

@@ -145,12 +145,13 @@ cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s);
 // ---- KP: persistent FastFCA EM kernel (ffca_persist.cuh) ---------------------
 // One cooperative launch that runs `iters` whole iterations (pass + refresh)
 // of a complex128 I <= 4 problem whose tiles * (nchunk + 1) CTAs are resident
-// at once. `sync` = 2 * tiles + 1 zeroed ints (arrival counters, tile
-// generations, abort word). fast_persist_slots: CTAs resident at once (0:
+// at once. `sync` = 3 * tiles + 1 zeroed ints (arrival counters, tile
+// generations, W generations, abort word). fast_persist_slots: CTAs resident at once (0:
 // not available for this order).
 struct PersistCtl {
   int* arrive;  // [tiles] chunk CTAs that finished a pass of the tile (cumulative over iterations)
-  int* ready;   // [tiles] iterations whose refresh is complete
+  int* ready;   // [tiles] iterations whose refresh has published P and lambda
+  int* wready;  // [tiles] iterations whose refresh has stored W and log|det P|^2 (LAR)
   int* abort;   // [1] a wait timed out
   int tiles, nchunk;
   int iters;    // iterations run inside the kernel (numbered 1..iters as the plain loop's p.iter)

@@ -75,6 +75,9 @@ struct PersistCfg {
   using Sm = Fast2Smem<I, double, WARPS, STAGES, false, false, false>;
 };
 
+#ifndef FFCA_PERSIST_LAR_EARLY
+#define FFCA_PERSIST_LAR_EARLY 0  // LAR: publish a tile before W is stored (second generation word)
+#endif
 #ifndef FFCA_PERSIST_MINB
 #define FFCA_PERSIST_MINB 2  // CTAs per SM: the refresher role (K1's per-bin code) needs the
                              // full register budget (at 3 per SM it spills ~0.7-2.7 KB and
@@ -116,6 +119,9 @@ __global__ void __launch_bounds__(kWarps * 32, FFCA_PERSIST_MINB)
       fast_em2_body<I, double, Cfg::WARPS, Cfg::STAGES, true, false, false, false>(fp, tile, chunk,
                                                                                   pre);
       if (l > 0 && !s_ok) return;  // aborted inside the pass (CTA-uniform)
+      // (LAR) the tile's W generation, read while the fence below drains: the
+      // acquire fence after the ticket orders the later W loads behind it
+      const int wseen = (ctl.lar && warp == 0) ? ld_relaxed_gpu(ctl.wready + tile) : 0;
       __threadfence();   // this thread's v and partial stores, device-wide
       __syncthreads();   // (also: the body's shared memory is free for the next iteration)
       if (!ctl.lar) {
@@ -180,17 +186,41 @@ __global__ void __launch_bounds__(kWarps * 32, FFCA_PERSIST_MINB)
       PencilParams q = pp;
       q.iter = l + 1;
       q.nchunk = 1;  // (the staged sums are one "chunk")
+#if FFCA_PERSIST_LAR_EARLY
+      // publish after P / lambda, W later under its own generation word (the
+      // tile's next refresh may run on another CTA). Measured no faster: the
+      // refreshing CTA starts its next pass late by the W computation and is
+      // the tile's last arriver again, so the tile's iteration is the same.
       auto publish = [&]() {
         __threadfence();  // P, lambda of this bin, device-wide
         asm volatile("barrier.sync 2, 32;" ::: "memory");
         if (lane == 0) atomicExch(ctl.ready + tile, l + 1);
       };
+      const bool wok = wseen >= l || wait_ge(ctl.wready + tile, l, ctl.abort);
       if (active)
         pencil_update_body<I, true>(q, g, staged, publish);
       else {
         staged();
         publish();
       }
+      __threadfence();  // W, log|det P|^2 of this bin, device-wide
+      asm volatile("barrier.sync 2, 32;" ::: "memory");
+      if (lane == 0) atomicExch(ctl.wready + tile, l + 1);
+      if (!__all_sync(0xffffffffu, wok) && lane == 0 && pp.st)
+        report_error(pp.st, l + 1, FFCA_ERR_CUDA, (unsigned long long)tile);
+#else
+      // the whole per-bin state (P, lambda, W, log|det P|^2) is stored before
+      // the tile is published: the tile's next refresh may run on another CTA
+      // and reads all of it behind this one release
+      (void)wseen;
+      if (active)
+        pencil_update_body<I, true>(q, g, staged);
+      else
+        staged();
+      __threadfence();
+      asm volatile("barrier.sync 2, 32;" ::: "memory");
+      if (lane == 0) atomicExch(ctl.ready + tile, l + 1);
+#endif
     }
   } else {
     // ---- refresher role: warp 0 of the CTA, lane = bin of the tile.
