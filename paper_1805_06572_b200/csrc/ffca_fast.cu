@@ -113,14 +113,15 @@ bool fast_persist_shape(int64_t G, int64_t N, int I, int dtype) {
   return tiles * 3 <= fast_persist_slots(I);
 }
 // Shapes on which KP measured faster than the plain schedule
-// (profiles/r02_persist_sweep_lar.jsonl, 48 shapes): I = 3 up to 33 tiles
-// (+2..31%), I = 2 up to 9 tiles with >= 1000 frames (+6..18%; shorter or
-// wider I = 2 problems tie within 4%). At I = 4 the plain schedule's
-// lane-parallel K1p beats the one-thread-per-bin refresh (KP 0.67-0.92x).
+// (profiles/r02_persist_sweep_lar.jsonl, 48 shapes, each schedule with its own
+// chunk plan): I = 3 up to 33 tiles (+2..37%, one shape -3%), I = 2 up to 9
+// tiles with >= 500k TF-bins (+17..35%; smaller or wider I = 2 problems are
+// within +-6%). At I = 4 the plain schedule's lane-parallel K1p beats the
+// one-thread-per-bin refresh (KP 0.67-0.92x).
 bool fast_persist_auto(int64_t G, int64_t N, int I, int dtype) {
   if (!fast_persist_shape(G, N, I, dtype) || G * N < 32768) return false;
   const int64_t tiles = (G + 31) / 32;
-  return (I == 3 && tiles <= 33) || (I == 2 && tiles <= 9 && N >= 1000);
+  return (I == 3 && tiles <= 33) || (I == 2 && tiles <= 9 && G * N >= 500000);
 }
 // whether a run with these flags takes the KP path (given that its chunking fits)
 bool fast_persist_wanted(unsigned flags, int64_t G, int64_t N, int I, int dtype) {
@@ -161,9 +162,6 @@ bool fast_par_split_shape(int64_t G, int64_t N, int I) {
 
 void plan_fast_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_frames,
                       int* nchunk) {
-  if (fast_persist_wanted(0, G, N, I, dtype) &&
-      plan_persist_chunks(G, N, I, dtype, chunk_frames, nchunk))
-    return;
   if (I >= 5 && fast_par_split_shape(G, N, I)) {
     // two bin windows (split-phase schedule): each window's pass should fill
     // the GPU by itself, with chunks of >= 48 frames (config 2: 41 chunks of
@@ -176,8 +174,12 @@ void plan_fast_chunks(int64_t G, int64_t N, int I, int dtype, int64_t* chunk_fra
     plan_chunks(G, N, fast_par_blocks_per_sm(I, dtype), chunk_frames, nchunk,
                 fast_par_bins_per_cta(), 16);
   else
+    // I <= 3: at most 17 chunks. The one-thread-per-bin refresh K1 reads every
+    // chunk's partials in dependent batches, which the wave model does not
+    // see: on single small mixtures 13-17 chunks beat the slot-filling 26-34
+    // by 8-20% (profiles/r02_chunk_probe.jsonl; config 1 17.4 -> 19.9 G)
     plan_chunks(G, N, fast_update_blocks_per_sm(I, dtype), chunk_frames, nchunk,
-                fast_tile_bins(I, dtype));
+                fast_tile_bins(I, dtype), 8 * kWarps, I <= 3 ? 17 : 0);
 }
 
 cudaError_t launch_fast_em(const FastIterParams& p, int I, int dtype, cudaStream_t s) {
@@ -298,7 +300,7 @@ int sm_count() {
 }
 
 void plan_chunks(int64_t G, int64_t N, int blocks_per_sm, int64_t* chunk_frames, int* nchunk,
-                 int tile_bins, int64_t min_frames) {
+                 int tile_bins, int64_t min_frames, int64_t max_chunks) {
   // Pick the frame chunking that minimises the modelled makespan
   //   waves(tiles * nchunk / resident CTAs) * (frames per chunk + per-CTA overhead)
   // so that the grid does not end on a mostly idle last wave (config 4:
@@ -308,6 +310,7 @@ void plan_chunks(int64_t G, int64_t N, int blocks_per_sm, int64_t* chunk_frames,
   int64_t max_nc = (N + min_frames - 1) / min_frames;
   if (max_nc < 1) max_nc = 1;
   if (max_nc > 4096) max_nc = 4096;
+  if (max_chunks > 0 && max_nc > max_chunks) max_nc = max_chunks;
   constexpr int64_t kOverhead = 24;  // frames-equivalent: P/W load, ring fill, reduction
   int64_t best_cf = N, best_cost = -1;
   for (int64_t nc = 1; nc <= max_nc; ++nc) {

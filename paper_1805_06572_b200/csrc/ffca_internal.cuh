@@ -215,7 +215,7 @@ cudaError_t launch_ll_reduce(const double* llg, int64_t M, int64_t F, int64_t N,
 // chunking of the frame axis so that the grid fills the GPU without a
 // mostly idle last wave; blocks_per_sm = resident CTAs of the streaming kernel
 void plan_chunks(int64_t G, int64_t N, int blocks_per_sm, int64_t* chunk_frames, int* nchunk,
-                 int tile_bins = 32, int64_t min_frames = 8 * kWarps);
+                 int tile_bins = 32, int64_t min_frames = 8 * kWarps, int64_t max_chunks = 0);
 int fast_blocks_per_sm(int I, int dtype);
 // the FastFCA update pass's CTA tile (bins) and resident CTAs per SM
 int fast_tile_bins(int I, int dtype);

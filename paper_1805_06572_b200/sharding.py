@@ -172,6 +172,8 @@ def shard_chunk_frames(M, N, F, I, dtype="c128", algorithm="fast", max_world=MAX
     worlds = sorted({w for w in (1, 2, 4, 8, 16, 32, 64) if w <= max_world} | {max_world})
     min_frames = 16 if I >= 5 else 32
     max_nc = max(1, min(4096, -(-N // min_frames)))
+    if algorithm == "fast" and I <= 3:
+        max_nc = min(max_nc, 17)  # (the per-bin refresh K1 reads every chunk: ffca_fast.cu)
     cands = sorted({-(-N // nc) for nc in range(1, max_nc + 1)}, reverse=True)
     costs = {w: [_plan_cost(shard_bins(w), N, I, cf, dtype, algorithm) for cf in cands]
              for w in worlds}
