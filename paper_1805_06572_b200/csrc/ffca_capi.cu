@@ -630,10 +630,20 @@ static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
         FFCA_TRY(ke);
       }
     }
+    // Plain schedule chained with programmatic dependent launch (I <= 4 pass +
+    // one-thread-per-bin refresh, nothing else on the stream in between): the
+    // next kernel is launched while the current one runs, prefetches what
+    // does not depend on it (the pass: its first y / v frames) and waits
+    // (griddepcontrol.wait) before it reads the other's output; each kernel
+    // releases its dependent only after its own wait, so a pass never
+    // overlaps the previous pass and a refresh never the previous refresh.
+    const bool chain = pdl_chain_enabled() && !hist && !ev && !kev && I <= 4 &&
+                       pencil_thread_kernel(G, I);
     for (int l = l0; l < L; ++l) {
       const NvtxIter nvtx_it(l);
       if (ev) FFCA_TRY(cudaEventRecord(ev[l], s));
       p.update = 1;
+      p.pdl_wait = chain ? 1 : 0;
       const bool last = (l == L - 1);
       p.mu_out = (last && (fl & FFCA_FLAG_IMAGES)) ? a->images : nullptr;
       p.mu_back = 1;
@@ -664,8 +674,10 @@ static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
       q.st = w.st;
       q.iter = l + 1;
       q.St = w.St;
+      q.pdl_wait = chain ? 1 : 0;
       FFCA_TRY(launch_pencil_update(q, I, s));
     }
+    p.pdl_wait = 0;
     if (ev) FFCA_TRY(cudaEventRecord(ev[L], s));
     if (ll) {
       p.update = 0;

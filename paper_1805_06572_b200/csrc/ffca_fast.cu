@@ -98,6 +98,10 @@ static int64_t env_i64(const char* name, int64_t dflt) {
 }
 // FFCA_PERSIST: 0 never, 1 whenever the shape fits, unset: the measured-win
 // region (fast_persist_auto)
+bool pdl_chain_enabled() {
+  static const int v = (int)env_i64("FFCA_PDL_CHAIN", 1);
+  return v != 0;
+}
 bool fast_persist_lar() {
   static const int v = (int)env_i64("FFCA_PERSIST_LAR", 1);
   return v != 0;

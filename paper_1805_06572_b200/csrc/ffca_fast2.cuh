@@ -503,8 +503,20 @@ __device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
 // the same code for every iteration of a resident (tile, chunk). The per-bin
 // state another CTA may have rewritten during the same kernel (P, W, lambda)
 // is read with L2 loads (__ldcg), never through L1.
-struct NoPreTile {  // (stand-alone pass: nothing to wait for)
+struct NoPreTile {  // (nothing to wait for)
   __device__ __forceinline__ bool operator()() const { return true; }
+};
+// stand-alone pass: with `on` (FastIterParams::pdl_wait) wait for the kernel
+// this launch programmatically depends on, then release the next one
+struct PdlGate {
+  bool on;
+  __device__ __forceinline__ bool operator()() const {
+    if (on) {
+      pdl_wait_primary();
+      pdl_release_dependents();
+    }
+    return true;
+  }
 };
 // `pre` (persistent kernel): called once the frame ring's first stages are in
 // flight and before any per-bin state (P, W, lambda) is read — the wait for
@@ -1145,8 +1157,11 @@ __device__ __forceinline__ void fast_em2_body(const FastIterParams& p, const uns
 template <int I, typename R, int WARPS, int STAGES, bool UPDATE, bool LL, bool MU,
           bool BULK = false>
 __global__ void __launch_bounds__(WARPS * 32, (fast2_minb<I, R, UPDATE, LL, MU>())) fast_em2_kernel(const FastIterParams p) {
-  pdl_release_dependents();
-  fast_em2_body<I, R, WARPS, STAGES, UPDATE, LL, MU, BULK>(p, blockIdx.x, blockIdx.y);
+  // (split-phase windows: dependents cover other bins and are released on entry;
+  // chained plain schedule: released inside the pass, after its own wait)
+  if (!p.pdl_wait) pdl_release_dependents();
+  fast_em2_body<I, R, WARPS, STAGES, UPDATE, LL, MU, BULK>(p, blockIdx.x, blockIdx.y,
+                                                          PdlGate{p.pdl_wait != 0});
 }
 
 // TMA bulk-copy frame ring for the complex128 update pass (off: measured
@@ -1177,7 +1192,7 @@ cudaError_t launch_fast2_kern(const FastIterParams& p, cudaStream_t s) {
   if (cudaError_t e = ensure_smem<fast_em2_kernel<I, R, WARPS, STAGES, UPDATE, LL, MU, BULK>>(Sm::BYTES))
     return e;
   dim3 grid((unsigned)((window_end(p.g1, p.G) - p.g0 + 31) / 32), (unsigned)p.nchunk);
-  return launch_ex(kern, grid, dim3(WARPS * 32), Sm::BYTES, s, p.pdl != 0, 0, p);
+  return launch_ex(kern, grid, dim3(WARPS * 32), Sm::BYTES, s, p.pdl != 0 || p.pdl_wait != 0, 0, p);
 }
 
 template <int I, typename R, bool UPDATE, bool LL, bool MU>

@@ -58,6 +58,11 @@ struct FastIterParams {
   // launch with programmatic stream serialisation: this pass may start while
   // the previous kernel on the stream (a pass over OTHER bins) drains
   int pdl;
+  // plain schedule chained with programmatic dependent launch: the pass was
+  // launched while the previous per-bin refresh may still run; it prefetches
+  // its first frames, then waits for that kernel (griddepcontrol.wait) before
+  // it reads P / lambda, and only then releases its own dependent
+  int pdl_wait;
 };
 // every CTA of a streaming pass releases its programmatic dependents on entry:
 // a pass over other bins launched after it with FastIterParams::pdl fills
@@ -65,6 +70,13 @@ struct FastIterParams {
 __device__ __forceinline__ void pdl_release_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// wait until the kernel this one programmatically depends on has completed
+// and its memory is visible (a no-op for a normally launched kernel)
+__device__ __forceinline__ void pdl_wait_primary() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+// whether the plain FastFCA schedule chains its launches (FFCA_PDL_CHAIN=0: off)
+bool pdl_chain_enabled();
 // kernel launch with the optional programmatic-serialisation attribute
 // and an optional scheduling priority (0: the stream's; else a value in the
 // device's stream-priority range, lower = more urgent; kept in graph nodes)
@@ -136,10 +148,14 @@ struct PencilParams {
   double2* St;  // [2][G][I][I] scratch for the split path (I >= 5)
   int64_t g0, g1;  // bin window (g1 = 0: to G), as FastIterParams
   int prio;        // launch priority (0: the stream's), see launch_ex
+  int pdl_wait;    // launched programmatically behind the streaming pass (K1, I <= 4): wait
+                   // for it before the partials are read, then release the next pass
 };
 // whether launch_pencil_update honours a bin window (the 3-kernel I >= 5
 // path, FFCA_K1=thread, does not)
 bool pencil_window_capable(int64_t G, int I);
+// whether the refresh is the one-thread-per-bin K1 (honours PencilParams::pdl_wait)
+bool pencil_thread_kernel(int64_t G, int I);
 cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s);
 
 // ---- KP: persistent FastFCA EM kernel (ffca_persist.cuh) ---------------------

@@ -26,8 +26,13 @@ namespace ffca {
 template <int I>
 __global__ void __launch_bounds__(FFCA_K1_THREADS, FFCA_K1_MINB) pencil_update_kernel(const PencilParams p) {
   const int64_t g = p.g0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= window_end(p.g1, p.G)) return;
-  pencil_update_body<I>(p, g);
+  if (g >= window_end(p.g1, p.G)) {
+    // (griddepcontrol.launch_dependents counts per CTA: a bin-less thread must
+    // not release the next pass before the pass this kernel depends on is done)
+    if (p.pdl_wait) pdl_wait_primary();
+    return;
+  }
+  pencil_update_body<I>(p, g, PdlGateSum{p.pdl_wait != 0});
 }
 
 // split path, step 1: S_t -> scratch [2][G][I][I]
@@ -173,16 +178,20 @@ static bool use_par(int64_t G, int I) {
   return I >= 5 || (I == 4 && G < 16384);
 }
 
+// whether launch_pencil_update takes the one-thread-per-bin kernel (which honours
+// PencilParams::pdl_wait)
+bool pencil_thread_kernel(int64_t G, int I) { return !use_par(G, I) && I <= 4; }
+
 cudaError_t launch_pencil_update(const PencilParams& p, int I, cudaStream_t s) {
   if (use_par(p.G, I)) return launch_pencil_par(p, I, s);
   if (I <= 4) {  // fused single kernel; only instantiated for I <= 4
     constexpr int T = FFCA_K1_THREADS;
     const unsigned nb = nblk(window_end(p.g1, p.G) - p.g0, T);
     switch (I) {
-      case 1: return launch_ex(pencil_update_kernel<1>, dim3(nb), dim3(T), 0, s, false, p.prio, p);
-      case 2: return launch_ex(pencil_update_kernel<2>, dim3(nb), dim3(T), 0, s, false, p.prio, p);
-      case 3: return launch_ex(pencil_update_kernel<3>, dim3(nb), dim3(T), 0, s, false, p.prio, p);
-      default: return launch_ex(pencil_update_kernel<4>, dim3(nb), dim3(T), 0, s, false, p.prio, p);
+      case 1: return launch_ex(pencil_update_kernel<1>, dim3(nb), dim3(T), 0, s, p.pdl_wait != 0, p.prio, p);
+      case 2: return launch_ex(pencil_update_kernel<2>, dim3(nb), dim3(T), 0, s, p.pdl_wait != 0, p.prio, p);
+      case 3: return launch_ex(pencil_update_kernel<3>, dim3(nb), dim3(T), 0, s, p.pdl_wait != 0, p.prio, p);
+      default: return launch_ex(pencil_update_kernel<4>, dim3(nb), dim3(T), 0, s, p.pdl_wait != 0, p.prio, p);
     }
     return cudaGetLastError();
   }

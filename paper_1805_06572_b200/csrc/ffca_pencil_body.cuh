@@ -15,6 +15,18 @@ namespace ffca {
 struct NoPreSum {
   FFCA_DEV const double* operator()() const { return nullptr; }
 };
+// stand-alone refresh launched programmatically behind the streaming pass:
+// wait for it, then release the next pass
+struct PdlGateSum {
+  bool on;
+  FFCA_DEV const double* operator()() const {
+    if (on) {
+      pdl_wait_primary();
+      pdl_release_dependents();
+    }
+    return nullptr;
+  }
+};
 // `pre` (persistent kernel): called after this bin's P and W loads are issued
 // and before the chunk partials are read — the wait for the tile's chunk CTAs.
 // It may return a shared-memory copy of the tile's partials,
@@ -29,9 +41,9 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
 
   // the basis of the pass being finished (this bin's P_e, W_e): requested
   // first, so that their latency overlaps the partials' (or the wait)
-  // (stand-alone the 2 I^2 complex registers are not affordable during the
-  // partial sums: loaded after them)
-  constexpr bool kEarly = !std::is_same<PreSum, NoPreSum>::value;
+  // (stand-alone — also behind a programmatic wait — the 2 I^2 complex registers
+  // are not affordable during the partial sums: loaded after them)
+  constexpr bool kEarly = !std::is_same<PreSum, NoPreSum>::value && !std::is_same<PreSum, PdlGateSum>::value;
   double2 We[I][I];
   auto load_basis = [&]() {
 #pragma unroll
@@ -55,7 +67,7 @@ FFCA_DEV bool pencil_prep(const PencilParams& p, int64_t g, double2 (&S1)[I][I],
     // keep the chunk order (bitwise identical sums)
     // loads in flight per batch: ~64 (I = 4: register bound), ~108 at I = 3
     // (with the basis already in registers, half the batch at I = 3)
-    constexpr int CB = I == 3 ? (std::is_same<PreSum, NoPreSum>::value ? 6 : 3)
+    constexpr int CB = I == 3 ? (kEarly ? 3 : 6)
                               : (2 * NP >= 64 ? 1 : (64 / (2 * NP) > 8 ? 8 : 64 / (2 * NP)));
 #pragma unroll 1
     for (int c0 = 0; c0 < p.nchunk; c0 += CB) {
