@@ -333,6 +333,10 @@ int plan_parts(const ffca_run_args* a) {
   return k < 1 ? 1 : (k > 16 ? 16 : k);
 }
 
+// largest run (TF-bins) whose plain schedule is chained with programmatic
+// dependent launch (see fastfca_enqueue / fca_enqueue)
+constexpr int64_t kPdlChainMaxPoints = 300000;
+
 bool graph_mode(const ffca_run_args* a) {
   return (a->flags & FFCA_FLAG_GRAPH) && !a->iter_events && !a->kernel_events && !debug_sync();
 }
@@ -637,8 +641,10 @@ static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
     // (griddepcontrol.wait) before it reads the other's output; each kernel
     // releases its dependent only after its own wait, so a pass never
     // overlaps the previous pass and a refresh never the previous refresh.
+    // Measured: config 0 (128k TF-bins) 11.1-11.5 -> 13.1 G; no change at config 1
+    // (513k) and above, where the launch latency is a small share: small runs only.
     const bool chain = pdl_chain_enabled() && !hist && !ev && !kev && I <= 4 &&
-                       pencil_thread_kernel(G, I);
+                       G * N <= kPdlChainMaxPoints && pencil_thread_kernel(G, I);
     for (int l = l0; l < L; ++l) {
       const NvtxIter nvtx_it(l);
       if (ev) FFCA_TRY(cudaEventRecord(ev[l], s));
@@ -735,10 +741,16 @@ static int fca_enqueue(const ffca_run_args* a, cudaStream_t s) {
     FFCA_TRY(cudaMemcpyAsync(a->S_out, a->S0, Sslice * sizeof(double2),
                              cudaMemcpyDeviceToDevice, s));
   } else {
+    // plain schedule chained with programmatic dependent launch, as FastFCA's
+    // (I <= 4 pass K4 + lane-parallel finish K4b, nothing else on the stream)
+    // (config 0 9.7 -> 10.3 G; config 1 loses, 18.3 -> 16.3 G: small runs only)
+    const bool chain = pdl_chain_enabled() && !hist && !ev && !kev && I <= 4 &&
+                       G * N <= kPdlChainMaxPoints;
     for (int l = 0; l < L; ++l) {
       const NvtxIter nvtx_it(l);
       if (ev) FFCA_TRY(cudaEventRecord(ev[l], s));
       p.update = 1;
+      p.pdl_wait = chain ? 1 : 0;
       const bool last = (l == L - 1);
       p.mu_out = (last && (fl & FFCA_FLAG_IMAGES)) ? a->images : nullptr;
       p.iter = l + 1;
@@ -759,8 +771,9 @@ static int fca_enqueue(const ffca_run_args* a, cudaStream_t s) {
           w.Spart, w.nchunk, N, G, F, w.Sp, (double2*)a->S_out,
           (hist && a->S_hist) ? (double2*)a->S_hist + (size_t)l * Sslice : nullptr,
           ll ? w.llbin : nullptr, ll ? w.llg + (size_t)l * G : nullptr, I,
-          (l == L - 1) ? nullptr : w.st, l + 1, s));
+          (l == L - 1) ? nullptr : w.st, l + 1, s, chain ? 1 : 0));
     }
+    p.pdl_wait = 0;
     if (ev) FFCA_TRY(cudaEventRecord(ev[L], s));
     if (ll) {
       p.update = 0;

@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(WARPS * 32, (fca_minb<I>())) fca_em_kernel(con
     for (int e = warp; e < 2 * NP; e += WARPS) sS[e * 32 + lane] = p.Sp[(size_t)e * G + g];
     __syncthreads();
   };
-  if (!FFCA_K4_RING_FIRST) load_tile();
+  const bool ring_first = FFCA_K4_RING_FIRST || p.pdl_wait;
+  if (!ring_first) load_tile();
   const int64_t n0 = (int64_t)blockIdx.y * p.chunk_frames;
   const int64_t n1 = min(p.N, n0 + p.chunk_frames);
   const int64_t NF = p.N * p.F;
@@ -131,7 +132,13 @@ __global__ void __launch_bounds__(WARPS * 32, (fca_minb<I>())) fca_em_kernel(con
     if (s < K) ring.issue();
     cp_async_commit();
   }
-  if (FFCA_K4_RING_FIRST) load_tile();  // (S1, S2 after the ring prologue)
+  if (ring_first) {  // (S1, S2 after the ring prologue)
+    if (p.pdl_wait) {  // chained schedule: the finish that wrote S1, S2 may still run
+      pdl_wait_primary();
+      pdl_release_dependents();
+    }
+    load_tile();
+  }
 
   const unsigned sS_addr = (unsigned)__cvta_generic_to_shared(sS + lane);
   auto Sget = [&](int which, int a, int b) -> double2 {
@@ -435,8 +442,7 @@ static cudaError_t launch_fca_em_v(const FcaIterParams& p, cudaStream_t s) {
   auto kern = fca_em_kernel<I, R, kFcaWarps, UPDATE, LL, MU>;
   if (cudaError_t e = ensure_smem<fca_em_kernel<I, R, kFcaWarps, UPDATE, LL, MU>>(smem)) return e;
   dim3 grid((unsigned)((p.G + 31) / 32), (unsigned)p.nchunk);
-  kern<<<grid, kFcaWarps * 32, smem, s>>>(p);
-  return cudaGetLastError();
+  return launch_ex(kern, grid, dim3(kFcaWarps * 32), smem, s, p.pdl_wait != 0, 0, p);
 }
 
 template <int I, typename R>
@@ -524,9 +530,9 @@ cudaError_t launch_fca_prepare(const double2* S, double* Sp, int64_t G, int64_t 
 cudaError_t launch_fca_finish(const double* Spart, int nchunk, int64_t N, int64_t G, int64_t F,
                               double* Sp, double2* S_model, double2* S_hist,
                               const double* llbin, double* llg, int I, ffca_status_dev* st,
-                              int iter, cudaStream_t s) {
+                              int iter, cudaStream_t s, int pdl) {
   return launch_fca_bin_par(Spart, nchunk, N, G, F, Sp, S_model, S_hist, llbin, llg, nullptr,
-                            nullptr, I, st, iter, s);
+                            nullptr, I, st, iter, s, pdl);
 }
 
 cudaError_t launch_fca_sraw(const double* Spart, int nchunk, int64_t N, int64_t G,

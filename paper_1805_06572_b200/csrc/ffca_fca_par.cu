@@ -323,6 +323,11 @@ __global__ void __launch_bounds__(64)
   constexpr int LB = Lay::LB;
   constexpr int LD = Lay::LD;
   constexpr int NS = I / 2 + 1;
+  // chained plain schedule: every thread waits for the streaming pass this
+  // launch may programmatically depend on (a no-op otherwise) before the
+  // CTA releases the next pass (launch_dependents counts per CTA)
+  pdl_wait_primary();
+  pdl_release_dependents();
   extern __shared__ __align__(16) double sm[];
   const int r = threadIdx.x % LB;
   const int grp = threadIdx.x / LB;
@@ -574,24 +579,23 @@ static cudaError_t launch_fca_bin_par_t(const double* Spart, int nchunk, int64_t
                                         int64_t F, double* Sp, double2* S_model,
                                         double2* S_hist, const double* llbin, double* llg,
                                         double2* S_raw, const double2* S_in, ffca_status_dev* st,
-                                        int iter, cudaStream_t s) {
+                                        int iter, cudaStream_t s, int pdl) {
   using Lay = BinParLayout<I>;
   const unsigned nb = (unsigned)((G + Lay::GROUPS - 1) / Lay::GROUPS);
-  fca_bin_par_kernel<I><<<nb, 64, Lay::SMEM, s>>>(Spart, nchunk, N, G, F, Sp, S_model, S_hist,
-                                                  llbin, llg, S_raw, S_in, st, iter);
-  return cudaGetLastError();
+  return launch_ex(fca_bin_par_kernel<I>, dim3(nb), dim3(64), Lay::SMEM, s, pdl != 0, 0, Spart,
+                   nchunk, N, G, F, Sp, S_model, S_hist, llbin, llg, S_raw, S_in, st, iter);
 }
 
 cudaError_t launch_fca_bin_par(const double* Spart, int nchunk, int64_t N, int64_t G, int64_t F,
                                double* Sp, double2* S_model, double2* S_hist,
                                const double* llbin, double* llg, double2* S_raw,
                                const double2* S_in, int I, ffca_status_dev* st, int iter,
-                               cudaStream_t s) {
+                               cudaStream_t s, int pdl) {
   switch (I) {
 #define FFCA_CASE(II)                                                                         \
   case II:                                                                                    \
     return launch_fca_bin_par_t<II>(Spart, nchunk, N, G, F, Sp, S_model, S_hist, llbin, llg, \
-                                    S_raw, S_in, st, iter, s);
+                                    S_raw, S_in, st, iter, s, pdl);
     FFCA_CASE(1)
     FFCA_CASE(2)
     FFCA_CASE(3)

@@ -126,6 +126,9 @@ struct FcaIterParams {
   int nchunk;
   ffca_status_dev* st;
   int iter;
+  // chained plain schedule (as FastIterParams::pdl_wait): prefetch the first
+  // frames, wait for the per-bin finish, release the next finish, load S1 / S2
+  int pdl_wait;
 };
 cudaError_t launch_fca_em(const FcaIterParams& p, int I, int dtype, cudaStream_t s);
 
@@ -211,14 +214,16 @@ cudaError_t launch_fca_bin_par(const double* Spart, int nchunk, int64_t N, int64
                                double* Sp, double2* S_model, double2* S_hist,
                                const double* llbin, double* llg, double2* S_raw,
                                const double2* S_in, int I, ffca_status_dev* st, int iter,
-                               cudaStream_t s);
+                               cudaStream_t s, int pdl = 0);
 // stage API: S_raw (2,G,I,I) = sum_n Phi_j / w_j / N from the chunk partials
 cudaError_t launch_fca_sraw(const double* Spart, int nchunk, int64_t N, int64_t G,
                             const double* Sp, double2* S_raw, int I, cudaStream_t s);
 cudaError_t launch_fca_finish(const double* Spart, int nchunk, int64_t N, int64_t G, int64_t F,
                               double* Sp, double2* S_model, double2* S_hist,
                               const double* llbin, double* llg, int I, ffca_status_dev* st,
-                              int iter, cudaStream_t s);
+                              int iter, cudaStream_t s, int pdl = 0);
+// (pdl: launched programmatically behind the streaming pass, see fca_enqueue; the
+// kernel waits for its primary before anything else, then releases its dependent)
 
 // ---- likelihood bookkeeping -------------------------------------------------
 // llg[g] = coef_logdet * N * logdet2[g] - sum_c llbin[c][g]   (logdet2 may be null)
