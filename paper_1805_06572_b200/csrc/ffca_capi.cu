@@ -335,7 +335,18 @@ int plan_parts(const ffca_run_args* a) {
 
 // largest run (TF-bins) whose plain schedule is chained with programmatic
 // dependent launch (see fastfca_enqueue / fca_enqueue)
-constexpr int64_t kPdlChainMaxPoints = 300000;
+// (measured per shape, profiles/r02_pdl_chain_probe.txt: I = 2 gains 6-12% up to
+// ~600k TF-bins and loses up to 9% at 1-2M; I = 3 gains nothing beyond 300k and
+// loses up to 11% at 1-2M; FFCA_PDL_CHAIN_MAX overrides)
+int64_t pdl_chain_max_points(int I) {
+  static int64_t v = -2;
+  if (v == -2) {
+    const char* e = getenv("FFCA_PDL_CHAIN_MAX");
+    v = (e && *e) ? atoll(e) : -1;
+  }
+  if (v >= 0) return v;
+  return I <= 2 ? 600000 : 300000;
+}
 
 bool graph_mode(const ffca_run_args* a) {
   return (a->flags & FFCA_FLAG_GRAPH) && !a->iter_events && !a->kernel_events && !debug_sync();
@@ -644,7 +655,7 @@ static int fastfca_enqueue(const ffca_run_args* a, cudaStream_t s) {
     // Measured: config 0 (128k TF-bins) 11.1-11.5 -> 13.1 G; no change at config 1
     // (513k) and above, where the launch latency is a small share: small runs only.
     const bool chain = pdl_chain_enabled() && !hist && !ev && !kev && I <= 4 &&
-                       G * N <= kPdlChainMaxPoints && pencil_thread_kernel(G, I);
+                       G * N <= pdl_chain_max_points(I) && pencil_thread_kernel(G, I);
     for (int l = l0; l < L; ++l) {
       const NvtxIter nvtx_it(l);
       if (ev) FFCA_TRY(cudaEventRecord(ev[l], s));
@@ -745,7 +756,7 @@ static int fca_enqueue(const ffca_run_args* a, cudaStream_t s) {
     // (I <= 4 pass K4 + lane-parallel finish K4b, nothing else on the stream)
     // (config 0 9.7 -> 10.3 G; config 1 loses, 18.3 -> 16.3 G: small runs only)
     const bool chain = pdl_chain_enabled() && !hist && !ev && !kev && I <= 4 &&
-                       G * N <= kPdlChainMaxPoints;
+                       G * N <= pdl_chain_max_points(3);  // (measured at config 0 / 1 only)
     for (int l = 0; l < L; ++l) {
       const NvtxIter nvtx_it(l);
       if (ev) FFCA_TRY(cudaEventRecord(ev[l], s));
